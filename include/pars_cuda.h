@@ -1,0 +1,210 @@
+/*
+ * pars_cuda.h — C ABI of the B200-native PARS predictor hot path
+ * (libpars_cuda.so, sm_100a).
+ *
+ * This is the drop-in boundary underneath the reference's C++ predictor and
+ * scheduler API (/root/reference/proj/include/pars/*.hpp). The C++ host shim
+ * (paper_2510_03243_b200/host/*.cpp, compiled against those unmodified
+ * headers) and the Python bindings (paper_2510_03243_b200/_lib.py) both call
+ * only the functions below. Plain pointers and sizes, no C++ or torch types.
+ *
+ * Conventions
+ *   - Every function returns PARS_OK (0) or a negative PARS_ERR_* code; the
+ *     message (verbatim the reference's pars::Error text where one exists) is
+ *     available from pars_last_error() on the calling thread.
+ *   - pars_* functions take HOST buffers (caller-owned) and do the
+ *     host<->device copies themselves; pars_dev_* functions take DEVICE
+ *     pointers plus a cudaStream_t (passed as void*, NULL = the ctx stream)
+ *     and are asynchronous on that stream.
+ *   - A pars_ctx binds one CUDA device and owns its scratch memory; calls on
+ *     one ctx are serialised by an internal mutex (the reference's Scorer is
+ *     called concurrently from OpenMP threads, scorer.cpp:13-21).
+ *   - There is no CPU fallback: without a usable sm_100 device every
+ *     compute entry point fails with PARS_ERR_CUDA.
+ */
+#ifndef PARS_CUDA_H
+#define PARS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARS_OK 0
+#define PARS_ERR_INVALID (-1)     /* contract violation (reference: pars::Error) */
+#define PARS_ERR_CUDA (-2)        /* CUDA runtime / no device */
+#define PARS_ERR_OOM (-3)         /* device or host allocation failed */
+#define PARS_ERR_UNSUPPORTED (-4) /* shape outside the implemented envelope */
+
+/* Arithmetic modes for scoring. */
+#define PARS_MODE_EXACT_F64 0 /* bit-identical to the reference (fp64, sequential
+                                 ascending-index dot, no FMA) */
+#define PARS_MODE_FAST_F32 1  /* fp32 weights/products, tree reduction; within
+                                 1e-5 of sum|w_i v_i| */
+
+typedef struct pars_ctx pars_ctx;
+typedef struct pars_features pars_features; /* device-resident CSR */
+typedef struct pars_workload pars_workload; /* host-resident synthetic prompts */
+
+/* pars::FeatureExtractor (features.hpp:17-25) as a C POD.
+ * kind: 0 HashedText, 1 PrecomputedEmbedding; norm: 0 None, 1 L2. */
+typedef struct {
+  int32_t kind;
+  uint32_t dim;
+  int32_t norm;
+  int32_t n_word;
+  int32_t n_char;
+  int32_t word[8];
+  int32_t chr[8];
+} pars_extractor;
+
+/* ---- library / context ---------------------------------------------- */
+const char* pars_last_error(void);
+const char* pars_version(void);
+int pars_device_count(int* count);
+int pars_ctx_create(int device, pars_ctx** out);
+void pars_ctx_destroy(pars_ctx* ctx);
+int pars_ctx_synchronize(pars_ctx* ctx);
+/* Number of kernel launches this ctx has issued (telemetry for bench.py). */
+uint64_t pars_ctx_launches(const pars_ctx* ctx);
+/* Pinned host memory for fast host<->device copies (optional). */
+int pars_host_alloc(size_t bytes, void** out);
+void pars_host_free(void* p);
+
+/* ---- featurize + score ----------------------------------------------
+ * Replaces Scorer::score_batch / LinearScorer::score(const PromptRecord&)
+ * (scorer.cpp:9-24, :36-42) fused with extract_features' HashedText branch
+ * (features.cpp:62-122): whitespace tokenizer, FNV-1a word/char n-grams,
+ * sign hashing, merge, zero erase, L2, dot in ascending index order, +bias.
+ * text: concatenated prompt bytes; offsets[n+1] (int64, offsets[0] may be
+ * nonzero). weights: dim doubles. */
+int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                    const int64_t* offsets, int64_t n, const double* weights,
+                    double bias, int mode, double* scores);
+int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex,
+                        const char* d_text, const int64_t* d_offsets,
+                        int64_t n, const double* d_weights, double bias,
+                        int mode, double* d_scores, void* stream);
+/* PrecomputedEmbedding branch (features.cpp:67-76): X is n x dim row-major. */
+int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex,
+                          const double* X, int64_t n, const double* weights,
+                          double bias, int mode, double* scores);
+
+/* ---- features (extract_all, features.cpp:124-150) -------------------- */
+int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                 const int64_t* offsets, int64_t n, const double* embeddings,
+                 pars_features** out);
+/* Upload caller FeatureVecs (sorted unique idx per row) as a CSR. */
+int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows,
+                         const int64_t* row_ptr, const uint32_t* idx,
+                         const double* val, pars_features** out);
+int64_t pars_features_rows(const pars_features* f);
+int64_t pars_features_nnz(const pars_features* f);
+/* Copies the CSR back to the host: row_ptr[rows+1], idx[nnz], val[nnz]. */
+int pars_features_download(pars_ctx* ctx, const pars_features* f,
+                           int64_t* row_ptr, uint32_t* idx, double* val);
+void pars_features_free(pars_features* f);
+/* LinearScorer::score(const FeatureVec&) for every row (scorer.cpp:40-42). */
+int pars_features_score(pars_ctx* ctx, const pars_features* f,
+                        const double* weights, double bias, double* scores);
+
+/* ---- pair construction / loss (pairs.hpp, pairs.cpp, train.cpp) ------
+ * build_pairs (pairs.cpp:8-36): seeded sampler; host (the mt19937_64 stream
+ * is sequential), bit-identical to the reference. Returns the pair count
+ * (>0) or a negative error ("no informative pairs"). */
+int64_t pars_build_pairs(const int64_t* lengths, int64_t n, double delta,
+                         uint64_t max_pairs, uint64_t seed, uint32_t* a,
+                         uint32_t* b, int32_t* y, double* rel_diff);
+/* dmin[m] = min{d>=1 : !(relative_length_difference(m, m-d) < delta)}
+ * (INT32_MAX if none) for m in [0, max_len]: the integer form of Eq. 1. */
+int pars_length_gap_table(double delta, int64_t max_len, int32_t* dmin);
+
+/* All-pairs margin ranking loss over unordered pairs i<j:
+ * keep = L_i != L_j && |L_i-L_j| >= dmin[max]; y = sign(L_i-L_j);
+ * hinge = max(0, -y(s_i-s_j) + margin) (pairs.hpp:27-31). Outputs the
+ * integer gradient coefficients c (grad = X^T c, c_a -= y, c_b += y on active
+ * pairs), kept/active counts and the loss sum. */
+int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths,
+                  int64_t n, double delta, double margin, int32_t* coeff,
+                  uint64_t* kept, uint64_t* active, double* loss_sum);
+/* Device form over a slice [tile_begin, tile_end) of the upper-triangle tile
+ * list (tile count from pars_allpairs_tiles); coeff/counters are ACCUMULATED
+ * (int32 c[n]; uint64 counters[2] = kept, active; double loss partials[]
+ * one per tile in the slice, reduced deterministically by the caller or by
+ * pars_dev_allpairs_finish). d_lengths are int32. */
+int64_t pars_allpairs_tiles(int64_t n);
+int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores,
+                      const int32_t* d_lengths, int64_t n, double delta,
+                      double margin, int64_t max_len, int64_t tile_begin,
+                      int64_t tile_end, int32_t* d_coeff,
+                      unsigned long long* d_counters, double* d_loss_partials,
+                      void* stream);
+/* grad[d] = sum_i c_i x_i[d] (fp64) for rows [row_begin,row_end) of f. */
+int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
+                  int64_t row_begin, int64_t row_end, double* d_grad,
+                  void* stream);
+
+/* ---- training (train.cpp:122-216, pairwise objective) ----------------
+ * One SGD epoch over explicit pairs (train.cpp:154-166 with apply
+ * :141-151): bit-identical weights and loss to the reference. w is in/out. */
+int pars_sgd_epoch(pars_ctx* ctx, const pars_features* f, const uint32_t* a,
+                   const uint32_t* b, const int32_t* y, int64_t npairs,
+                   int32_t batch, double lr, double margin, double* w,
+                   double bias, double* epoch_loss, uint64_t* active);
+/* train() for Objective::Pairwise from all-zero weights: extract_all on the
+ * GPU, per-epoch build_pairs with derive_seed(seed, 0x10000+e), SGD epochs.
+ * loss_trace has `epochs` slots. */
+int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex,
+                        const char* text, const int64_t* offsets,
+                        const int64_t* lengths, int64_t n, double delta,
+                        double margin, int32_t epochs, int32_t batch,
+                        double lr, uint64_t seed, uint64_t pairs_per_epoch,
+                        double* w_out, double* bias_out, double* loss_trace);
+
+/* ---- priority ordering (scheduler.cpp:33-60) --------------------------
+ * Full select_batch order: boosted first by tie_rank; the rest ascending by
+ * score then tie_rank; equal keys keep input order (stable LSD radix).
+ * tie_rank = rank of (arrival_time, prompt_id bytes) — see
+ * pars_tie_ranks. order[n] receives indices into the input. */
+int pars_priority_order(pars_ctx* ctx, const double* scores,
+                        const uint8_t* boosted, const uint32_t* tie_rank,
+                        int64_t n, int64_t* order);
+int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores,
+                            const uint8_t* d_boosted,
+                            const uint32_t* d_tie_rank, int64_t n,
+                            uint32_t* d_order, void* stream);
+/* Host helper: dense ranks of (arrival, id) with equal keys sharing a rank.
+ * ids: arena + offsets[n+1] (raw bytes, compared unsigned). */
+int pars_tie_ranks(const double* arrival, const char* ids,
+                   const int64_t* id_offsets, int64_t n, uint32_t* rank);
+
+/* ---- Kendall tau-b counts (metrics.cpp:42-64) -------------------------
+ * counts[5] = {n_c, n_d, n0, n1, n2}; tau_b finished on the host exactly
+ * as finish_tau (metrics.cpp:13-32). Degenerate input -> PARS_ERR_INVALID
+ * with the reference's message. */
+int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y,
+                     int64_t n, uint64_t* counts, double* tau_b);
+
+/* ---- synthetic workloads (host; dataset.cpp:204-297 restated) ----------
+ * synthesize_dataset(n, lognormal(mu, sigma), seed) with the reference's
+ * generator (bit-identical text and lengths); pad_tokens > 0 pads every
+ * prompt with " w<k>" tokens, k = Rng(pad_seed).below(50), to exactly
+ * pad_tokens whitespace tokens. */
+int pars_workload_synthesize(uint64_t n, double mu, double sigma,
+                             uint64_t seed, int64_t pad_tokens,
+                             uint64_t pad_seed, pars_workload** out);
+int64_t pars_workload_count(const pars_workload* w);
+int64_t pars_workload_text_bytes(const pars_workload* w);
+/* Pointers stay valid until pars_workload_free. */
+const char* pars_workload_text(const pars_workload* w);
+const int64_t* pars_workload_offsets(const pars_workload* w);
+const int64_t* pars_workload_output_len(const pars_workload* w);
+const int64_t* pars_workload_prompt_len(const pars_workload* w);
+void pars_workload_free(pars_workload* w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARS_CUDA_H */

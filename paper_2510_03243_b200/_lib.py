@@ -1,0 +1,415 @@
+"""ctypes bindings to libpars_cuda.so (include/pars_cuda.h).
+
+This is the Python face of the B200 hot path; the function names and
+argument meanings mirror the reference's C++ predictor/scheduler API
+(/root/reference/proj/include/pars/*.hpp) so the parity tests read like the
+reference's own tests. There is no CPU fallback: if the shared library is
+missing or no sm_100 device is present, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libpars_cuda.so"
+
+MODE_EXACT = 0  # PARS_MODE_EXACT_F64
+MODE_FAST = 1  # PARS_MODE_FAST_F32
+
+
+class ParsError(RuntimeError):
+    """pars::Error equivalent: carries the library's message verbatim."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class Extractor(C.Structure):
+    """pars::FeatureExtractor (features.hpp:17-25)."""
+
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("dim", C.c_uint32),
+        ("norm", C.c_int32),
+        ("n_word", C.c_int32),
+        ("n_char", C.c_int32),
+        ("word", C.c_int32 * 8),
+        ("chr", C.c_int32 * 8),
+    ]
+
+    @classmethod
+    def make(cls, dim: int = 4096, word: Sequence[int] = (1,), char: Sequence[int] = (3,),
+             norm: str = "l2", kind: str = "hashed") -> "Extractor":
+        e = cls()
+        e.kind = 0 if kind in ("hashed", "hashed_text") else 1
+        e.dim = dim
+        e.norm = 1 if norm == "l2" else 0
+        if len(word) > 8 or len(char) > 8:
+            raise ValueError("at most 8 word / 8 char n-gram orders")
+        e.n_word, e.n_char = len(word), len(char)
+        for i, w in enumerate(word):
+            e.word[i] = w
+        for i, c in enumerate(char):
+            e.chr[i] = c
+        return e
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(str(LIB_PATH))
+    vp, i64, u64, i32, u32, dbl = C.c_void_p, C.c_int64, C.c_uint64, C.c_int32, C.c_uint32, C.c_double
+    sig = {
+        "pars_last_error": (C.c_char_p, []),
+        "pars_version": (C.c_char_p, []),
+        "pars_device_count": (C.c_int, [vp]),
+        "pars_ctx_create": (C.c_int, [C.c_int, vp]),
+        "pars_ctx_destroy": (None, [vp]),
+        "pars_ctx_synchronize": (C.c_int, [vp]),
+        "pars_ctx_launches": (u64, [vp]),
+        "pars_host_alloc": (C.c_int, [C.c_size_t, vp]),
+        "pars_host_free": (None, [vp]),
+        "pars_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
+        "pars_dev_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
+        "pars_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
+        "pars_extract": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
+        "pars_features_upload": (C.c_int, [vp, u32, i64, vp, vp, vp, vp]),
+        "pars_features_rows": (i64, [vp]),
+        "pars_features_nnz": (i64, [vp]),
+        "pars_features_download": (C.c_int, [vp, vp, vp, vp, vp]),
+        "pars_features_free": (None, [vp]),
+        "pars_features_score": (C.c_int, [vp, vp, vp, dbl, vp]),
+        "pars_build_pairs": (i64, [vp, i64, dbl, u64, u64, vp, vp, vp, vp]),
+        "pars_length_gap_table": (C.c_int, [dbl, i64, vp]),
+        "pars_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, vp, vp, vp, vp]),
+        "pars_allpairs_tiles": (i64, [i64]),
+        "pars_dev_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, i64, i64, i64, vp, vp, vp, vp]),
+        "pars_dev_xt_c": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
+        "pars_sgd_epoch": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp]),
+        "pars_train_pairwise": (C.c_int, [vp, vp, vp, vp, vp, i64, dbl, dbl, i32, i32, dbl, u64,
+                                          u64, vp, vp, vp]),
+        "pars_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+        "pars_dev_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
+        "pars_tie_ranks": (C.c_int, [vp, vp, vp, i64, vp]),
+        "pars_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp]),
+        "pars_workload_synthesize": (C.c_int, [u64, dbl, dbl, u64, i64, u64, vp]),
+        "pars_workload_count": (i64, [vp]),
+        "pars_workload_text_bytes": (i64, [vp]),
+        "pars_workload_text": (vp, [vp]),
+        "pars_workload_offsets": (vp, [vp]),
+        "pars_workload_output_len": (vp, [vp]),
+        "pars_workload_prompt_len": (vp, [vp]),
+        "pars_workload_free": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+_L: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    global _L
+    if _L is None:
+        _L = _load()
+    return _L
+
+
+def _err(code: int) -> ParsError:
+    return ParsError(code, lib().pars_last_error().decode(errors="replace"))
+
+
+def _check(rc: int):
+    if rc < 0:
+        raise _err(rc)
+    return rc
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    rc = lib().pars_device_count(C.byref(n))
+    return n.value if rc == 0 else 0
+
+
+# ---- host-side helpers (sequential by construction) --------------------------
+
+def build_pairs(lengths, delta: float, max_pairs: int, seed: int):
+    """build_pairs (pairs.cpp:8-36): returns (a, b, y, rel_diff)."""
+    lens = _c(lengths, np.int64)
+    a = np.zeros(max_pairs, np.uint32)
+    b = np.zeros(max_pairs, np.uint32)
+    y = np.zeros(max_pairs, np.int32)
+    rel = np.zeros(max_pairs, np.float64)
+    n = lib().pars_build_pairs(_p(lens), len(lens), delta, max_pairs, seed, _p(a), _p(b), _p(y), _p(rel))
+    _check(n)
+    return a[:n].copy(), b[:n].copy(), y[:n].copy(), rel[:n].copy()
+
+
+def length_gap_table(delta: float, max_len: int) -> np.ndarray:
+    t = np.zeros(max_len + 1, np.int32)
+    _check(lib().pars_length_gap_table(delta, max_len, _p(t)))
+    return t
+
+
+def ids_arena(ids):
+    bs = [i.encode() if isinstance(i, str) else bytes(i) for i in ids]
+    offs = np.zeros(len(bs) + 1, np.int64)
+    offs[1:] = np.cumsum([len(b) for b in bs])
+    return np.frombuffer(b"".join(bs) + b"\0", np.uint8).copy(), offs
+
+
+def tie_ranks(arrival, ids) -> np.ndarray:
+    arena, offs = ids_arena(ids)
+    arr = _c(arrival, np.float64)
+    r = np.zeros(len(arr), np.uint32)
+    _check(lib().pars_tie_ranks(_p(arr), _p(arena), _p(offs), len(arr), _p(r)))
+    return r
+
+
+@dataclass
+class Workload:
+    """Synthetic prompts (dataset.cpp:204-297 restated on the host)."""
+
+    text: np.ndarray  # uint8 view of the (pinned) arena
+    offsets: np.ndarray
+    output_len: np.ndarray
+    prompt_len: np.ndarray
+    _h: int = 0
+
+    @classmethod
+    def synthesize(cls, n: int, seed: int, mu: float = 5.0, sigma: float = 1.2,
+                   pad_tokens: int = 0, pad_seed: int = 5) -> "Workload":
+        L = lib()
+        h = C.c_void_p()
+        _check(L.pars_workload_synthesize(n, mu, sigma, seed, pad_tokens, pad_seed, C.byref(h)))
+        cnt = L.pars_workload_count(h)
+        nb = L.pars_workload_text_bytes(h)
+        text = np.ctypeslib.as_array(C.cast(L.pars_workload_text(h), C.POINTER(C.c_uint8)),
+                                     shape=(max(nb, 1),))[:nb]
+        offs = np.ctypeslib.as_array(C.cast(L.pars_workload_offsets(h), C.POINTER(C.c_int64)),
+                                     shape=(cnt + 1,)).copy()
+        ol = np.ctypeslib.as_array(C.cast(L.pars_workload_output_len(h), C.POINTER(C.c_int64)),
+                                   shape=(cnt,)).copy()
+        pl = np.ctypeslib.as_array(C.cast(L.pars_workload_prompt_len(h), C.POINTER(C.c_int64)),
+                                   shape=(cnt,)).copy()
+        return cls(text, offs, ol, pl, h.value)
+
+    def __len__(self):
+        return len(self.output_len)
+
+    def prompt(self, i) -> bytes:
+        return self.text[self.offsets[i]:self.offsets[i + 1]].tobytes()
+
+    def close(self):
+        if self._h:
+            lib().pars_workload_free(C.c_void_p(self._h))
+            self._h = 0
+            self.text = np.zeros(0, np.uint8)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pack_texts(texts: Sequence[bytes]):
+    """Concatenate prompt strings into (arena uint8, offsets int64[n+1])."""
+    bs = [t.encode() if isinstance(t, str) else bytes(t) for t in texts]
+    offs = np.zeros(len(bs) + 1, np.int64)
+    offs[1:] = np.cumsum([len(b) for b in bs])
+    arena = np.frombuffer(b"".join(bs), np.uint8).copy() if bs else np.zeros(0, np.uint8)
+    if arena.size == 0:
+        arena = np.zeros(1, np.uint8)
+    return arena, offs
+
+
+class Features:
+    """Device-resident CSR produced by extract_all (pars_features*)."""
+
+    def __init__(self, ctx: "Context", handle: int, dim: int):
+        self.ctx, self.h, self.dim = ctx, handle, dim
+
+    @property
+    def rows(self) -> int:
+        return lib().pars_features_rows(C.c_void_p(self.h))
+
+    @property
+    def nnz(self) -> int:
+        return lib().pars_features_nnz(C.c_void_p(self.h))
+
+    def download(self):
+        rows, nnz = self.rows, self.nnz
+        rp = np.zeros(rows + 1, np.int64)
+        idx = np.zeros(max(nnz, 1), np.uint32)
+        val = np.zeros(max(nnz, 1), np.float64)
+        _check(lib().pars_features_download(self.ctx.h, C.c_void_p(self.h), _p(rp), _p(idx), _p(val)))
+        return rp, idx[:nnz], val[:nnz]
+
+    def score(self, weights, bias: float = 0.0) -> np.ndarray:
+        out = np.zeros(self.rows, np.float64)
+        _check(lib().pars_features_score(self.ctx.h, C.c_void_p(self.h), _p(_c(weights, np.float64)),
+                                         bias, _p(out)))
+        return out
+
+    def free(self):
+        if self.h:
+            lib().pars_features_free(C.c_void_p(self.h))
+            self.h = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One CUDA device + its scratch (pars_ctx*)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.pars_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib().pars_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return lib().pars_ctx_launches(self.h)
+
+    def synchronize(self):
+        _check(lib().pars_ctx_synchronize(self.h))
+
+    # -- scoring ---------------------------------------------------------------
+    def score_text(self, ex: Extractor, text: np.ndarray, offsets: np.ndarray, weights,
+                   bias: float = 0.0, mode: int = MODE_EXACT) -> np.ndarray:
+        """Scorer::score_batch over prompts given as an arena + offsets."""
+        offs = _c(offsets, np.int64)
+        n = len(offs) - 1
+        out = np.zeros(max(n, 0), np.float64)
+        t = text if isinstance(text, np.ndarray) else np.frombuffer(bytes(text), np.uint8)
+        _check(lib().pars_score_text(self.h, C.byref(ex), _p(t), _p(offs), n,
+                                     _p(_c(weights, np.float64)), bias, mode, _p(out)))
+        return out
+
+    def score_texts(self, ex: Extractor, texts: Sequence[bytes], weights, bias=0.0,
+                    mode=MODE_EXACT) -> np.ndarray:
+        arena, offs = pack_texts(texts)
+        return self.score_text(ex, arena, offs, weights, bias, mode)
+
+    def dev_score_text(self, ex: Extractor, d_text: int, d_offsets: int, n: int, d_weights: int,
+                       bias: float, mode: int, d_scores: int, stream: int = 0):
+        _check(lib().pars_dev_score_text(self.h, C.byref(ex), d_text, d_offsets, n, d_weights,
+                                         bias, mode, d_scores, stream or None))
+
+    def score_embeddings(self, ex: Extractor, X, weights, bias=0.0, mode=MODE_EXACT):
+        X = _c(X, np.float64)
+        out = np.zeros(X.shape[0], np.float64)
+        _check(lib().pars_score_embeddings(self.h, C.byref(ex), _p(X), X.shape[0],
+                                           _p(_c(weights, np.float64)), bias, mode, _p(out)))
+        return out
+
+    # -- features ------------------------------------------------------------
+    def extract(self, ex: Extractor, text: np.ndarray, offsets: np.ndarray,
+                embeddings=None) -> Features:
+        """extract_all (features.cpp:124-141) -> device CSR."""
+        offs = _c(offsets, np.int64)
+        emb = None if embeddings is None else _c(embeddings, np.float64)
+        h = C.c_void_p()
+        _check(lib().pars_extract(self.h, C.byref(ex), _p(text), _p(offs), len(offs) - 1, _p(emb),
+                                  C.byref(h)))
+        return Features(self, h.value, ex.dim)
+
+    def extract_texts(self, ex: Extractor, texts: Sequence[bytes]) -> Features:
+        arena, offs = pack_texts(texts)
+        return self.extract(ex, arena, offs)
+
+    def upload_features(self, dim: int, row_ptr, idx, val) -> Features:
+        rp = _c(row_ptr, np.int64)
+        h = C.c_void_p()
+        _check(lib().pars_features_upload(self.h, dim, len(rp) - 1, _p(rp),
+                                          _p(_c(idx, np.uint32)), _p(_c(val, np.float64)),
+                                          C.byref(h)))
+        return Features(self, h.value, dim)
+
+    # -- pairs / training ----------------------------------------------------
+    def allpairs(self, scores, lengths, delta: float = 0.2, margin: float = 1.0):
+        """All-pairs margin ranking loss: (coeff int32[n], kept, active, loss_sum)."""
+        s = _c(scores, np.float64)
+        L = _c(lengths, np.int64)
+        c = np.zeros(len(s), np.int32)
+        kept, act, loss = C.c_uint64(), C.c_uint64(), C.c_double()
+        _check(lib().pars_allpairs(self.h, _p(s), _p(L), len(s), delta, margin, _p(c),
+                                   C.byref(kept), C.byref(act), C.byref(loss)))
+        return c, kept.value, act.value, loss.value
+
+    def sgd_epoch(self, feats: Features, a, b, y, batch: int, lr: float, margin: float, w,
+                  bias: float = 0.0):
+        w = np.array(w, np.float64, copy=True)
+        a, b, y = _c(a, np.uint32), _c(b, np.uint32), _c(y, np.int32)
+        el, act = C.c_double(), C.c_uint64()
+        _check(lib().pars_sgd_epoch(self.h, C.c_void_p(feats.h), _p(a), _p(b), _p(y), len(a), batch,
+                                    lr, margin, _p(w), bias, C.byref(el), C.byref(act)))
+        return w, el.value, act.value
+
+    def train_pairwise(self, ex: Extractor, text, offsets, lengths, delta=0.2, margin=1.0,
+                       epochs=5, batch=128, lr=0.1, seed=0, pairs_per_epoch=100000):
+        """train() with Objective::Pairwise (train.cpp:122-216)."""
+        offs = _c(offsets, np.int64)
+        lens = _c(lengths, np.int64)
+        w = np.zeros(ex.dim, np.float64)
+        bias = C.c_double()
+        lt = np.zeros(max(epochs, 1), np.float64)
+        _check(lib().pars_train_pairwise(self.h, C.byref(ex), _p(text), _p(offs), _p(lens),
+                                         len(offs) - 1, delta, margin, epochs, batch, lr, seed,
+                                         pairs_per_epoch, _p(w), C.byref(bias), _p(lt)))
+        return w, bias.value, lt[:epochs].copy()
+
+    # -- scheduling / metrics ------------------------------------------------
+    def priority_order(self, scores, tie_rank, boosted=None) -> np.ndarray:
+        """select_batch's full admission order (scheduler.cpp:33-60)."""
+        s = _c(scores, np.float64)
+        t = _c(tie_rank, np.uint32)
+        bst = None if boosted is None else _c(boosted, np.uint8)
+        out = np.zeros(len(s), np.int64)
+        _check(lib().pars_priority_order(self.h, _p(s), _p(bst), _p(t), len(s), _p(out)))
+        return out
+
+    def kendall_tau(self, x, y):
+        """kendall_tau_b (metrics.cpp:42-64): (tau_b, counts[n_c,n_d,n0,n1,n2])."""
+        x, y = _c(x, np.float64), _c(y, np.float64)
+        counts = np.zeros(5, np.uint64)
+        tau = C.c_double()
+        _check(lib().pars_kendall_tau(self.h, _p(x), _p(y), len(x), _p(counts), C.byref(tau)))
+        return tau.value, counts

@@ -1,0 +1,937 @@
+// C ABI (include/pars_cuda.h): context, device memory, host<->device staging
+// and orchestration of the kernels in featurize.cu / pairs.cu / sort.cu /
+// sgd.cu. Each entry cites the reference function it replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "featurize.cuh"
+#include "pairs.cuh"
+
+namespace pars_b200 {
+
+namespace {
+thread_local std::string g_error;
+}
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+}
+const char* get_error() { return g_error.c_str(); }
+
+}  // namespace pars_b200
+
+using namespace pars_b200;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct pars_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::mutex mu;
+  std::atomic<uint64_t> launches{0};
+  // grow-only scratch
+  DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  double dmin_delta = -1.0;
+  int64_t dmin_max = -1;
+};
+
+struct pars_features {
+  pars_ctx* ctx = nullptr;
+  uint32_t dim = 0;
+  int64_t rows = 0, nnz = 0;
+  int64_t* d_rp = nullptr;
+  uint32_t* d_idx = nullptr;
+  double* d_val = nullptr;
+  std::vector<int64_t> h_rp;  // host mirror of the row pointers
+};
+
+namespace pars_b200 {
+void count_launch(pars_ctx* ctx, uint64_t k) {
+  if (ctx) ctx->launches.fetch_add(k, std::memory_order_relaxed);
+}
+}  // namespace pars_b200
+
+namespace pars_b200 {
+namespace capi_detail {
+
+int ensure(DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap) return PARS_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = std::max<size_t>(bytes, 256);
+  want = want + want / 4;  // headroom for growth
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("device allocation of %zu bytes failed", bytes);
+      return PARS_ERR_OOM;
+    }
+    want = bytes;
+  }
+  b.cap = want;
+  return PARS_OK;
+}
+
+struct Guard {
+  pars_ctx* c;
+  std::lock_guard<std::mutex> lk;
+  explicit Guard(pars_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
+};
+
+cudaStream_t pick(pars_ctx* ctx, void* s) {
+  return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+int check_ctx(pars_ctx* ctx) {
+  if (!ctx) {
+    set_error("null pars_ctx");
+    return PARS_ERR_INVALID;
+  }
+  return PARS_OK;
+}
+
+__global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (float)in[i];
+}
+
+// Sequential fp64 dot per CSR row (features.hpp:31-35 + scorer.cpp:40-42).
+__global__ void csr_score_kernel(const int64_t* __restrict__ rp, const uint32_t* __restrict__ idx,
+                                 const double* __restrict__ val, int64_t rows,
+                                 const double* __restrict__ w, double bias,
+                                 double* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) s = __dadd_rn(s, __dmul_rn(w[idx[e]], val[e]));
+  out[r] = __dadd_rn(s, bias);
+}
+
+// Compact per-prompt slots into a CSR.
+__global__ void compact_kernel(const int64_t* __restrict__ slot, const int64_t* __restrict__ rp,
+                               int64_t n, const uint32_t* __restrict__ sidx,
+                               const double* __restrict__ sval, uint32_t* __restrict__ idx,
+                               double* __restrict__ val) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t s = slot[i], b = rp[i], e = rp[i + 1];
+  for (int64_t k = threadIdx.x; k < e - b; k += blockDim.x) {
+    idx[b + k] = sidx[s + k];
+    val[b + k] = sval[s + k];
+  }
+}
+
+// Dense embeddings -> CSR rows with every index (features.cpp:67-76, zeros
+// kept), L2 with the reference's sequential sum of squares.
+__global__ void dense_csr_kernel(const double* __restrict__ X, int64_t n, uint32_t dim, int norm,
+                                 uint32_t* __restrict__ idx, double* __restrict__ val) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* x = X + i * (int64_t)dim;
+  double inv = 1.0;
+  bool scale = false;
+  if (norm) {
+    double sq = 0.0;
+    for (uint32_t k = 0; k < dim; ++k) sq = __dadd_rn(sq, __dmul_rn(x[k], x[k]));
+    if (sq > 0.0) {
+      inv = __ddiv_rn(1.0, __dsqrt_rn(sq));
+      scale = true;
+    }
+  }
+  for (uint32_t k = 0; k < dim; ++k) {
+    idx[i * (int64_t)dim + k] = k;
+    val[i * (int64_t)dim + k] = scale ? __dmul_rn(x[k], inv) : x[k];
+  }
+}
+
+int upload_weights(pars_ctx* ctx, const FeatConfig& cfg, const double* w, int mode,
+                   cudaStream_t st) {
+  PARS_TRY(ensure(ctx->w64, (size_t)cfg.dim * 8));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->w64.p, w, (size_t)cfg.dim * 8, cudaMemcpyHostToDevice, st));
+  if (mode == PARS_MODE_FAST_F32) {
+    PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
+    f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(
+        (const double*)ctx->w64.p, (float*)ctx->w32.p, cfg.dim);
+    count_launch(ctx);
+  }
+  return PARS_OK;
+}
+
+int check_mode(int mode) {
+  if (mode != PARS_MODE_EXACT_F64 && mode != PARS_MODE_FAST_F32) {
+    set_error("unknown scoring mode %d", mode);
+    return PARS_ERR_INVALID;
+  }
+  return PARS_OK;
+}
+
+// Scores [i0, i1) whose text and offsets are already on the device.
+int score_chunk(pars_ctx* ctx, const FeatConfig& cfg, int mode, const uint8_t* d_text_base,
+                const int64_t* d_offs, int64_t n, double bias, double* d_scores, cudaStream_t st) {
+  PARS_TRY(ensure(ctx->longl, (size_t)std::max<int64_t>(n, 1) * 4 + 16));
+  FeatArgs a{};
+  a.text = d_text_base;
+  a.offsets = d_offs;
+  a.n = n;
+  a.w64 = (const double*)ctx->w64.p;
+  a.w32 = (const float*)ctx->w32.p;
+  a.bias = bias;
+  a.scores = d_scores;
+  a.long_count = (int32_t*)ctx->longl.p;
+  a.long_list = (int32_t*)ctx->longl.p + 4;
+  return launch_featurize(ctx, cfg, mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast,
+                          a, st);
+}
+
+int ensure_dmin(pars_ctx* ctx, double delta, int64_t max_len, cudaStream_t st) {
+  if (ctx->dmin_delta == delta && ctx->dmin_max >= max_len && ctx->dmin_buf.p) return PARS_OK;
+  std::vector<int32_t> t((size_t)max_len + 1);
+  PARS_TRY(pars_length_gap_table(delta, max_len, t.data()));
+  PARS_TRY(ensure(ctx->dmin_buf, t.size() * 4));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->dmin_buf.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  ctx->dmin_delta = delta;
+  ctx->dmin_max = max_len;
+  return PARS_OK;
+}
+
+constexpr int64_t kMaxLengthTable = 1ll << 26;
+
+}  // namespace capi_detail
+}  // namespace pars_b200
+using namespace pars_b200::capi_detail;
+
+extern "C" {
+
+const char* pars_last_error(void) { return get_error(); }
+const char* pars_version(void) { return "pars-b200 0.1 (sm_100a)"; }
+
+int pars_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    set_error("no CUDA device: %s", cudaGetErrorString(e));
+    return PARS_ERR_CUDA;
+  }
+  *count = n;
+  return PARS_OK;
+}
+
+int pars_ctx_create(int device, pars_ctx** out) {
+  *out = nullptr;
+  int n = 0;
+  PARS_TRY(pars_device_count(&n));
+  if (device < 0 || device >= n) {
+    set_error("device %d out of range (%d devices)", device, n);
+    return PARS_ERR_INVALID;
+  }
+  cudaDeviceProp prop;
+  PARS_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_error("libpars_cuda is built for sm_100a (B200); device %d is sm_%d%d", device,
+              prop.major, prop.minor);
+    return PARS_ERR_CUDA;
+  }
+  PARS_CUDA_CHECK(cudaSetDevice(device));
+  auto* c = new pars_ctx();
+  c->device = device;
+  PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    PARS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_copy[k], cudaEventDisableTiming));
+    PARS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+  }
+  *out = c;
+  return PARS_OK;
+}
+
+void pars_ctx_destroy(pars_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->copy_stream);
+  DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
+                    &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
+                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(c->ev_copy[k]);
+    cudaEventDestroy(c->ev_done[k]);
+  }
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->copy_stream);
+  delete c;
+}
+
+int pars_ctx_synchronize(pars_ctx* ctx) {
+  PARS_TRY(check_ctx(ctx));
+  cudaSetDevice(ctx->device);
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return PARS_OK;
+}
+
+uint64_t pars_ctx_launches(const pars_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int pars_host_alloc(size_t bytes, void** out) {
+  PARS_CUDA_CHECK(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocDefault));
+  return PARS_OK;
+}
+void pars_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+// ---- scoring -------------------------------------------------------------
+
+// Scorer::score_batch fused with extract_features (scorer.cpp:9-24,
+// features.cpp:62-122). Host buffers; the text is streamed to the device in
+// chunks on a copy stream, overlapped with the kernel of the previous chunk.
+int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                    const int64_t* offsets, int64_t n, const double* weights, double bias, int mode,
+                    double* scores) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
+  if (ex->kind != 0) {
+    set_error("pars_score_text: extractor kind is precomputed_embedding; use pars_score_embeddings");
+    return PARS_ERR_INVALID;
+  }
+  if (n < 0) {
+    set_error("negative prompt count");
+    return PARS_ERR_INVALID;
+  }
+  if (n == 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+  PARS_TRY(upload_weights(ctx, cfg, weights, mode, st));
+  // chunk by text bytes (~64 MB) and prompt count
+  const int64_t kChunkBytes = 64ll << 20, kChunkPrompts = 1 << 18;
+  std::vector<int64_t> starts;
+  for (int64_t i = 0; i < n;) {
+    starts.push_back(i);
+    int64_t j = i + 1;
+    while (j < n && j - i < kChunkPrompts && offsets[j + 1] - offsets[i] <= kChunkBytes) ++j;
+    i = j;
+  }
+  starts.push_back(n);
+  const int nchunks = (int)starts.size() - 1;
+  // worst-case buffers
+  int64_t max_bytes = 0, max_n = 0;
+  for (int k = 0; k < nchunks; ++k) {
+    max_bytes = std::max(max_bytes, offsets[starts[k + 1]] - offsets[starts[k]]);
+    max_n = std::max(max_n, starts[k + 1] - starts[k]);
+  }
+  for (int b = 0; b < 2; ++b) {
+    PARS_TRY(ensure(ctx->text[b], (size_t)max_bytes + 16));
+    PARS_TRY(ensure(ctx->offs[b], (size_t)(max_n + 1) * 8));
+    PARS_TRY(ensure(ctx->scores[b], (size_t)max_n * 8));
+  }
+  // the weights upload (on st) must land before any kernel: already ordered on st
+  for (int k = 0; k < nchunks; ++k) {
+    const int b = k & 1;
+    const int64_t i0 = starts[k], i1 = starts[k + 1], m = i1 - i0;
+    const int64_t t0 = offsets[i0], tb = offsets[i1] - t0;
+    if (k >= 2) PARS_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->text[b].p, text + t0, (size_t)tb, cudaMemcpyHostToDevice, cs));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->offs[b].p, offsets + i0, (size_t)(m + 1) * 8,
+                                    cudaMemcpyHostToDevice, cs));
+    PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_copy[b], cs));
+    PARS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copy[b], 0));
+    // offsets are absolute: shift the device text base so text[offsets[i]] is valid
+    const uint8_t* base = static_cast<const uint8_t*>(ctx->text[b].p) - t0;
+    PARS_TRY(score_chunk(ctx, cfg, mode, base, (const int64_t*)ctx->offs[b].p, m, bias,
+                         (double*)ctx->scores[b].p, st));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(scores + i0, ctx->scores[b].p, (size_t)m * 8,
+                                    cudaMemcpyDeviceToHost, st));
+    PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_done[b], st));
+  }
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* d_text,
+                        const int64_t* d_offsets, int64_t n, const double* d_weights, double bias,
+                        int mode, double* d_scores, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  PARS_TRY(ensure(ctx->longl, (size_t)n * 4 + 16));
+  FeatArgs a{};
+  a.text = reinterpret_cast<const uint8_t*>(d_text);
+  a.offsets = d_offsets;
+  a.n = n;
+  a.w64 = d_weights;
+  if (mode == PARS_MODE_FAST_F32) {
+    PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
+    f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(d_weights,
+                                                                        (float*)ctx->w32.p, cfg.dim);
+    count_launch(ctx);
+    a.w32 = (const float*)ctx->w32.p;
+  }
+  a.bias = bias;
+  a.scores = d_scores;
+  a.long_count = (int32_t*)ctx->longl.p;
+  a.long_list = (int32_t*)ctx->longl.p + 4;
+  return launch_featurize(ctx, cfg, mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast,
+                          a, st);
+}
+
+int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex, const double* X, int64_t n,
+                          const double* weights, double bias, int mode, double* scores) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(upload_weights(ctx, cfg, weights, mode, st));
+  PARS_TRY(ensure(ctx->misc, (size_t)n * cfg.dim * 8));
+  PARS_TRY(ensure(ctx->scores[0], (size_t)n * 8));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->misc.p, X, (size_t)n * cfg.dim * 8, cudaMemcpyHostToDevice, st));
+  PARS_TRY(launch_score_dense(ctx, cfg, mode, (const double*)ctx->misc.p, n,
+                              (const double*)ctx->w64.p, (const float*)ctx->w32.p, bias,
+                              (double*)ctx->scores[0].p, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(scores, ctx->scores[0].p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+// ---- features ------------------------------------------------------------
+
+// extract_all (features.cpp:124-141) into a device-resident CSR.
+int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, const int64_t* offsets,
+                 int64_t n, const double* emb, pars_features** out) {
+  *out = nullptr;
+  PARS_TRY(check_ctx(ctx));
+  FeatConfig cfg;
+  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
+  if (n < 0) {
+    set_error("negative prompt count");
+    return PARS_ERR_INVALID;
+  }
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  auto* f = new pars_features();
+  f->ctx = ctx;
+  f->dim = cfg.dim;
+  f->rows = n;
+  f->h_rp.assign((size_t)n + 1, 0);
+  auto fail_free = [&](int rc) {
+    if (f->d_rp) cudaFree(f->d_rp);
+    if (f->d_idx) cudaFree(f->d_idx);
+    if (f->d_val) cudaFree(f->d_val);
+    delete f;
+    return rc;
+  };
+  if (ex->kind == 1) {
+    if (n > 0 && !emb) {
+      set_error("prompt '%s' has no embedding but extractor kind is precomputed_embedding", "?");
+      return fail_free(PARS_ERR_INVALID);
+    }
+    const int64_t nnz = n * (int64_t)cfg.dim;
+    for (int64_t i = 0; i <= n; ++i) f->h_rp[i] = i * (int64_t)cfg.dim;
+    f->nnz = nnz;
+    if (cudaMalloc(&f->d_rp, (size_t)(n + 1) * 8) != cudaSuccess ||
+        cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(nnz, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(nnz, 1) * 8) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("device allocation failed (extract, embeddings)");
+      return fail_free(PARS_ERR_OOM);
+    }
+    if (ensure(ctx->misc, (size_t)std::max<int64_t>(nnz, 1) * 8) != PARS_OK) return fail_free(PARS_ERR_OOM);
+    cudaMemcpyAsync(f->d_rp, f->h_rp.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
+    if (n > 0) {
+      cudaMemcpyAsync(ctx->misc.p, emb, (size_t)nnz * 8, cudaMemcpyHostToDevice, st);
+      dense_csr_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(
+          (const double*)ctx->misc.p, n, cfg.dim, cfg.norm, f->d_idx, f->d_val);
+      count_launch(ctx);
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("CUDA error in extract (embeddings): %s", cudaGetErrorString(cudaGetLastError()));
+      return fail_free(PARS_ERR_CUDA);
+    }
+    *out = f;
+    return PARS_OK;
+  }
+  // hashed text: per-prompt slots sized by the feature upper bound
+  std::vector<int64_t> slot((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) slot[i + 1] = slot[i] + feat_cap(cfg, offsets[i + 1] - offsets[i]);
+  const int64_t cap_total = slot[n];
+  const int64_t t0 = n > 0 ? offsets[0] : 0, tb = n > 0 ? offsets[n] - t0 : 0;
+  int rc = PARS_OK;
+  if ((rc = ensure(ctx->text[0], (size_t)tb + 16)) != PARS_OK ||
+      (rc = ensure(ctx->offs[0], (size_t)(n + 1) * 8)) != PARS_OK ||
+      (rc = ensure(ctx->misc, (size_t)std::max<int64_t>(cap_total, 1) * 12 + (size_t)(n + 1) * 8 * 2 + 1024)) != PARS_OK ||
+      (rc = ensure(ctx->longl, (size_t)std::max<int64_t>(n, 1) * 4 + 16)) != PARS_OK ||
+      (rc = ensure(ctx->scores[0], (size_t)std::max<int64_t>(n, 1) * 8)) != PARS_OK)
+    return fail_free(rc);
+  char* mp = (char*)ctx->misc.p;
+  int64_t* d_slot = (int64_t*)mp;
+  int64_t* d_rp_tmp = d_slot + (n + 1);
+  uint32_t* s_idx = (uint32_t*)(d_rp_tmp + (n + 1));
+  double* s_val = (double*)(((uintptr_t)(s_idx + cap_total) + 15) & ~(uintptr_t)15);
+  int32_t* d_nnz = (int32_t*)ctx->scores[0].p;
+  if (n > 0) {
+    cudaMemcpyAsync(ctx->text[0].p, text + t0, (size_t)tb, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(ctx->offs[0].p, offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_slot, slot.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
+    FeatArgs a{};
+    a.text = static_cast<const uint8_t*>(ctx->text[0].p) - t0;
+    a.offsets = (const int64_t*)ctx->offs[0].p;
+    a.n = n;
+    a.slot_base = d_slot;
+    a.out_idx = s_idx;
+    a.out_val = s_val;
+    a.out_nnz = d_nnz;
+    a.long_count = (int32_t*)ctx->longl.p;
+    a.long_list = (int32_t*)ctx->longl.p + 4;
+    if ((rc = launch_featurize(ctx, cfg, kFeatCsr, a, st)) != PARS_OK) return fail_free(rc);
+    std::vector<int32_t> nnz((size_t)n);
+    cudaMemcpyAsync(nnz.data(), d_nnz, (size_t)n * 4, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("CUDA error in extract: %s", cudaGetErrorString(cudaGetLastError()));
+      return fail_free(PARS_ERR_CUDA);
+    }
+    for (int64_t i = 0; i < n; ++i) f->h_rp[i + 1] = f->h_rp[i] + nnz[i];
+  }
+  f->nnz = f->h_rp[n];
+  if (cudaMalloc(&f->d_rp, (size_t)(n + 1) * 8) != cudaSuccess ||
+      cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess ||
+      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed (extract)");
+    return fail_free(PARS_ERR_OOM);
+  }
+  cudaMemcpyAsync(f->d_rp, f->h_rp.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
+  if (n > 0) {
+    compact_kernel<<<(unsigned)n, 128, 0, st>>>(d_slot, f->d_rp, n, s_idx, s_val, f->d_idx, f->d_val);
+    count_launch(ctx);
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("CUDA error in extract (compact): %s", cudaGetErrorString(cudaGetLastError()));
+    return fail_free(PARS_ERR_CUDA);
+  }
+  *out = f;
+  return PARS_OK;
+}
+
+int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows, const int64_t* row_ptr,
+                         const uint32_t* idx, const double* val, pars_features** out) {
+  *out = nullptr;
+  PARS_TRY(check_ctx(ctx));
+  Guard g(ctx);
+  auto* f = new pars_features();
+  f->ctx = ctx;
+  f->dim = dim;
+  f->rows = rows;
+  f->h_rp.assign(row_ptr, row_ptr + rows + 1);
+  const int64_t base = row_ptr[0];
+  for (auto& r : f->h_rp) r -= base;
+  f->nnz = f->h_rp[rows];
+  for (int64_t k = 0; k < f->nnz; ++k)
+    if (idx[k] >= dim) {
+      set_error("feature index %u outside dimension %u", idx[k], dim);
+      delete f;
+      return PARS_ERR_INVALID;
+    }
+  if (cudaMalloc(&f->d_rp, (size_t)(rows + 1) * 8) != cudaSuccess ||
+      cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess ||
+      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed (features upload)");
+    delete f;
+    return PARS_ERR_OOM;
+  }
+  cudaMemcpyAsync(f->d_rp, f->h_rp.data(), (size_t)(rows + 1) * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(f->d_idx, idx, (size_t)f->nnz * 4, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(f->d_val, val, (size_t)f->nnz * 8, cudaMemcpyHostToDevice, ctx->stream);
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  *out = f;
+  return PARS_OK;
+}
+
+int64_t pars_features_rows(const pars_features* f) { return f ? f->rows : -1; }
+int64_t pars_features_nnz(const pars_features* f) { return f ? f->nnz : -1; }
+
+int pars_features_download(pars_ctx* ctx, const pars_features* f, int64_t* row_ptr, uint32_t* idx,
+                           double* val) {
+  PARS_TRY(check_ctx(ctx));
+  Guard g(ctx);
+  std::memcpy(row_ptr, f->h_rp.data(), (size_t)(f->rows + 1) * 8);
+  if (f->nnz > 0) {
+    PARS_CUDA_CHECK(cudaMemcpyAsync(idx, f->d_idx, (size_t)f->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(val, f->d_val, (size_t)f->nnz * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return PARS_OK;
+}
+
+void pars_features_free(pars_features* f) {
+  if (!f) return;
+  cudaSetDevice(f->ctx->device);
+  if (f->d_rp) cudaFree(f->d_rp);
+  if (f->d_idx) cudaFree(f->d_idx);
+  if (f->d_val) cudaFree(f->d_val);
+  delete f;
+}
+
+int pars_features_score(pars_ctx* ctx, const pars_features* f, const double* weights, double bias,
+                        double* scores) {
+  PARS_TRY(check_ctx(ctx));
+  if (f->rows == 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->w64, (size_t)f->dim * 8));
+  PARS_TRY(ensure(ctx->scores[0], (size_t)f->rows * 8));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->w64.p, weights, (size_t)f->dim * 8, cudaMemcpyHostToDevice, st));
+  csr_score_kernel<<<(unsigned)ceil_div(f->rows, 128), 128, 0, st>>>(
+      f->d_rp, f->d_idx, f->d_val, f->rows, (const double*)ctx->w64.p, bias,
+      (double*)ctx->scores[0].p);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  PARS_CUDA_CHECK(cudaMemcpyAsync(scores, ctx->scores[0].p, (size_t)f->rows * 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+// ---- all-pairs -----------------------------------------------------------
+
+int64_t pars_allpairs_tiles(int64_t n) { return allpairs_tile_count(n); }
+
+int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths, int64_t n,
+                  double delta, double margin, int32_t* coeff, uint64_t* kept, uint64_t* active,
+                  double* loss_sum) {
+  PARS_TRY(check_ctx(ctx));
+  if (delta < 0.0 || delta >= 1.0) {
+    set_error("all-pairs: delta %g outside [0, 1)", delta);
+    return PARS_ERR_INVALID;
+  }
+  *kept = *active = 0;
+  *loss_sum = 0.0;
+  if (n <= 0) return PARS_OK;
+  int64_t max_len = 0;
+  std::vector<int32_t> L((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (lengths[i] < 0 || lengths[i] > kMaxLengthTable) {
+      set_error("all-pairs: length %lld outside [0, %lld]", (long long)lengths[i],
+                (long long)kMaxLengthTable);
+      return PARS_ERR_UNSUPPORTED;
+    }
+    L[i] = (int32_t)lengths[i];
+    max_len = std::max<int64_t>(max_len, lengths[i]);
+  }
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure_dmin(ctx, delta, max_len, st));
+  const int64_t tiles = allpairs_tile_count(n);
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * 8 + (size_t)n * 4 + (size_t)n * 4 + 64 + (size_t)tiles * 8 + 1024));
+  char* p = (char*)ctx->pairs_in.p;
+  double* d_s = (double*)p;
+  int32_t* d_L = (int32_t*)(d_s + n);
+  int32_t* d_c = d_L + n;
+  unsigned long long* d_cnt = (unsigned long long*)(((uintptr_t)(d_c + n) + 15) & ~(uintptr_t)15);
+  double* d_part = (double*)(d_cnt + 4);
+  double* d_loss = d_part + tiles;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_s, scores, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_L, L.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemsetAsync(d_c, 0, (size_t)n * 4, st));
+  PARS_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 32, st));
+  PARS_TRY(launch_allpairs(ctx, d_s, d_L, (const int32_t*)ctx->dmin_buf.p, n, margin, 0, tiles,
+                           d_c, d_cnt, d_part, st));
+  PARS_TRY(launch_sum_partials(ctx, d_part, tiles, d_loss, st));
+  unsigned long long cnt[2];
+  PARS_CUDA_CHECK(cudaMemcpyAsync(coeff, d_c, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(loss_sum, d_loss, 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  *kept = cnt[0];
+  *active = cnt[1];
+  return PARS_OK;
+}
+
+int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores, const int32_t* d_lengths, int64_t n,
+                      double delta, double margin, int64_t max_len, int64_t tile_begin,
+                      int64_t tile_end, int32_t* d_coeff, unsigned long long* d_counters,
+                      double* d_loss_partials, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  if (delta < 0.0 || delta >= 1.0) {
+    set_error("all-pairs: delta %g outside [0, 1)", delta);
+    return PARS_ERR_INVALID;
+  }
+  if (max_len < 0 || max_len > kMaxLengthTable) {
+    set_error("all-pairs: max_len %lld outside [0, %lld]", (long long)max_len,
+              (long long)kMaxLengthTable);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  PARS_TRY(ensure_dmin(ctx, delta, max_len, st));
+  return launch_allpairs(ctx, d_scores, d_lengths, (const int32_t*)ctx->dmin_buf.p, n, margin,
+                         tile_begin, tile_end, d_coeff, d_counters, d_loss_partials, st);
+}
+
+int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff, int64_t row_begin,
+                  int64_t row_end, double* d_grad, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  row_begin = std::max<int64_t>(0, row_begin);
+  row_end = std::min<int64_t>(f->rows, row_end);
+  if (row_end <= row_begin) {
+    PARS_CUDA_CHECK(cudaMemsetAsync(d_grad, 0, (size_t)f->dim * 8, st));
+    return PARS_OK;
+  }
+  const int parts = xtc_parts(row_end - row_begin);
+  PARS_TRY(ensure(ctx->misc2, (size_t)parts * f->dim * 8));
+  return launch_xtc(ctx, f->d_rp, f->d_idx, f->d_val, d_coeff, row_begin, row_end, f->dim,
+                    (double*)ctx->misc2.p, d_grad, st);
+}
+
+// ---- training ------------------------------------------------------------
+
+namespace pars_b200 {
+namespace capi_detail {
+
+int sgd_epoch_impl(pars_ctx* ctx, const pars_features* f, const uint32_t* a, const uint32_t* b,
+                   const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,
+                   double* d_w, double bias, double* epoch_loss, uint64_t* active) {
+  if (batch < 1 || batch > 32767) {
+    set_error("sgd: batch size %d outside [1, 32767]", batch);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  if ((size_t)f->dim * 8 + (size_t)batch * 29 + 64 > 220 * 1024) {
+    set_error("sgd: dimension %u too large for the shared-memory weight vector", f->dim);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = ctx->stream;
+  *epoch_loss = 0.0;
+  *active = 0;
+  if (npairs <= 0) return PARS_OK;
+  for (int64_t p = 0; p < npairs; ++p)
+    if (a[p] >= f->rows || b[p] >= f->rows) {
+      set_error("sgd: pair %lld references a row outside [0, %lld)", (long long)p, (long long)f->rows);
+      return PARS_ERR_INVALID;
+    }
+  const int64_t nb = (npairs + batch - 1) / batch;
+  std::vector<int64_t> ent_off((size_t)nb + 1, 0);
+  for (int64_t q = 0; q < nb; ++q) {
+    int64_t s = 0;
+    const int64_t p1 = std::min<int64_t>(npairs, (q + 1) * batch);
+    for (int64_t p = q * batch; p < p1; ++p)
+      s += (f->h_rp[a[p] + 1] - f->h_rp[a[p]]) + (f->h_rp[b[p] + 1] - f->h_rp[b[p]]);
+    ent_off[q + 1] = ent_off[q] + s;
+  }
+  const int64_t total = ent_off[nb];
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)npairs * 12 + 64 + 32));
+  uint32_t* d_a = (uint32_t*)ctx->pairs_in.p;
+  uint32_t* d_b = d_a + npairs;
+  int32_t* d_y = (int32_t*)(d_b + npairs);
+  double* d_loss = (double*)(((uintptr_t)(d_y + npairs) + 15) & ~(uintptr_t)15);
+  unsigned long long* d_act = (unsigned long long*)(d_loss + 1);
+  const size_t sb = sgd_scratch_bytes(nb, batch, f->dim, total) + 4096;
+  PARS_TRY(ensure(ctx->sgd, sb));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_a, a, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, b, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_y, y, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->sgd.p, ent_off.data(), ent_off.size() * 8, cudaMemcpyHostToDevice, st));
+  PARS_TRY(launch_sgd_epoch(ctx, f->d_rp, f->d_idx, f->d_val, f->dim, d_a, d_b, d_y, npairs, batch,
+                            lr, margin, bias, d_w, d_loss, d_act, total, ctx->sgd.p, sb, st));
+  unsigned long long act = 0;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(epoch_loss, d_loss, 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(&act, d_act, 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  *active = act;
+  return PARS_OK;
+}
+
+}  // namespace capi_detail
+}  // namespace pars_b200
+
+int pars_sgd_epoch(pars_ctx* ctx, const pars_features* f, const uint32_t* a, const uint32_t* b,
+                   const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,
+                   double* w, double bias, double* epoch_loss, uint64_t* active) {
+  PARS_TRY(check_ctx(ctx));
+  Guard g(ctx);
+  PARS_TRY(ensure(ctx->misc2, (size_t)f->dim * 8));
+  double* d_w = (double*)ctx->misc2.p;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_w, w, (size_t)f->dim * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PARS_TRY(sgd_epoch_impl(ctx, f, a, b, y, npairs, batch, lr, margin, d_w, bias, epoch_loss, active));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(w, d_w, (size_t)f->dim * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return PARS_OK;
+}
+
+// train() for Objective::Pairwise (train.cpp:122-166, 212-216).
+int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                        const int64_t* offsets, const int64_t* lengths, int64_t n, double delta,
+                        double margin, int32_t epochs, int32_t batch, double lr, uint64_t seed,
+                        uint64_t pairs_per_epoch, double* w_out, double* bias_out,
+                        double* loss_trace) {
+  PARS_TRY(check_ctx(ctx));
+  // validate (train.cpp:96-106), same order and messages
+  if (epochs < 0) { set_error("train: epochs must be >= 0"); return PARS_ERR_INVALID; }
+  if (batch < 1) { set_error("train: batch_size must be >= 1"); return PARS_ERR_INVALID; }
+  if (!(lr > 0.0)) { set_error("train: learning_rate must be > 0"); return PARS_ERR_INVALID; }
+  if (margin < 0.0) { set_error("train: margin must be >= 0"); return PARS_ERR_INVALID; }
+  if (delta < 0.0 || delta >= 1.0) {
+    set_error("train: delta %g outside [0, 1)", delta);
+    return PARS_ERR_INVALID;
+  }
+  if (pairs_per_epoch < 1) { set_error("train: pairs_per_epoch must be >= 1"); return PARS_ERR_INVALID; }
+  if (n <= 0) { set_error("train: empty dataset"); return PARS_ERR_INVALID; }
+  pars_features* f = nullptr;
+  PARS_TRY(pars_extract(ctx, ex, text, offsets, n, nullptr, &f));
+  const uint32_t dim = ex->dim;
+  int rc = PARS_OK;
+  {
+    Guard g(ctx);
+    cudaStream_t st = ctx->stream;
+    rc = ensure(ctx->misc2, (size_t)dim * 8);
+    double* d_w = (double*)ctx->misc2.p;
+    if (rc == PARS_OK) rc = cudaMemsetAsync(d_w, 0, (size_t)dim * 8, st) == cudaSuccess ? PARS_OK : PARS_ERR_CUDA;
+    std::vector<uint32_t> pa(pairs_per_epoch), pb(pairs_per_epoch);
+    std::vector<int32_t> py(pairs_per_epoch);
+    for (int e = 0; e < epochs && rc == PARS_OK; ++e) {
+      const uint64_t es = splitmix64(seed ^ splitmix64(0x10000u + (uint64_t)e));  // derive_seed
+      const int64_t np = pars_build_pairs(lengths, n, delta, pairs_per_epoch, es, pa.data(),
+                                          pb.data(), py.data(), nullptr);
+      if (np < 0) {
+        rc = (int)np;
+        break;
+      }
+      double el = 0.0;
+      uint64_t act = 0;
+      rc = sgd_epoch_impl(ctx, f, pa.data(), pb.data(), py.data(), np, batch, lr, margin, d_w, 0.0,
+                          &el, &act);
+      if (rc != PARS_OK) break;
+      const double mean = el / (double)np;
+      if (!std::isfinite(mean)) {
+        set_error("training diverged at epoch %d", e);
+        rc = PARS_ERR_INVALID;
+        break;
+      }
+      loss_trace[e] = mean;
+    }
+    if (rc == PARS_OK) {
+      if (cudaMemcpyAsync(w_out, d_w, (size_t)dim * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("CUDA error reading trained weights");
+        rc = PARS_ERR_CUDA;
+      }
+    }
+  }
+  *bias_out = 0.0;  // pairwise bias gradient cancels (train.hpp:41-43)
+  pars_features_free(f);
+  return rc;
+}
+
+// ---- priority ordering (scheduler.cpp:33-60) -------------------------------
+
+int pars_priority_order(pars_ctx* ctx, const double* scores, const uint8_t* boosted,
+                        const uint32_t* tie_rank, int64_t n, int64_t* order) {
+  PARS_TRY(check_ctx(ctx));
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * (8 + 1 + 4 + 4) + 64));
+  double* d_s = (double*)ctx->pairs_in.p;
+  uint32_t* d_t = (uint32_t*)(d_s + n);
+  uint32_t* d_o = d_t + n;
+  uint8_t* d_b = (uint8_t*)(d_o + n);
+  PARS_TRY(ensure(ctx->sort, sort_scratch_bytes(n) + 4096));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_s, scores, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, tie_rank, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  if (boosted) PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, boosted, (size_t)n, cudaMemcpyHostToDevice, st));
+  PARS_TRY(launch_priority_sort(ctx, d_s, boosted ? d_b : nullptr, d_t, n, d_o, ctx->sort.p, st));
+  std::vector<uint32_t> o((size_t)n);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(o.data(), d_o, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) order[i] = o[i];
+  return PARS_OK;
+}
+
+int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores, const uint8_t* d_boosted,
+                            const uint32_t* d_tie, int64_t n, uint32_t* d_order, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  PARS_TRY(ensure(ctx->sort, sort_scratch_bytes(n) + 4096));
+  return launch_priority_sort(ctx, d_scores, d_boosted, d_tie, n, d_order, ctx->sort.p, st);
+}
+
+// ---- Kendall tau-b (metrics.cpp:13-64) -----------------------------------
+
+int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n, uint64_t* counts,
+                     double* tau_b) {
+  PARS_TRY(check_ctx(ctx));
+  if (n < 2) {
+    set_error("kendall_tau_b: need at least 2 items, got %zu", (size_t)n);
+    return PARS_ERR_INVALID;
+  }
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * 16 + 64));
+  double* d_x = (double*)ctx->pairs_in.p;
+  double* d_y = d_x + n;
+  unsigned long long* d_c = (unsigned long long*)(d_y + n);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_y, y, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemsetAsync(d_c, 0, 32, st));
+  PARS_TRY(launch_tau(ctx, d_x, d_y, n, d_c, st));
+  unsigned long long c[4];
+  PARS_CUDA_CHECK(cudaMemcpyAsync(c, d_c, 32, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  const uint64_t n0 = (uint64_t)n * (uint64_t)(n - 1) / 2;
+  counts[0] = c[0];
+  counts[1] = c[1];
+  counts[2] = n0;
+  counts[3] = c[2];
+  counts[4] = c[3];
+  // finish_tau (metrics.cpp:13-32)
+  if (c[2] == n0) {
+    set_error("degenerate ranking: all values tied in first argument");
+    return PARS_ERR_INVALID;
+  }
+  if (c[3] == n0) {
+    set_error("degenerate ranking: all values tied in second argument");
+    return PARS_ERR_INVALID;
+  }
+  const double denom = std::sqrt(static_cast<double>(n0 - c[2]) * static_cast<double>(n0 - c[3]));
+  const double tau = (static_cast<double>(c[0]) - static_cast<double>(c[1])) / denom;
+  *tau_b = std::clamp(tau, -1.0, 1.0);
+  return PARS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace pars_b200 {
+
+int64_t allpairs_tile_count(int64_t n);
+int launch_allpairs(pars_ctx* ctx, const double* s, const int32_t* L, const int32_t* dmin,
+                    int64_t n, double margin, int64_t t0, int64_t t1, int32_t* coeff,
+                    unsigned long long* counters, double* loss_part, cudaStream_t st);
+int launch_sum_partials(pars_ctx* ctx, const double* p, int64_t n, double* out, cudaStream_t st);
+int launch_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
+               unsigned long long* out, cudaStream_t st);
+int xtc_parts(int64_t rows);
+int launch_xtc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
+               const int32_t* c, int64_t r0, int64_t r1, uint32_t dim, double* partial,
+               double* grad, cudaStream_t st);
+
+// priority sort (sort.cu)
+struct SortBuffers {
+  uint64_t* khi[2];
+  uint32_t* klo[2];
+  uint32_t* val[2];
+  uint32_t* hist;       // [256][blocks]
+  uint32_t* digit_hist; // [12][256] all-digit histogram
+};
+size_t sort_scratch_bytes(int64_t n);
+int launch_priority_sort(pars_ctx* ctx, const double* scores, const uint8_t* boosted,
+                         const uint32_t* tie, int64_t n, uint32_t* order, void* scratch,
+                         cudaStream_t st);
+
+// SGD epoch (sgd.cu)
+struct SgdPlan {
+  int64_t npairs;
+  int32_t batch;
+  int64_t nbatches;
+  uint32_t dim;
+};
+size_t sgd_scratch_bytes(int64_t nbatches, int32_t batch, uint32_t dim, int64_t max_entries);
+int launch_sgd_epoch(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
+                     uint32_t dim, const uint32_t* a, const uint32_t* b, const int32_t* y,
+                     int64_t npairs, int32_t batch, double lr, double margin, double bias,
+                     double* w, double* loss_out, unsigned long long* active_out,
+                     int64_t total_entries, void* scratch, size_t scratch_bytes,
+                     cudaStream_t st);
+
+}  // namespace pars_b200

@@ -1,0 +1,223 @@
+// Priority ordering: stable LSD radix sort over (score, tie_rank) keys.
+//
+// Reference: select_batch's comparator (scheduler.cpp:43-50) — boosted
+// requests first by (arrival, id); the rest ascending by score, ties by
+// (arrival_time, prompt_id), then by waiting index. With tie_rank = dense
+// rank of (arrival_time, prompt_id) the comparator is the lexicographic
+// order of the 96-bit key
+//     hi64 = boosted ? 0 : ordered_bits(score)     lo32 = tie_rank
+// and the index tiebreak is exactly the stability of an LSD radix sort
+// applied in input order. ordered_bits maps doubles to uint64 preserving <,
+// with -0.0 canonicalised to +0.0 (they compare equal in the reference).
+//
+// Kernels (8-bit digits, 12 digit positions):
+//   radix_init      keys + all 12 digit histograms in one pass (one D2H read
+//                   lets the host skip positions where every key shares the
+//                   digit — typically the constant high exponent bytes and the
+//                   unused high bytes of tie_rank);
+//   radix_hist      per-CTA digit counts of the current order (digit-major);
+//   radix_scan      exclusive scan of the [256][ctas] table (one CTA);
+//   radix_scatter   stable rank within the CTA via warp __match_any_sync +
+//                   per-warp digit counters, then a scattered write.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "pairs.cuh"
+
+namespace pars_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kTileKeys = kThreads * kItems;  // 2048
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint64_t ordered_bits(double x) {
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  if ((b << 1) == 0) b = 0;  // -0.0 == +0.0
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, int pos) {
+  return pos < 4 ? (lo >> (8 * pos)) & 0xffu : (uint32_t)(hi >> (8 * (pos - 4))) & 0xffu;
+}
+
+__global__ void radix_init(const double* __restrict__ score, const uint8_t* __restrict__ boosted,
+                           const uint32_t* __restrict__ tie, int64_t n, uint64_t* __restrict__ khi,
+                           uint32_t* __restrict__ klo, uint32_t* __restrict__ val,
+                           uint32_t* __restrict__ dh) {
+  __shared__ uint32_t h[12 * 256];
+  for (int k = threadIdx.x; k < 12 * 256; k += blockDim.x) h[k] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool bst = boosted && boosted[i];
+    const uint64_t hi = bst ? 0ull : ordered_bits(score[i]);
+    const uint32_t lo = tie[i];
+    khi[i] = hi;
+    klo[i] = lo;
+    val[i] = (uint32_t)i;
+#pragma unroll
+    for (int p = 0; p < 12; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, p)], 1u);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 12 * 256; k += blockDim.x)
+    if (h[k]) atomicAdd(&dh[k], h[k]);
+}
+
+__global__ void __launch_bounds__(kThreads) radix_hist(const uint64_t* __restrict__ khi,
+                                                       const uint32_t* __restrict__ klo,
+                                                       int64_t n, int pos, int nblocks,
+                                                       uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kTileKeys;
+  for (int k = threadIdx.x; k < kTileKeys; k += kThreads) {
+    const int64_t i = base + k;
+    if (i < n) atomicAdd(&h[digit_of(khi[i], klo[i], pos)], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(1024) radix_scan(uint32_t* __restrict__ a, int64_t m) {
+  __shared__ uint32_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (m + 1023) / 1024;
+  const int64_t b = t * per, e = min(m, b + per);
+  uint32_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += a[i];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint32_t v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[t] - s;
+  for (int64_t i = b; i < e; ++i) {
+    const uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) radix_scatter(
+    const uint64_t* __restrict__ khi_in, const uint32_t* __restrict__ klo_in,
+    const uint32_t* __restrict__ val_in, uint64_t* __restrict__ khi_out,
+    uint32_t* __restrict__ klo_out, uint32_t* __restrict__ val_out, int64_t n, int pos,
+    int nblocks, const uint32_t* __restrict__ offsets) {
+  __shared__ uint32_t wcnt[kThreads / 32][256];
+  __shared__ uint32_t gbase[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < (kThreads / 32) * 256; k += kThreads) (&wcnt[0][0])[k] = 0;
+  gbase[threadIdx.x] = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+  __syncthreads();
+  const int64_t sub = (int64_t)blockIdx.x * kTileKeys + warp * (32 * kItems);
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t hi[kItems];
+  uint32_t lo[kItems], vv[kItems], dg[kItems], rk[kItems];
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int64_t i = sub + r * 32 + lane;
+    const bool ok = i < n;
+    hi[r] = ok ? khi_in[i] : 0ull;
+    lo[r] = ok ? klo_in[i] : 0u;
+    vv[r] = ok ? val_in[i] : 0u;
+    const uint32_t d = ok ? digit_of(hi[r], lo[r], pos) : 256u;
+    dg[r] = d;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const uint32_t before = ok ? wcnt[warp][d] : 0u;
+    rk[r] = before + __popc(peers & lt);
+    __syncwarp();
+    if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // exclusive prefix over warps per digit (thread = digit)
+    const int d = threadIdx.x;
+    uint32_t run = gbase[d];
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint32_t c = wcnt[w][d];
+      wcnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    if (dg[r] < 256u) {
+      const uint32_t p = wcnt[warp][dg[r]] + rk[r];
+      khi_out[p] = hi[r];
+      klo_out[p] = lo[r];
+      val_out[p] = vv[r];
+    }
+  }
+}
+
+}  // namespace
+
+size_t sort_scratch_bytes(int64_t n) {
+  const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kTileKeys);
+  size_t b = 0;
+  b += 2 * (size_t)n * 8 + 2 * (size_t)n * 4 + 2 * (size_t)n * 4;
+  b += (size_t)nb * 256 * 4 + 12 * 256 * 4 + 1024;
+  return b;
+}
+
+int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boosted,
+                         const uint32_t* tie, int64_t n, uint32_t* order, void* scratch,
+                         cudaStream_t st) {
+  if (n == 0) return PARS_OK;
+  if (n > 0x7fffffffLL) {
+    set_error("priority order: n=%lld exceeds 2^31-1", (long long)n);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  const int nb = (int)ceil_div(n, kTileKeys);
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  uint64_t* khi[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
+  uint32_t* klo[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
+  uint32_t* val[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
+  uint32_t* hist = (uint32_t*)take((size_t)nb * 256 * 4);
+  uint32_t* dh = (uint32_t*)take(12 * 256 * 4);
+  PARS_CUDA_CHECK(cudaMemsetAsync(dh, 0, 12 * 256 * 4, st));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ig = std::min<int64_t>(ceil_div(n, 256), (int64_t)sms * 4);
+  radix_init<<<(unsigned)ig, 256, 0, st>>>(score, boosted, tie, n, khi[0], klo[0], val[0], dh);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  std::vector<uint32_t> hh(12 * 256);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(hh.data(), dh, hh.size() * 4, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  int cur = 0;
+  for (int pos = 0; pos < 12; ++pos) {
+    bool trivial = false;
+    for (int d = 0; d < 256; ++d)
+      if (hh[pos * 256 + d] == (uint32_t)n) trivial = true;
+    if (trivial) continue;
+    radix_hist<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], n, pos, nb, hist);
+    radix_scan<<<1, 1024, 0, st>>>(hist, (int64_t)nb * 256);
+    radix_scatter<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], val[cur], khi[cur ^ 1],
+                                           klo[cur ^ 1], val[cur ^ 1], n, pos, nb, hist);
+    count_launch(ctx, 3);
+    PARS_CUDA_CHECK(cudaGetLastError());
+    cur ^= 1;
+  }
+  PARS_CUDA_CHECK(cudaMemcpyAsync(order, val[cur], (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  return PARS_OK;
+}
+
+}  // namespace pars_b200

@@ -1,0 +1,271 @@
+"""GPU parity: every CUDA path through the C ABI against the oracle / the
+reference's golden fixtures. Bit-exact for features, exact-mode scores,
+masks, coefficients, counts, orders and the SGD trajectory; fast fp32 mode
+within 1e-5 of sum|w_i v_i| (the magnitude scale)."""
+import numpy as np
+import pytest
+
+from conftest import extractor_from, golden, unhex
+from oracle.bind import Extractor as OEx
+from oracle.bind import fnv64_array
+
+pytestmark = pytest.mark.gpu
+
+
+def oex(e):
+    return OEx.make(dim=e.dim, word=tuple(e.word[:e.n_word]), char=tuple(e.chr[:e.n_char]),
+                    norm="l2" if e.norm else "none", kind="hashed" if e.kind == 0 else "embedding")
+
+
+def grouped_feature_cases():
+    groups = {}
+    for c in golden("features.json")["cases"]:
+        key = repr(c["extractor"])
+        groups.setdefault(key, (c["extractor"], []))[1].append(c)
+    return list(groups.values())
+
+
+@pytest.mark.parametrize("desc,cases", grouped_feature_cases(),
+                         ids=lambda v: str(v.get("dim")) if isinstance(v, dict) else "")
+def test_extract_matches_reference_goldens(ctx, desc, cases):
+    from paper_2510_03243_b200 import pack_texts
+    e = extractor_from(desc)
+    texts = [bytes.fromhex(c["text"]) for c in cases]
+    # prefix the arena so offsets[0] != 0 and prompt starts are unaligned
+    arena, offs = pack_texts([b"#pad#"] + texts)
+    feats = ctx.extract(e, arena, offs[1:])
+    rp, idx, val = feats.download()
+    for k, c in enumerate(cases):
+        got_i = idx[rp[k]:rp[k + 1]]
+        got_v = val[rp[k]:rp[k + 1]]
+        assert got_i.tolist() == c["idx"], (k, c["text"][:40])
+        assert [float(v).hex() for v in got_v] == c["val"], (k, c["text"][:40])
+
+
+@pytest.mark.parametrize("desc,cases", grouped_feature_cases(),
+                         ids=lambda v: str(v.get("dim")) if isinstance(v, dict) else "")
+def test_exact_scores_bit_identical(ctx, oracle, desc, cases):
+    from paper_2510_03243_b200 import MODE_EXACT, pack_texts
+    e = extractor_from(desc)
+    texts = [bytes.fromhex(c["text"]) for c in cases]
+    rng = np.random.default_rng(desc["dim"])
+    w = rng.normal(size=desc["dim"])
+    arena, offs = pack_texts(texts)
+    got = ctx.score_text(e, arena, offs, w, bias=0.125, mode=MODE_EXACT)
+    want = oracle.score_batch(oex(e), arena, offs, w, 0.125)
+    assert [x.hex() for x in got] == [x.hex() for x in want]
+
+
+def test_fast_scores_within_tolerance(ctx, oracle):
+    from paper_2510_03243_b200 import MODE_FAST, Workload
+    wl = Workload.synthesize(3000, 5)
+    e = extractor_from(dict(kind=0, dim=4096, norm=1, word=[1], char=[3]))
+    w = np.random.default_rng(0).normal(size=4096)
+    got = ctx.score_text(e, wl.text, wl.offsets, w, 0.5, mode=MODE_FAST)
+    want = oracle.score_batch(oex(e), wl.text, wl.offsets, w, 0.5)
+    # magnitude scale sum |w_i v_i| per prompt
+    rp, idx, val = oracle.extract_all(oex(e), wl.text, wl.offsets)
+    scale = np.array([np.abs(w[idx[rp[i]:rp[i + 1]]] * val[rp[i]:rp[i + 1]]).sum() + 0.5
+                      for i in range(len(wl))])
+    rel = np.abs(got - want) / scale
+    assert rel.max() <= 1e-5, rel.max()
+
+
+def test_long_prompts_take_the_wide_counter_path(ctx, oracle):
+    from paper_2510_03243_b200 import MODE_EXACT, pack_texts
+    e = extractor_from(dict(kind=0, dim=4096, norm=1, word=[1], char=[3]))
+    long1 = b" ".join(b"tok%d" % (i % 17) for i in range(20000))  # >32767 features
+    long2 = b"aaa " * 40000  # one bucket with a count far above 2^15
+    texts = [b"short one", long1, b"x", long2, b""]
+    arena, offs = pack_texts(texts)
+    w = np.random.default_rng(2).normal(size=4096)
+    got = ctx.score_text(e, arena, offs, w, 0.0, MODE_EXACT)
+    want = oracle.score_batch(oex(e), arena, offs, w, 0.0)
+    assert [x.hex() for x in got] == [x.hex() for x in want]
+    f = ctx.extract(e, arena, offs)
+    rp, idx, val = f.download()
+    orp, oidx, oval = oracle.extract_all(oex(e), arena, offs)
+    assert (rp == orp).all() and (idx == oidx).all() and (val == oval).all()
+
+
+def test_readme_workload_scores_and_sjf_order(ctx):
+    """Appendix B: gen(500, seed 22) scored with the README model; burst
+    SJF order FNV 7432e2f4c44cbabd."""
+    from paper_2510_03243_b200 import Extractor, Workload, tie_ranks
+    m = golden("models.json")
+    z = golden("readme_model.npz")
+    w = z["weights"]
+    assert fnv64_array(w) == m["readme"]["weights_fnv"]
+    wl = Workload.synthesize(500, 22)
+    s = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w)
+    assert [x.hex() for x in s] == [x.hex() for x in z["s500"]]
+    ids = ["p%06d" % i for i in range(500)]
+    order = ctx.priority_order(s, tie_ranks(np.zeros(500), ids))
+    assert fnv64_array(order.astype(np.uint64)) == m["workload500"]["order_fnv"]
+
+
+def test_c1_scores_and_order(ctx):
+    """Config 1: 1,024 prompts (<=128 tokens) scored and sorted, bit-exact."""
+    from paper_2510_03243_b200 import Extractor, Workload, tie_ranks
+    m = golden("models.json")
+    z = golden("readme_model.npz")
+    g = Workload.synthesize(2048, 22)
+    sel = z["c1_index"]
+    texts = [g.prompt(i) for i in sel]
+    from paper_2510_03243_b200 import pack_texts
+    arena, offs = pack_texts(texts)
+    s = ctx.score_text(Extractor.make(), arena, offs, z["weights"])
+    assert fnv64_array(s) == m["c1"]["scores_fnv"] == "5548c3b3d81d615d"
+    ids = ["p%06d" % i for i in sel]
+    order = ctx.priority_order(s, tie_ranks(np.zeros(len(sel)), ids))
+    assert fnv64_array(order.astype(np.uint64)) == m["c1"]["order_fnv"] == "e6e78f54425df769"
+
+
+def test_priority_order_matches_select_batch_goldens(ctx):
+    from paper_2510_03243_b200 import tie_ranks
+    for c in golden("select.json"):
+        arrival, score = unhex(c["arrival"]), unhex(c["score"])
+        order = ctx.priority_order(score, tie_ranks(arrival, c["ids"]), np.array(c["boosted"], np.uint8))
+        assert order.tolist() == c["order"]
+
+
+def test_priority_order_large_random_with_ties(ctx, oracle):
+    from paper_2510_03243_b200 import tie_ranks
+    rng = np.random.default_rng(7)
+    n = 200_000
+    score = rng.choice(np.concatenate([rng.normal(size=50), [0.0, -0.0]]), size=n)
+    arrival = rng.choice(np.arange(100) * 0.25, size=n)
+    ids = ["q%d" % rng.integers(0, 1000) for _ in range(n)]
+    boosted = (rng.random(n) < 0.05).astype(np.uint8)
+    got = ctx.priority_order(score, tie_ranks(arrival, ids), boosted)
+    want = oracle.select_order(arrival, ids, score, boosted, 1e9)
+    assert (got == want).all()
+
+
+def test_allpairs_matches_oracle(ctx, oracle):
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 255, 256, 257, 3001):
+        lens = rng.integers(1, 400, size=n)
+        s = rng.normal(size=n)
+        c, kept, act, loss = ctx.allpairs(s, lens, 0.2, 1.0)
+        oc, okept, oact, oloss = oracle.allpairs(s, lens, 0.2, 1.0)
+        assert (c == oc).all() and kept == okept and act == oact
+        assert abs(loss - oloss) <= 1e-12 * max(1.0, abs(oloss))
+
+
+def test_allpairs_c2_mask_count(ctx):
+    """C2 dataset: exhaustive Eq. 1 count 30,028,032;
+    at w = 0 every kept pair is active with loss exactly margin."""
+    from paper_2510_03243_b200 import Workload
+    wl = Workload.synthesize(8192, 21)
+    c, kept, act, loss = ctx.allpairs(np.zeros(8192), wl.output_len, 0.2, 1.0)
+    assert kept == 30_028_032 == act
+    assert loss == float(kept)
+
+
+def test_kendall_tau_matches_goldens_and_oracle(ctx, oracle):
+    for c in golden("tau.json"):
+        tau, counts = ctx.kendall_tau(unhex(c["x"]), unhex(c["y"]))
+        assert counts.tolist() == c["counts"]
+        assert float(tau).hex() == c["tau"]
+    rng = np.random.default_rng(9)
+    x = rng.integers(0, 50, size=5000).astype(float)
+    y = rng.normal(size=5000).round(2)
+    tau, counts = ctx.kendall_tau(x, y)
+    otau, ocounts = oracle.kendall(x, y)
+    assert counts.tolist() == ocounts.tolist() and tau == otau
+
+
+def test_kendall_degenerate_error(ctx):
+    from paper_2510_03243_b200 import ParsError
+    with pytest.raises(ParsError, match="degenerate ranking"):
+        ctx.kendall_tau(np.ones(10), np.arange(10.0))
+
+
+def test_sgd_epoch_bit_identical(ctx, oracle):
+    from paper_2510_03243_b200 import Extractor, Workload, build_pairs
+    wl = Workload.synthesize(1500, 12)
+    e = Extractor.make()
+    f = ctx.extract(e, wl.text, wl.offsets)
+    rp, idx, val = f.download()
+    a, b, y, _ = build_pairs(wl.output_len, 0.2, 20000, 99)
+    w0 = np.random.default_rng(1).normal(size=4096) * 0.01
+    for batch in (128, 1, 7, 4096):
+        w, el, act = ctx.sgd_epoch(f, a, b, y, batch, 0.1, 1.0, w0)
+        ow, oel, oact = oracle.sgd_epoch(rp, idx, val, 4096, a, b, y, batch, 0.1, 1.0, w0)
+        assert act == oact
+        assert el.hex() == oel.hex()
+        assert (w.view(np.uint64) == ow.view(np.uint64)).all()
+
+
+def test_train_small_goldens(ctx):
+    from paper_2510_03243_b200 import Extractor, Workload
+    for c in golden("train_small.json"):
+        wl = Workload.synthesize(c["n"], c["seed"])
+        w, b, lt = ctx.train_pairwise(Extractor.make(dim=c["dim"]), wl.text, wl.offsets,
+                                      wl.output_len, delta=c["delta"], margin=c["margin"],
+                                      epochs=c["epochs"], batch=c["batch"], lr=c["lr"],
+                                      seed=c["seed"], pairs_per_epoch=c["ppe"])
+        assert [float(x).hex() for x in lt] == c["loss_trace"]
+        assert fnv64_array(w) == c["weights_fnv"]
+
+
+def test_readme_training_pipeline_bit_identical(ctx, ref):
+    """README recipe (gen 4000 seed 21, split 0.2, train seed 21): weights
+    FNV db7217cbd5a86b9b and the loss trace, trained on the GPU."""
+    from paper_2510_03243_b200 import Extractor
+    m = golden("models.json")
+    full = ref.synthesize(4000, 21)
+    tr, _ = ref.split(full, 0.2, 21)
+    w, b, lt = ctx.train_pairwise(Extractor.make(), tr.text, tr.offs, tr.output_len, seed=21)
+    assert fnv64_array(w) == m["readme"]["weights_fnv"]
+    assert [float(x).hex() for x in lt] == m["readme"]["loss_trace"]
+
+
+def test_c2_epoch_bit_identical(ctx):
+    """Config 2: one epoch on gen(8192, seed 21): loss 0.55296763305525443,
+    weights FNV f97c96a353829ee2."""
+    from paper_2510_03243_b200 import Extractor, Workload
+    m = golden("models.json")
+    wl = Workload.synthesize(8192, 21)
+    w, b, lt = ctx.train_pairwise(Extractor.make(), wl.text, wl.offsets, wl.output_len, seed=21,
+                                  epochs=1)
+    assert float(lt[0]).hex() == m["c2"]["loss0"]
+    assert fnv64_array(w) == m["c2"]["weights_fnv"] == "f97c96a353829ee2"
+
+
+def test_embedding_scores_exact(ctx, oracle):
+    from paper_2510_03243_b200 import MODE_EXACT, MODE_FAST, Extractor
+    rng = np.random.default_rng(4)
+    for norm in ("l2", "none"):
+        e = Extractor.make(dim=64, kind="embedding", norm=norm)
+        X = rng.normal(size=(300, 64))
+        X[0] = 0.0
+        w = rng.normal(size=64)
+        got = ctx.score_embeddings(e, X, w, 0.25, MODE_EXACT)
+        want = oracle.score_dense(oex(e), X, w, 0.25)
+        assert [x.hex() for x in got] == [x.hex() for x in want]
+        fast = ctx.score_embeddings(e, X, w, 0.25, MODE_FAST)
+        assert np.allclose(fast, want, rtol=0, atol=1e-4)
+
+
+def test_features_score_matches_linear_scorer(ctx, oracle):
+    from paper_2510_03243_b200 import Extractor, Workload
+    wl = Workload.synthesize(700, 8)
+    e = Extractor.make()
+    f = ctx.extract(e, wl.text, wl.offsets)
+    w = np.random.default_rng(5).normal(size=4096)
+    got = f.score(w, -0.5)
+    want = oracle.score_batch(oex(e), wl.text, wl.offsets, w, -0.5)
+    assert [x.hex() for x in got] == [x.hex() for x in want]
+
+
+def test_errors_are_loud(ctx):
+    from paper_2510_03243_b200 import Extractor, ParsError, pack_texts
+    arena, offs = pack_texts([b"a b"])
+    with pytest.raises(ParsError, match="feature extractor dimension is 0"):
+        ctx.score_text(Extractor.make(dim=0), arena, offs, np.zeros(1))
+    with pytest.raises(ParsError, match="word n-gram order must be >= 1"):
+        ctx.score_text(Extractor.make(word=(0,)), arena, offs, np.zeros(4096))
+    with pytest.raises(ParsError, match=r"train: delta 1 outside \[0, 1\)"):
+        ctx.train_pairwise(Extractor.make(), arena, offs, np.array([3]), delta=1.0)
