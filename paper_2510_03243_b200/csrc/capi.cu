@@ -49,7 +49,8 @@ struct pars_ctx {
   std::mutex mu;
   std::atomic<uint64_t> launches{0};
   // grow-only scratch
-  DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf;
+  DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
+      gscratch;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -180,6 +181,17 @@ int upload_weights(pars_ctx* ctx, const FeatConfig& cfg, const double* w, int mo
   return PARS_OK;
 }
 
+int attach_gscratch(pars_ctx* ctx, const FeatConfig& cfg, int fmode, FeatArgs* a) {
+  const size_t need = feat_global_scratch_bytes(cfg, fmode);
+  a->gscratch = nullptr;
+  a->gscratch_bytes = 0;
+  if (need == 0) return PARS_OK;
+  PARS_TRY(ensure(ctx->gscratch, need));
+  a->gscratch = static_cast<unsigned char*>(ctx->gscratch.p);
+  a->gscratch_bytes = ctx->gscratch.cap;
+  return PARS_OK;
+}
+
 int check_mode(int mode) {
   if (mode != PARS_MODE_EXACT_F64 && mode != PARS_MODE_FAST_F32) {
     set_error("unknown scoring mode %d", mode);
@@ -202,8 +214,9 @@ int score_chunk(pars_ctx* ctx, const FeatConfig& cfg, int mode, const uint8_t* d
   a.scores = d_scores;
   a.long_count = (int32_t*)ctx->longl.p;
   a.long_list = (int32_t*)ctx->longl.p + 4;
-  return launch_featurize(ctx, cfg, mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast,
-                          a, st);
+  const int fm = mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast;
+  PARS_TRY(attach_gscratch(ctx, cfg, fm, &a));
+  return launch_featurize(ctx, cfg, fm, a, st);
 }
 
 int ensure_dmin(pars_ctx* ctx, double delta, int64_t max_len, cudaStream_t st) {
@@ -277,7 +290,7 @@ void pars_ctx_destroy(pars_ctx* c) {
   cudaStreamSynchronize(c->copy_stream);
   DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
                     &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
-                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf};
+                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int k = 0; k < 2; ++k) {
@@ -402,8 +415,9 @@ int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* d_t
   a.scores = d_scores;
   a.long_count = (int32_t*)ctx->longl.p;
   a.long_list = (int32_t*)ctx->longl.p + 4;
-  return launch_featurize(ctx, cfg, mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast,
-                          a, st);
+  const int fm = mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast;
+  PARS_TRY(attach_gscratch(ctx, cfg, fm, &a));
+  return launch_featurize(ctx, cfg, fm, a, st);
 }
 
 int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex, const double* X, int64_t n,
@@ -516,6 +530,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
     a.out_nnz = d_nnz;
     a.long_count = (int32_t*)ctx->longl.p;
     a.long_list = (int32_t*)ctx->longl.p + 4;
+    if ((rc = attach_gscratch(ctx, cfg, kFeatCsr, &a)) != PARS_OK) return fail_free(rc);
     if ((rc = launch_featurize(ctx, cfg, kFeatCsr, a, st)) != PARS_OK) return fail_free(rc);
     std::vector<int32_t> nnz((size_t)n);
     cudaMemcpyAsync(nnz.data(), d_nnz, (size_t)n * 4, cudaMemcpyDeviceToHost, st);
@@ -639,7 +654,10 @@ int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths, i
   }
   *kept = *active = 0;
   *loss_sum = 0.0;
-  if (n <= 0) return PARS_OK;
+  if (n < 2) {
+    if (n == 1) coeff[0] = 0;
+    return PARS_OK;
+  }
   int64_t max_len = 0;
   std::vector<int32_t> L((size_t)n);
   for (int64_t i = 0; i < n; ++i) {

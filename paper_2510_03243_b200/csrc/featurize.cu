@@ -41,6 +41,7 @@ constexpr int kRing = 128;       // token ring entries per warp (start,end)
 constexpr int kProd = 256;       // exact-mode product buffer (doubles)
 constexpr uint32_t kBias2 = 0x80008000u;  // two biased 16-bit zero counters
 constexpr int64_t kPackedMaxFeatures = 32767;
+constexpr int kGlobalWarps = 1184;  // 148 SMs x 8 warps
 
 struct WarpSmem {
   uint32_t* counts;  // packed (2 x u16 biased) or wide (int32)
@@ -199,17 +200,21 @@ __device__ void hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_
   int64_t n_start = 0, n_end = 0, done = 0;
   uint32_t carry_ns = 0;
   const int64_t look = c.max_word > 1 ? c.max_word - 1 : 0;
-  for (int64_t wbase = beg & ~(int64_t)3; wbase < end; wbase += 128) {
-    const int64_t p = wbase + 4 * lane;
+  // windows are aligned on the ABSOLUTE address so every lane's 4-byte load
+  // is naturally aligned whatever the arena/offset alignment
+  const int64_t len = end - beg;
+  const int64_t mis = (int64_t)(reinterpret_cast<uintptr_t>(base) & 3u);
+  for (int64_t wrel = -mis; wrel < len; wrel += 128) {
+    const int64_t p = wrel + 4 * lane;  // relative to base; may be negative
     uint32_t word;
-    if (p >= beg && p + 4 <= end) {
-      word = __ldg(reinterpret_cast<const uint32_t*>(text + p));
+    if (p >= 0 && p + 4 <= len) {
+      word = __ldg(reinterpret_cast<const uint32_t*>(base + p));
     } else {
       word = 0x20202020u;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (p + k >= beg && p + k < end)
-          word = (word & ~(0xffu << (8 * k))) | ((uint32_t)text[p + k] << (8 * k));
+        if (p + k >= 0 && p + k < len)
+          word = (word & ~(0xffu << (8 * k))) | ((uint32_t)base[p + k] << (8 * k));
     }
     uint32_t ns = 0;
 #pragma unroll
@@ -223,7 +228,7 @@ __device__ void hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_
     int tot_s, tot_e;
     int ps = warp_excl_scan(__popc(starts), lane, &tot_s);
     int pe = warp_excl_scan(__popc(ends), lane, &tot_e);
-    const uint32_t rel = (uint32_t)(p - beg);
+    const uint32_t rel = (uint32_t)p;
     for (uint32_t m = starts; m; m &= m - 1) {
       int k = __ffs(m) - 1;
       S.tok_s[(n_start + ps++) % kRing] = rel + k;
@@ -242,7 +247,7 @@ __device__ void hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_
     }
   }
   if (carry_ns) {  // the last token runs to the end of the prompt
-    if (lane == 0) S.tok_e[n_end % kRing] = (uint32_t)(end - beg);
+    if (lane == 0) S.tok_e[n_end % kRing] = (uint32_t)len;
     ++n_end;
     __syncwarp();
   }
@@ -366,12 +371,15 @@ __host__ __device__ inline size_t warp_smem_bytes(const FeatConfig& c, int mode,
   return b;
 }
 
-template <bool POW2, bool WIDE, bool DEF, int MODE>
+// G: the per-warp table lives in a global-memory scratch region instead of
+// shared memory (dimensions whose histogram does not fit on chip).
+template <bool POW2, bool WIDE, bool DEF, int MODE, bool G>
 __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t per = warp_smem_bytes(c, MODE, WIDE);
-  unsigned char* my = smem + per * warp;
+  unsigned char* my = G ? a.gscratch + per * ((size_t)blockIdx.x * (blockDim.x >> 5) + warp)
+                        : smem + per * warp;
   WarpSmem S;
   S.counts = reinterpret_cast<uint32_t*>(my);
   S.bitmap = S.counts + count_words(c.dim, WIDE);
@@ -404,22 +412,33 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
   }
 }
 
+constexpr size_t kMaxSmemPerBlock = 200 * 1024;
+
 template <bool POW2, bool WIDE, bool DEF, int MODE>
 int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st,
                int64_t items_hint) {
   const size_t per = warp_smem_bytes(c, MODE, WIDE);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (per > kMaxSmemPerBlock) {
+    // global-memory tables: fixed grid, region per warp provided by the caller
+    if (!a.gscratch || a.gscratch_bytes < per * (size_t)kGlobalWarps) {
+      set_error("featurize: global scratch missing for dimension %u", c.dim);
+      return PARS_ERR_INVALID;
+    }
+    auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, true>;
+    kern<<<kGlobalWarps / 4, 128, 0, st>>>(c, a);
+    count_launch(ctx);
+    PARS_CUDA_CHECK(cudaGetLastError());
+    return PARS_OK;
+  }
   int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per));
   if (WIDE) warps = 1;
   const size_t smem = per * warps;
-  if (smem > 227 * 1024) {
-    set_error("feature dimension %u exceeds the shared-memory histogram (max 65536)", c.dim);
-    return PARS_ERR_UNSUPPORTED;
-  }
-  auto kern = featurize_kernel<POW2, WIDE, DEF, MODE>;
+  auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, false>;
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t want = ceil_div(std::max<int64_t>(items_hint, 1), warps);
@@ -546,6 +565,15 @@ bool build_feat_config(const pars_extractor* ex, FeatConfig* c) {
 
 size_t feat_warp_smem(const FeatConfig& cfg, int mode, bool wide) {
   return warp_smem_bytes(cfg, mode, wide);
+}
+
+size_t feat_global_scratch_bytes(const FeatConfig& cfg, int mode) {
+  size_t need = 0;
+  for (int wide = 0; wide < 2; ++wide) {
+    const size_t per = warp_smem_bytes(cfg, mode, wide != 0);
+    if (per > kMaxSmemPerBlock) need = std::max(need, per * (size_t)kGlobalWarps);
+  }
+  return need;
 }
 
 int launch_featurize(pars_ctx* ctx, const FeatConfig& c, int mode, const FeatArgs& a,

@@ -43,12 +43,17 @@ struct FeatArgs {
   // long-prompt hand-off (packed kernel -> wide kernel)
   int32_t* long_list;
   int32_t* long_count;
+  // per-warp tables in global memory for dimensions too large for smem
+  unsigned char* gscratch;
+  size_t gscratch_bytes;
 };
 
 bool build_feat_config(const pars_extractor* ex, FeatConfig* cfg);
 
 // Per-warp shared-memory bytes for a configuration (0 if unsupported).
 size_t feat_warp_smem(const FeatConfig& cfg, int mode, bool wide);
+// Global scratch needed when a table does not fit in shared memory (else 0).
+size_t feat_global_scratch_bytes(const FeatConfig& cfg, int mode);
 
 // Launches the packed kernel over all prompts followed by the wide kernel
 // over prompts whose feature count may exceed the 16-bit counters.
