@@ -60,42 +60,32 @@ __host__ __device__ inline uint32_t count_words(uint32_t dim, bool wide) {
   return wide ? ((dim + 7) & ~7u) : ((((dim + 1) / 2) + 3) & ~3u);
 }
 
+// One hashed feature: +-1 into the bucket counter. Returns via `sq` the exact
+// change of sum(count^2): (c+d)^2 - c^2 = 2cd + 1, from the atomic's old
+// value — so the L2 norm needs no second pass over the histogram. First
+// touch of a bucket sets its bit in the touched bitmap.
 template <bool WIDE>
-__device__ __forceinline__ void emit(const WarpSmem& S, uint32_t idx, bool pos) {
-  uint32_t old;
-  bool first;
+__device__ __forceinline__ void emit(const WarpSmem& S, uint32_t idx, bool pos, long long& sq) {
+  int oldc;
   if (WIDE) {
-    old = atomicAdd(&S.counts[idx], pos ? 1u : 0xffffffffu);
-    first = old == 0u;
+    oldc = (int)atomicAdd(&S.counts[idx], pos ? 1u : 0xffffffffu);
   } else {
-    uint32_t sh = (idx & 1u) << 4;
-    uint32_t d = pos ? (1u << sh) : (0u - (1u << sh));
-    old = atomicAdd(&S.counts[idx >> 1], d);
-    first = ((old >> sh) & 0xffffu) == 0x8000u;
+    const uint32_t sh = (idx & 1u) << 4;
+    const uint32_t d = pos ? (1u << sh) : (0u - (1u << sh));
+    const uint32_t old = atomicAdd(&S.counts[idx >> 1], d);
+    oldc = (int)((old >> sh) & 0xffffu) - 0x8000;
   }
-  if (first) atomicOr(&S.bitmap[idx >> 5], 1u << (idx & 31));
+  sq += 2ll * (pos ? oldc : -oldc) + 1;
+  if (oldc == 0) atomicOr(&S.bitmap[idx >> 5], 1u << (idx & 31));
 }
 
-// Counters of the 8 consecutive buckets [b0, b0+8) (b0 % 8 == 0): one
-// 16-byte shared load (packed) or two (wide).
 template <bool WIDE>
-__device__ __forceinline__ void load_group(const WarpSmem& S, uint32_t b0, int cnt[8]) {
-  if (WIDE) {
-    const uint4 u0 = *reinterpret_cast<const uint4*>(S.counts + b0);
-    const uint4 u1 = *reinterpret_cast<const uint4*>(S.counts + b0 + 4);
-    cnt[0] = (int)u0.x; cnt[1] = (int)u0.y; cnt[2] = (int)u0.z; cnt[3] = (int)u0.w;
-    cnt[4] = (int)u1.x; cnt[5] = (int)u1.y; cnt[6] = (int)u1.z; cnt[7] = (int)u1.w;
-  } else {
-    const uint4 u = *reinterpret_cast<const uint4*>(S.counts + (b0 >> 1));
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      cnt[2 * j] = (int)(w[j] & 0xffffu) - 0x8000;
-      cnt[2 * j + 1] = (int)(w[j] >> 16) - 0x8000;
-    }
-  }
+__device__ __forceinline__ int count_of(const WarpSmem& S, uint32_t idx) {
+  if (WIDE) return (int)S.counts[idx];
+  return (int)reinterpret_cast<const uint16_t*>(S.counts)[idx] - 0x8000;  // little-endian halves
 }
 
+// Reset the 8 counters of buckets [b0, b0+8) (b0 % 8 == 0).
 template <bool WIDE>
 __device__ __forceinline__ void clear_group(const WarpSmem& S, uint32_t b0) {
   if (WIDE) {
@@ -130,45 +120,59 @@ struct H<false> {
 
 __device__ __forceinline__ uint32_t ld_byte(const uint8_t* p) { return __ldg(p); }
 
-// Hash token `t` (ring index) and everything that starts at it.
+// Hash token `t` (ring index) and every n-gram that starts at it.
 template <bool POW2, bool WIDE, bool DEF>
 __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& S,
-                                           const uint8_t* base, int64_t t,
-                                           int64_t ntok_avail) {
+                                           const uint8_t* base, uint32_t t, uint32_t ntok_avail,
+                                           long long& sq) {
   using HT = H<POW2>;
   using T = typename HT::T;
-  const uint32_t s = S.tok_s[t % kRing], e = S.tok_e[t % kRing];
+  const uint32_t s = S.tok_s[t & (kRing - 1)], e = S.tok_e[t & (kRing - 1)];
   const uint8_t* tp = base + s;
   const int len = (int)(e - s);
   if (DEF) {
-    // word {1} + char {3} in one pass over the token bytes
+    // word {1} + char {3} in one pass; two bytes per iteration so the two
+    // trigram hashes of a step are independent (ILP)
     T hw = HT::seed(c.word_salt[0]);
     const T hc0 = HT::seed(c.char_salt[0]);
     uint32_t b2 = 0, b1 = 0;
-    for (int i = 0; i < len; ++i) {
-      uint32_t b = ld_byte(tp + i);
-      hw = HT::step(hw, b);
+    int i = 0;
+    for (; i + 2 <= len; i += 2) {
+      const uint32_t x = ld_byte(tp + i), y = ld_byte(tp + i + 1);
+      hw = HT::step(HT::step(hw, x), y);
       if (i >= 2) {
-        T h = HT::step(HT::step(HT::step(hc0, b2), b1), b);
-        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
+        const T h = HT::step(HT::step(HT::step(hc0, b2), b1), x);
+        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
       }
-      b2 = b1;
-      b1 = b;
+      if (i >= 1) {
+        const T h = HT::step(HT::step(HT::step(hc0, b1), x), y);
+        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+      }
+      b2 = x;
+      b1 = y;
+    }
+    if (i < len) {
+      const uint32_t x = ld_byte(tp + i);
+      hw = HT::step(hw, x);
+      if (i >= 2) {
+        const T h = HT::step(HT::step(HT::step(hc0, b2), b1), x);
+        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+      }
     }
     hw = HT::step(hw, 0x1fu);
-    emit<WIDE>(S, HT::bucket(hw, c), (hw & 1) != 0);
+    emit<WIDE>(S, HT::bucket(hw, c), (hw & 1) != 0, sq);
     return;
   }
   for (int k = 0; k < c.n_word; ++k) {
     const int order = c.word[k];
-    if (t + order - 1 >= ntok_avail) continue;  // n-gram runs past the last token
+    if (t + (uint32_t)order - 1 >= ntok_avail) continue;  // n-gram runs past the last token
     T h = HT::seed(c.word_salt[k]);
     for (int j = 0; j < order; ++j) {
-      const uint32_t sj = S.tok_s[(t + j) % kRing], ej = S.tok_e[(t + j) % kRing];
+      const uint32_t sj = S.tok_s[(t + j) & (kRing - 1)], ej = S.tok_e[(t + j) & (kRing - 1)];
       for (uint32_t q = sj; q < ej; ++q) h = HT::step(h, ld_byte(base + q));
       h = HT::step(h, 0x1fu);
     }
-    emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
+    emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
   }
   for (int k = 0; k < c.n_char; ++k) {
     const int order = c.chr[k];
@@ -176,7 +180,7 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
     for (int i = 0; i + order <= len; ++i) {
       T h = seed;
       for (int j = 0; j < order; ++j) h = HT::step(h, ld_byte(tp + i + j));
-      emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
+      emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
     }
   }
 }
@@ -192,30 +196,38 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   return x - v;
 }
 
-// Tokenise + hash one prompt into the warp's histogram.
+// 4 text bytes at base[p .. p+4) (p relative, may be out of range: spaces).
+__device__ __forceinline__ uint32_t load_word(const uint8_t* base, int64_t p, int64_t len) {
+  if (p >= 0 && p + 4 <= len) return __ldg(reinterpret_cast<const uint32_t*>(base + p));
+  uint32_t word = 0x20202020u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (p + k >= 0 && p + k < len)
+      word = (word & ~(0xffu << (8 * k))) | ((uint32_t)base[p + k] << (8 * k));
+  return word;
+}
+
+// Tokenise + hash one prompt into the warp's histogram; returns this lane's
+// share of sum(count^2).
 template <bool POW2, bool WIDE, bool DEF>
-__device__ void hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_t* text,
-                            int64_t beg, int64_t end, int lane) {
+__device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_t* text,
+                                 int64_t beg, int64_t end, int lane) {
   const uint8_t* base = text + beg;
-  int64_t n_start = 0, n_end = 0, done = 0;
+  uint32_t n_start = 0, n_end = 0, done = 0;
   uint32_t carry_ns = 0;
-  const int64_t look = c.max_word > 1 ? c.max_word - 1 : 0;
+  long long sq = 0;
+  const uint32_t look = c.max_word > 1 ? (uint32_t)c.max_word - 1 : 0;
+  const unsigned lt = (1u << lane) - 1u;
   // windows are aligned on the ABSOLUTE address so every lane's 4-byte load
-  // is naturally aligned whatever the arena/offset alignment
+  // is naturally aligned whatever the arena/offset alignment; the next
+  // window's word is loaded before the current one is processed.
   const int64_t len = end - beg;
   const int64_t mis = (int64_t)(reinterpret_cast<uintptr_t>(base) & 3u);
+  uint32_t next = load_word(base, -mis + 4 * lane, len);
   for (int64_t wrel = -mis; wrel < len; wrel += 128) {
     const int64_t p = wrel + 4 * lane;  // relative to base; may be negative
-    uint32_t word;
-    if (p >= 0 && p + 4 <= len) {
-      word = __ldg(reinterpret_cast<const uint32_t*>(base + p));
-    } else {
-      word = 0x20202020u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (p + k >= 0 && p + k < len)
-          word = (word & ~(0xffu << (8 * k))) | ((uint32_t)base[p + k] << (8 * k));
-    }
+    const uint32_t word = next;
+    if (wrel + 128 < len) next = load_word(base, p + 128, len);
     uint32_t ns = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) ns |= (is_space((word >> (8 * k)) & 0xffu) ? 0u : 1u) << k;
@@ -225,40 +237,46 @@ __device__ void hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_
     const uint32_t starts = ns & ~nsprev;
     const uint32_t ends = ~ns & nsprev & 0xfu;  // byte k is the exclusive end
     carry_ns = __shfl_sync(kFull, ns >> 3, 31);
-    int tot_s, tot_e;
-    int ps = warp_excl_scan(__popc(starts), lane, &tot_s);
-    int pe = warp_excl_scan(__popc(ends), lane, &tot_e);
+    // order of this lane's boundaries among the window's, via 8 ballots
+    uint32_t ps = 0, pe = 0, ts = 0, te = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t bs = __ballot_sync(kFull, (starts >> k) & 1u);
+      const uint32_t be = __ballot_sync(kFull, (ends >> k) & 1u);
+      ps += __popc(bs & lt);
+      pe += __popc(be & lt);
+      ts += __popc(bs);
+      te += __popc(be);
+    }
     const uint32_t rel = (uint32_t)p;
-    for (uint32_t m = starts; m; m &= m - 1) {
-      int k = __ffs(m) - 1;
-      S.tok_s[(n_start + ps++) % kRing] = rel + k;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if ((starts >> k) & 1u) S.tok_s[(n_start + ps++) & (kRing - 1)] = rel + k;
+      if ((ends >> k) & 1u) S.tok_e[(n_end + pe++) & (kRing - 1)] = rel + k;
     }
-    for (uint32_t m = ends; m; m &= m - 1) {
-      int k = __ffs(m) - 1;
-      S.tok_e[(n_end + pe++) % kRing] = rel + k;
-    }
-    n_start += tot_s;
-    n_end += tot_e;
+    n_start += ts;
+    n_end += te;
     __syncwarp();
     while (n_end - done >= 32 + look) {
-      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end);
+      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end, sq);
       done += 32;
       __syncwarp();
     }
   }
   if (carry_ns) {  // the last token runs to the end of the prompt
-    if (lane == 0) S.tok_e[n_end % kRing] = (uint32_t)len;
+    if (lane == 0) S.tok_e[n_end & (kRing - 1)] = (uint32_t)len;
     ++n_end;
     __syncwarp();
   }
   while (done < n_end) {
-    if (done + lane < n_end) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end);
+    if (done + lane < n_end) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end, sq);
     done += 32;
   }
   __syncwarp();
+  return sq;
 }
 
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
@@ -270,27 +288,16 @@ __device__ __forceinline__ float warp_sum_f32(float v) {
 }
 
 // Walk the touched buckets in ascending order and finish the prompt.
-// Lane l of an 8-word bitmap window owns buckets [b0, b0+8), so lane order is
-// bucket order; entries are compacted with a warp scan.
+// Window = 8 bitmap words (256 buckets); lane l owns byte (l&3) of word
+// (l>>2), i.e. buckets [b0, b0+8), so lane order is bucket order. A lane's
+// output position is the popcount of the window's bits before its own,
+// computed from two broadcast 16-byte loads (no shuffle scan).
 template <bool WIDE, int MODE>
 __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const FeatArgs& a,
-                              int64_t i, int lane) {
+                              int64_t i, int lane, long long sq_lane) {
   const uint32_t nbw = bitmap_words_padded(c.dim);
   const int sub = lane & 3, wsel = lane >> 2;
-  // pass A: exact integer sum of squares (features.cpp:113-116)
-  unsigned long long sq = 0;
-  if (c.norm) {
-    for (uint32_t wb = 0; wb < nbw; wb += 8) {
-      const uint32_t bits = (S.bitmap[wb + wsel] >> (8 * sub)) & 0xffu;
-      if (bits) {
-        int cnt[8];
-        load_group<WIDE>(S, (wb + wsel) * 32 + 8 * sub, cnt);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sq += (unsigned long long)((long long)cnt[j] * cnt[j]);
-      }
-    }
-    sq = warp_sum_u64(sq);
-  }
+  const long long sq = c.norm ? warp_sum_i64(sq_lane) : 0;  // features.cpp:113-116, exact
   const double inv = (c.norm && sq > 0) ? __ddiv_rn(1.0, __dsqrt_rn((double)sq)) : 1.0;
 
   double chain = 0.0;  // lane 0: sequential fp64 dot (exact mode)
@@ -298,32 +305,36 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
   int64_t row_pos = 0;
   const int64_t slot = (MODE == kFeatCsr) ? a.slot_base[i] : 0;
   for (uint32_t wb = 0; wb < nbw; wb += 8) {
-    const uint32_t bits = (S.bitmap[wb + wsel] >> (8 * sub)) & 0xffu;
-    if (__ballot_sync(kFull, bits != 0) == 0) continue;
-    __syncwarp();
-    if (sub == 0) S.bitmap[wb + wsel] = 0u;
-    const uint32_t b0 = (wb + wsel) * 32 + 8 * sub;
-    int cnt[8];
-    uint32_t nz = 0;
-    if (bits) {
-      load_group<WIDE>(S, b0, cnt);
-      clear_group<WIDE>(S, b0);
+    const uint4 q0 = *reinterpret_cast<const uint4*>(S.bitmap + wb);
+    const uint4 q1 = *reinterpret_cast<const uint4*>(S.bitmap + wb + 4);
+    const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    if ((q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w) == 0) continue;
+    uint32_t before = 0, total = 0, mine = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) nz |= (cnt[j] != 0 ? 1u : 0u) << j;  // erase zeros (:110)
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t pk = __popc(wv[k]);
+      total += pk;
+      before += (k < wsel) ? pk : 0u;
+      mine = (k == wsel) ? wv[k] : mine;
     }
-    int total;
-    const int pos = warp_excl_scan(__popc(nz), lane, &total);
-    if (total == 0) continue;
+    before += __popc(mine & ((1u << (8 * sub)) - 1u));
+    const uint32_t bits = (mine >> (8 * sub)) & 0xffu;
+    const uint32_t b0 = (wb + wsel) * 32 + 8 * sub;
     if (MODE == kFeatScoreExact) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (nz & (1u << j)) {
-          const double v = c.norm ? __dmul_rn((double)cnt[j], inv) : (double)cnt[j];
-          S.prod[pos + __popc(nz & ((1u << j) - 1))] = __dmul_rn(__ldg(a.w64 + b0 + j), v);
-        }
+      // zero-count buckets contribute +0.0, which never changes the chain
+      // (the running sum starts at +0.0 and can never become -0.0 under
+      // round-to-nearest), so no compaction is needed
+      uint32_t pos = before;
+      for (uint32_t m = bits; m; m &= m - 1) {
+        const uint32_t idx = b0 + __ffs(m) - 1;
+        const int cnt = count_of<WIDE>(S, idx);
+        const double v = c.norm ? __dmul_rn((double)cnt, inv) : (double)cnt;
+        S.prod[pos++] = cnt != 0 ? __dmul_rn(__ldg(a.w64 + idx), v) : 0.0;
+      }
+      if (bits) clear_group<WIDE>(S, b0);
       __syncwarp();
       if (lane == 0) {
-        int k = 0;
+        uint32_t k = 0;
         for (; k + 4 <= total; k += 4) {
           const double2 p01 = *reinterpret_cast<const double2*>(S.prod + k);
           const double2 p23 = *reinterpret_cast<const double2*>(S.prod + k + 2);
@@ -334,13 +345,25 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
         }
         for (; k < total; ++k) chain = __dadd_rn(chain, S.prod[k]);
       }
-      __syncwarp();
     } else if (MODE == kFeatScoreFast) {
       const float finv = (float)inv;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (nz & (1u << j)) facc += __ldg(a.w32 + b0 + j) * ((float)cnt[j] * finv);
+      for (uint32_t m = bits; m; m &= m - 1) {
+        const uint32_t idx = b0 + __ffs(m) - 1;
+        facc += __ldg(a.w32 + idx) * ((float)count_of<WIDE>(S, idx) * finv);
+      }
+      if (bits) clear_group<WIDE>(S, b0);
     } else {
+      // CSR rows must not contain erased zeros (features.cpp:110): compact
+      int cnt[8];
+      uint32_t nz = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = ((bits >> j) & 1u) ? count_of<WIDE>(S, b0 + j) : 0;
+        nz |= (cnt[j] != 0 ? 1u : 0u) << j;
+      }
+      if (bits) clear_group<WIDE>(S, b0);
+      int tot;
+      const int pos = warp_excl_scan(__popc(nz), lane, &tot);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (nz & (1u << j)) {
@@ -349,8 +372,10 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
           a.out_idx[o] = b0 + j;
           a.out_val[o] = v;
         }
-      row_pos += total;
+      row_pos += tot;
     }
+    __syncwarp();
+    if (sub == 0) S.bitmap[wb + wsel] = 0u;
   }
   if (MODE == kFeatScoreExact) {
     if (lane == 0) a.scores[i] = __dadd_rn(chain, a.bias);
@@ -407,8 +432,8 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
         continue;
       }
     }
-    hash_prompt<POW2, WIDE, DEF>(c, S, a.text, beg, end, lane);
-    finish_prompt<WIDE, MODE>(c, S, a, i, lane);
+    const long long sq = hash_prompt<POW2, WIDE, DEF>(c, S, a.text, beg, end, lane);
+    finish_prompt<WIDE, MODE>(c, S, a, i, lane, sq);
   }
 }
 
@@ -433,14 +458,32 @@ int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream
     PARS_CUDA_CHECK(cudaGetLastError());
     return PARS_OK;
   }
-  int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per));
-  if (WIDE) warps = 1;
-  const size_t smem = per * warps;
   auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, false>;
+  // warps per CTA: the choice that keeps the most warps resident per SM
+  // (the per-warp histogram makes shared memory the occupancy limiter)
+  int warps = 1, per_sm = 1, best = 0;
+  for (int w : {8, 4, 2, 1}) {
+    if (WIDE && w != 1) continue;
+    const size_t sm_bytes = per * w;
+    if (sm_bytes > kMaxSmemPerBlock) continue;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes) !=
+        cudaSuccess)
+      continue;
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32, sm_bytes);
+    if (b * w > best) {
+      best = b * w;
+      warps = w;
+      per_sm = b;
+    }
+  }
+  cudaGetLastError();
+  if (best == 0) {
+    set_error("featurize: no launchable configuration for dimension %u", c.dim);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  const size_t smem = per * warps;
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
-  if (per_sm < 1) per_sm = 1;
   int64_t want = ceil_div(std::max<int64_t>(items_hint, 1), warps);
   int64_t grid = std::min<int64_t>(want, (int64_t)sms * per_sm);
   if (WIDE) grid = (int64_t)sms * per_sm;  // count known only on device
