@@ -50,7 +50,7 @@ struct pars_ctx {
   std::atomic<uint64_t> launches{0};
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
-      gscratch;
+      gscratch, lists;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -181,14 +181,24 @@ int upload_weights(pars_ctx* ctx, const FeatConfig& cfg, const double* w, int mo
   return PARS_OK;
 }
 
-int attach_gscratch(pars_ctx* ctx, const FeatConfig& cfg, int fmode, FeatArgs* a) {
-  const size_t need = feat_global_scratch_bytes(cfg, fmode);
+int attach_scratch(pars_ctx* ctx, const FeatConfig& cfg, int fmode, int64_t n, FeatArgs* a) {
+  size_t gs = 0, ls = 0;
+  PARS_TRY(feat_scratch_bytes(cfg, fmode, n, &gs, &ls));
   a->gscratch = nullptr;
   a->gscratch_bytes = 0;
-  if (need == 0) return PARS_OK;
-  PARS_TRY(ensure(ctx->gscratch, need));
-  a->gscratch = static_cast<unsigned char*>(ctx->gscratch.p);
-  a->gscratch_bytes = ctx->gscratch.cap;
+  a->lists = nullptr;
+  a->lists_bytes = 0;
+  a->list_cap = feat_list_cap_words(cfg);
+  if (gs) {
+    PARS_TRY(ensure(ctx->gscratch, gs));
+    a->gscratch = static_cast<unsigned char*>(ctx->gscratch.p);
+    a->gscratch_bytes = ctx->gscratch.cap;
+  }
+  if (ls) {
+    PARS_TRY(ensure(ctx->lists, ls));
+    a->lists = static_cast<uint32_t*>(ctx->lists.p);
+    a->lists_bytes = ctx->lists.cap;
+  }
   return PARS_OK;
 }
 
@@ -215,7 +225,7 @@ int score_chunk(pars_ctx* ctx, const FeatConfig& cfg, int mode, const uint8_t* d
   a.long_count = (int32_t*)ctx->longl.p;
   a.long_list = (int32_t*)ctx->longl.p + 4;
   const int fm = mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast;
-  PARS_TRY(attach_gscratch(ctx, cfg, fm, &a));
+  PARS_TRY(attach_scratch(ctx, cfg, fm, n, &a));
   return launch_featurize(ctx, cfg, fm, a, st);
 }
 
@@ -290,7 +300,7 @@ void pars_ctx_destroy(pars_ctx* c) {
   cudaStreamSynchronize(c->copy_stream);
   DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
                     &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
-                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch};
+                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int k = 0; k < 2; ++k) {
@@ -416,7 +426,7 @@ int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* d_t
   a.long_count = (int32_t*)ctx->longl.p;
   a.long_list = (int32_t*)ctx->longl.p + 4;
   const int fm = mode == PARS_MODE_EXACT_F64 ? kFeatScoreExact : kFeatScoreFast;
-  PARS_TRY(attach_gscratch(ctx, cfg, fm, &a));
+  PARS_TRY(attach_scratch(ctx, cfg, fm, n, &a));
   return launch_featurize(ctx, cfg, fm, a, st);
 }
 
@@ -530,7 +540,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
     a.out_nnz = d_nnz;
     a.long_count = (int32_t*)ctx->longl.p;
     a.long_list = (int32_t*)ctx->longl.p + 4;
-    if ((rc = attach_gscratch(ctx, cfg, kFeatCsr, &a)) != PARS_OK) return fail_free(rc);
+    if ((rc = attach_scratch(ctx, cfg, kFeatCsr, n, &a)) != PARS_OK) return fail_free(rc);
     if ((rc = launch_featurize(ctx, cfg, kFeatCsr, a, st)) != PARS_OK) return fail_free(rc);
     std::vector<int32_t> nnz((size_t)n);
     cudaMemcpyAsync(nnz.data(), d_nnz, (size_t)n * 4, cudaMemcpyDeviceToHost, st);

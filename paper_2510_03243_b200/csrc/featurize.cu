@@ -1,4 +1,4 @@
-// Fused hashing featurizer + linear score head, one warp per prompt.
+// Fused hashing featurizer + linear score head.
 //
 // Reference semantics (all in /root/reference/proj/src/features.cpp):
 //   split_tokens :36-49 (C-locale isspace), word n-grams :80-92 (FNV-1a over
@@ -7,24 +7,28 @@
 //   sign = h&1 ? +1 : -1), sort+merge :102-109, erase zeros :110,
 //   L2 :113-120; scorer.cpp:36-42 + features.hpp:31-35 for the dot + bias.
 //
-// B200 design:
-//   * one warp owns one prompt at a time; the text is streamed through the
-//     warp 128 bytes per step (one aligned 4-byte load per lane), whitespace
-//     transitions are found with lane bitmasks + shuffles and compacted into a
-//     per-warp token ring in shared memory;
-//   * lane t hashes token t of a 32-token batch (word n-gram + all char
+// B200 design (one warp owns one prompt at a time):
+//   * tokenise: the prompt streams through the warp in 128-byte windows (one
+//     aligned 32-bit load per lane, next window prefetched); whitespace
+//     transitions come from lane bit masks, are ranked with 4 ballots and
+//     written to a per-warp transition ring in shared memory (transitions
+//     strictly alternate start/end, so token t = ring[2t], ring[2t+1]);
+//   * hash: lane t hashes token t of a 32-token batch (word n-gram + all char
 //     n-grams of that token). For power-of-two dims only the low log2(dim)+1
-//     bits of the 64-bit FNV state are ever observed, and FNV's xor/multiply
-//     are closed mod 2^32, so the hash runs in 32-bit arithmetic
-//     (P mod 2^32 = 0x1b3): one LOP3 + one IMAD per byte;
-//   * features are histogrammed into a per-warp shared-memory table of
-//     16-bit biased counters packed two per word (atomicAdd), with a
-//     touched-bucket bitmap set on first touch. Integer sums are exact and
-//     order-free, so the merge/erase of the reference needs no sort;
-//   * the bitmap is walked in ascending bucket order: L2 from the exact
-//     integer sum of squares, products w[idx]*v computed lane-parallel, and
-//     the bit-exact fp64 dot is a sequential __dadd_rn chain over the
-//     ascending products (exact mode) or a warp tree reduction (fast mode).
+//     bits of the 64-bit FNV state are observed and FNV is closed mod 2^32,
+//     so the hash runs in 32-bit arithmetic (P mod 2^32 = 0x1b3);
+//   * histogram: per-warp shared-memory table of biased 16-bit counters, two
+//     per word (atomicAdd); prompts with more than 32,767 hashed features are
+//     routed to the 32-bit-counter variant (so a counter can never wrap). The
+//     atomics' old values give the exact change of sum(count^2) (2cd+1), so
+//     the L2 norm needs no extra pass; a bitmap records first touches;
+//   * finish (exact fp64 mode): the touched buckets are walked in ascending
+//     order into a per-warp list (idx, count) in L2-resident global scratch;
+//     after a group of 16 prompts, lane k runs the sequential __dadd_rn chain
+//     of prompt k (products w[idx] * (count * inv) with __dmul_rn), so 16
+//     bit-exact chains proceed in parallel instead of one lane at a time.
+//     Fast fp32 mode reduces lane-parallel products with a warp tree; CSR
+//     mode compacts (idx, value) rows.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,33 +41,49 @@ namespace pars_b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRing = 128;       // token ring entries per warp (start,end)
-constexpr int kProd = 256;       // exact-mode product buffer (doubles)
-constexpr uint32_t kBias2 = 0x80008000u;  // two biased 16-bit zero counters
-constexpr int64_t kPackedMaxFeatures = 32767;
-constexpr int kGlobalWarps = 1184;  // 148 SMs x 8 warps
+constexpr int kRing = 256;                   // transition ring entries per warp
+constexpr int kGroup = 16;                   // prompts per exact chain group
+constexpr uint32_t kBias2 = 0x80008000u;     // two biased 16-bit zero counters
+constexpr int64_t kNarrowMaxFeatures = 32767;  // |count| <= features: 16 bits cannot wrap
+constexpr size_t kMaxSmemPerBlock = 200 * 1024;
 
 struct WarpSmem {
-  uint32_t* counts;  // packed (2 x u16 biased) or wide (int32)
+  uint32_t* counts;  // narrow: 2 x u16 biased per word; wide: int32
   uint32_t* bitmap;  // touched buckets
-  uint32_t* tok_s;   // ring: token start (relative to prompt begin)
-  uint32_t* tok_e;   // ring: token end (exclusive)
-  double* prod;      // exact-mode product buffer
+  uint32_t* ring;    // token transitions (relative byte offsets)
 };
 
 __host__ __device__ inline uint32_t bitmap_words_padded(uint32_t dim) {
   uint32_t w = (dim + 31) / 32;
   return (w + 7) & ~7u;
 }
-// Rounded so that every 8-bucket group read/clear stays inside the table.
+// Covers every 8-bucket group that can be touched (clears are per group).
 __host__ __device__ inline uint32_t count_words(uint32_t dim, bool wide) {
-  return wide ? ((dim + 7) & ~7u) : ((((dim + 1) / 2) + 3) & ~3u);
+  return wide ? ((dim + 7) / 8) * 8 : ((dim + 7) / 8) * 4;  // multiple of 4 words (16 B)
+}
+__host__ __device__ inline size_t warp_table_bytes(const FeatConfig& c, bool wide) {
+  return (size_t)count_words(c.dim, wide) * 4 + (size_t)bitmap_words_padded(c.dim) * 4 +
+         (size_t)kRing * 4;
+}
+// list entry: packed u32 (idx << 16 | count + 0x8000) for narrow counters and
+// dim <= 65536, else two u32 (idx, count)
+__host__ __device__ inline uint32_t entry_words(const FeatConfig& c, bool wide) {
+  return (!wide && c.dim <= 65536u) ? 1u : 2u;
+}
+// Per-warp list arena (u32 words), the same stride for the narrow and the
+// wide kernel: a full group of typical prompts, and never less than one
+// prompt's worst case (dim entries).
+__host__ inline uint32_t list_cap_words(const FeatConfig& c) {
+  uint32_t cap = 0;
+  for (int wide = 0; wide < 2; ++wide) {
+    const uint32_t ew = entry_words(c, wide != 0);
+    cap = std::max<uint32_t>(cap, std::max<uint32_t>(c.dim * ew, kGroup * 512u * ew) + 4u * ew);
+  }
+  return (cap + 3u) & ~3u;
 }
 
-// One hashed feature: +-1 into the bucket counter. Returns via `sq` the exact
-// change of sum(count^2): (c+d)^2 - c^2 = 2cd + 1, from the atomic's old
-// value — so the L2 norm needs no second pass over the histogram. First
-// touch of a bucket sets its bit in the touched bitmap.
+// One hashed feature. `sq` accumulates the exact change of sum(count^2):
+// (c+d)^2 - c^2 = 2cd + 1 with c the atomic's old value.
 template <bool WIDE>
 __device__ __forceinline__ void emit(const WarpSmem& S, uint32_t idx, bool pos, long long& sq) {
   int oldc;
@@ -96,6 +116,14 @@ __device__ __forceinline__ void clear_group(const WarpSmem& S, uint32_t b0) {
   }
 }
 
+template <bool WIDE>
+__device__ void clear_all(const WarpSmem& S, const FeatConfig& c, int lane) {
+  const uint32_t cw = count_words(c.dim, WIDE);
+  for (uint32_t k = lane; k < cw; k += 32) S.counts[k] = WIDE ? 0u : kBias2;
+  for (uint32_t k = lane; k < bitmap_words_padded(c.dim); k += 32) S.bitmap[k] = 0u;
+  __syncwarp();
+}
+
 // Hash state: 32-bit when only the low bits matter (power-of-two dims).
 template <bool POW2>
 struct H;
@@ -120,19 +148,19 @@ struct H<false> {
 
 __device__ __forceinline__ uint32_t ld_byte(const uint8_t* p) { return __ldg(p); }
 
-// Hash token `t` (ring index) and every n-gram that starts at it.
+// Hash token `t` and every n-gram that starts at it.
 template <bool POW2, bool WIDE, bool DEF>
 __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& S,
-                                           const uint8_t* base, uint32_t t, uint32_t ntok_avail,
+                                           const uint8_t* base, uint32_t t, uint32_t ntok,
                                            long long& sq) {
   using HT = H<POW2>;
   using T = typename HT::T;
-  const uint32_t s = S.tok_s[t & (kRing - 1)], e = S.tok_e[t & (kRing - 1)];
+  const uint32_t s = S.ring[(2 * t) & (kRing - 1)], e = S.ring[(2 * t + 1) & (kRing - 1)];
   const uint8_t* tp = base + s;
   const int len = (int)(e - s);
   if (DEF) {
     // word {1} + char {3} in one pass; two bytes per iteration so the two
-    // trigram hashes of a step are independent (ILP)
+    // trigram hashes of a step are independent
     T hw = HT::seed(c.word_salt[0]);
     const T hc0 = HT::seed(c.char_salt[0]);
     uint32_t b2 = 0, b1 = 0;
@@ -143,10 +171,8 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
       if (i >= 2) {
         const T h = HT::step(HT::step(HT::step(hc0, b2), b1), x);
         emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
-      }
-      if (i >= 1) {
-        const T h = HT::step(HT::step(HT::step(hc0, b1), x), y);
-        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+        const T g = HT::step(HT::step(HT::step(hc0, b1), x), y);
+        emit<WIDE>(S, HT::bucket(g, c), (g & 1) != 0, sq);
       }
       b2 = x;
       b1 = y;
@@ -165,10 +191,11 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
   }
   for (int k = 0; k < c.n_word; ++k) {
     const int order = c.word[k];
-    if (t + (uint32_t)order - 1 >= ntok_avail) continue;  // n-gram runs past the last token
+    if (t + (uint32_t)order > ntok) continue;  // n-gram runs past the last token
     T h = HT::seed(c.word_salt[k]);
     for (int j = 0; j < order; ++j) {
-      const uint32_t sj = S.tok_s[(t + j) & (kRing - 1)], ej = S.tok_e[(t + j) & (kRing - 1)];
+      const uint32_t sj = S.ring[(2 * (t + j)) & (kRing - 1)];
+      const uint32_t ej = S.ring[(2 * (t + j) + 1) & (kRing - 1)];
       for (uint32_t q = sj; q < ej; ++q) h = HT::step(h, ld_byte(base + q));
       h = HT::step(h, 0x1fu);
     }
@@ -210,18 +237,15 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t* base, int64_t p, in
 // Tokenise + hash one prompt into the warp's histogram; returns this lane's
 // share of sum(count^2).
 template <bool POW2, bool WIDE, bool DEF>
-__device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_t* text,
-                                 int64_t beg, int64_t end, int lane) {
-  const uint8_t* base = text + beg;
-  uint32_t n_start = 0, n_end = 0, done = 0;
+__device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_t* base,
+                                 int64_t len, int lane) {
+  uint32_t n_tr = 0, done = 0;
   uint32_t carry_ns = 0;
   long long sq = 0;
   const uint32_t look = c.max_word > 1 ? (uint32_t)c.max_word - 1 : 0;
   const unsigned lt = (1u << lane) - 1u;
-  // windows are aligned on the ABSOLUTE address so every lane's 4-byte load
-  // is naturally aligned whatever the arena/offset alignment; the next
-  // window's word is loaded before the current one is processed.
-  const int64_t len = end - beg;
+  // windows are aligned on the ABSOLUTE address so each lane's 4-byte load
+  // is naturally aligned whatever the arena/offset alignment
   const int64_t mis = (int64_t)(reinterpret_cast<uintptr_t>(base) & 3u);
   uint32_t next = load_word(base, -mis + 4 * lane, len);
   for (int64_t wrel = -mis; wrel < len; wrel += 128) {
@@ -233,43 +257,33 @@ __device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const u
     for (int k = 0; k < 4; ++k) ns |= (is_space((word >> (8 * k)) & 0xffu) ? 0u : 1u) << k;
     uint32_t prev = __shfl_up_sync(kFull, ns >> 3, 1);
     if (lane == 0) prev = carry_ns;
-    const uint32_t nsprev = ((ns << 1) | prev) & 0xfu;
-    const uint32_t starts = ns & ~nsprev;
-    const uint32_t ends = ~ns & nsprev & 0xfu;  // byte k is the exclusive end
+    const uint32_t trm = (ns ^ ((ns << 1) | prev)) & 0xfu;  // transitions at byte k
     carry_ns = __shfl_sync(kFull, ns >> 3, 31);
-    // order of this lane's boundaries among the window's, via 8 ballots
-    uint32_t ps = 0, pe = 0, ts = 0, te = 0;
+    uint32_t rank = 0, tot = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t bs = __ballot_sync(kFull, (starts >> k) & 1u);
-      const uint32_t be = __ballot_sync(kFull, (ends >> k) & 1u);
-      ps += __popc(bs & lt);
-      pe += __popc(be & lt);
-      ts += __popc(bs);
-      te += __popc(be);
+      const uint32_t b = __ballot_sync(kFull, (trm >> k) & 1u);
+      rank += __popc(b & lt);
+      tot += __popc(b);
     }
     const uint32_t rel = (uint32_t)p;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if ((starts >> k) & 1u) S.tok_s[(n_start + ps++) & (kRing - 1)] = rel + k;
-      if ((ends >> k) & 1u) S.tok_e[(n_end + pe++) & (kRing - 1)] = rel + k;
-    }
-    n_start += ts;
-    n_end += te;
+    for (uint32_t m = trm; m; m &= m - 1) S.ring[(n_tr + rank++) & (kRing - 1)] = rel + __ffs(m) - 1;
+    n_tr += tot;
     __syncwarp();
-    while (n_end - done >= 32 + look) {
-      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end, sq);
+    while ((n_tr >> 1) - done >= 32 + look) {
+      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_tr >> 1, sq);
       done += 32;
       __syncwarp();
     }
   }
   if (carry_ns) {  // the last token runs to the end of the prompt
-    if (lane == 0) S.tok_e[n_end & (kRing - 1)] = (uint32_t)len;
-    ++n_end;
+    if (lane == 0) S.ring[n_tr & (kRing - 1)] = (uint32_t)len;
+    ++n_tr;
     __syncwarp();
   }
-  while (done < n_end) {
-    if (done + lane < n_end) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_end, sq);
+  const uint32_t ntok = n_tr >> 1;
+  while (done < ntok) {
+    if (done + lane < ntok) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, ntok, sq);
     done += 32;
   }
   __syncwarp();
@@ -281,87 +295,149 @@ __device__ __forceinline__ long long warp_sum_i64(long long v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) { return __reduce_add_sync(kFull, v); }
 __device__ __forceinline__ float warp_sum_f32(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
 
-// Walk the touched buckets in ascending order and finish the prompt.
 // Window = 8 bitmap words (256 buckets); lane l owns byte (l&3) of word
-// (l>>2), i.e. buckets [b0, b0+8), so lane order is bucket order. A lane's
-// output position is the popcount of the window's bits before its own,
-// computed from two broadcast 16-byte loads (no shuffle scan).
-template <bool WIDE, int MODE>
-__device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const FeatArgs& a,
-                              int64_t i, int lane, long long sq_lane) {
-  const uint32_t nbw = bitmap_words_padded(c.dim);
+// (l>>2), i.e. buckets [b0, b0+8): lane order is bucket order. A lane's
+// rank in the window is the popcount of the window's bits before its own,
+// from two broadcast 16-byte loads.
+struct Win {
+  uint32_t bits, before, total, b0;
+  bool empty;
+};
+__device__ __forceinline__ Win window(const WarpSmem& S, uint32_t wb, int lane) {
   const int sub = lane & 3, wsel = lane >> 2;
-  const long long sq = c.norm ? warp_sum_i64(sq_lane) : 0;  // features.cpp:113-116, exact
-  const double inv = (c.norm && sq > 0) ? __ddiv_rn(1.0, __dsqrt_rn((double)sq)) : 1.0;
+  const uint4 q0 = *reinterpret_cast<const uint4*>(S.bitmap + wb);
+  const uint4 q1 = *reinterpret_cast<const uint4*>(S.bitmap + wb + 4);
+  const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+  Win w;
+  w.empty = (q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w) == 0;
+  uint32_t before = 0, total = 0, mine = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t pk = __popc(wv[k]);
+    total += pk;
+    before += (k < wsel) ? pk : 0u;
+    mine = (k == wsel) ? wv[k] : mine;
+  }
+  w.before = before + __popc(mine & ((1u << (8 * sub)) - 1u));
+  w.bits = (mine >> (8 * sub)) & 0xffu;
+  w.total = total;
+  w.b0 = (wb + wsel) * 32 + 8 * sub;
+  return w;
+}
 
-  double chain = 0.0;  // lane 0: sequential fp64 dot (exact mode)
-  float facc = 0.f;    // fast mode partial
+// Exact mode: append the prompt's touched buckets, ascending, to `list`
+// (zero-count entries included: they add +0.0, a no-op on a chain that
+// starts at +0.0 under round-to-nearest). Clears the table. Returns count.
+template <bool WIDE>
+__device__ uint32_t walk_to_list(const FeatConfig& c, const WarpSmem& S, uint32_t* list,
+                                 bool packed, int lane) {
+  const uint32_t nbw = bitmap_words_padded(c.dim);
+  uint32_t run = 0;
+  for (uint32_t wb = 0; wb < nbw; wb += 8) {
+    const Win w = window(S, wb, lane);
+    if (w.empty) continue;
+    uint32_t pos = run + w.before;
+    for (uint32_t m = w.bits; m; m &= m - 1) {
+      const uint32_t idx = w.b0 + __ffs(m) - 1;
+      const int cnt = count_of<WIDE>(S, idx);
+      if (packed) {
+        list[pos] = (idx << 16) | (uint32_t)(cnt + 0x8000);
+      } else {
+        list[2 * pos] = idx;
+        list[2 * pos + 1] = (uint32_t)cnt;
+      }
+      ++pos;
+    }
+    if (w.bits) clear_group<WIDE>(S, w.b0);
+    __syncwarp();
+    if ((lane & 3) == 0) S.bitmap[wb + (lane >> 2)] = 0u;
+    run += w.total;
+  }
+  __syncwarp();
+  return run;
+}
+
+__device__ __forceinline__ uint32_t touched_total(const FeatConfig& c, const WarpSmem& S, int lane) {
+  uint32_t t = 0;
+  for (uint32_t k = lane; k < bitmap_words_padded(c.dim); k += 32) t += __popc(S.bitmap[k]);
+  return warp_sum_u32(t);
+}
+
+// Lane k < n: the sequential fp64 dot of group member k (features.hpp:31-35).
+__device__ void chain_group(const FeatConfig& c, const FeatArgs& a, const uint32_t* lists,
+                            bool packed, int lane, int n, int64_t prompt, uint32_t off,
+                            uint32_t cnt_entries, double inv) {
+  if (lane < n) {
+    double s = 0.0;
+    const double* __restrict__ w = a.w64;
+    if (packed) {
+      const uint32_t* L = lists + off;
+      uint32_t k = 0;
+      for (; k + 4 <= cnt_entries; k += 4) {
+        const uint4 e = *reinterpret_cast<const uint4*>(L + k);
+        const uint32_t ev[4] = {e.x, e.y, e.z, e.w};
+        double p[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cn = (int)(ev[j] & 0xffffu) - 0x8000;
+          const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+          p[j] = cn != 0 ? __dmul_rn(__ldg(w + (ev[j] >> 16)), v) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s = __dadd_rn(s, p[j]);
+      }
+      for (; k < cnt_entries; ++k) {
+        const uint32_t e = L[k];
+        const int cn = (int)(e & 0xffffu) - 0x8000;
+        const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+        s = __dadd_rn(s, cn != 0 ? __dmul_rn(__ldg(w + (e >> 16)), v) : 0.0);
+      }
+    } else {
+      const uint32_t* L = lists + 2 * (size_t)off;
+      for (uint32_t k = 0; k < cnt_entries; ++k) {
+        const int cn = (int)L[2 * k + 1];
+        const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+        s = __dadd_rn(s, cn != 0 ? __dmul_rn(__ldg(w + L[2 * k]), v) : 0.0);
+      }
+    }
+    a.scores[prompt] = __dadd_rn(s, a.bias);
+  }
+  __syncwarp();
+}
+
+// Fast fp32 mode and CSR mode finish one prompt in place.
+template <bool WIDE, int MODE>
+__device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const FeatArgs& a, int64_t i,
+                              int lane, double inv) {
+  const uint32_t nbw = bitmap_words_padded(c.dim);
+  float facc = 0.f;
   int64_t row_pos = 0;
   const int64_t slot = (MODE == kFeatCsr) ? a.slot_base[i] : 0;
   for (uint32_t wb = 0; wb < nbw; wb += 8) {
-    const uint4 q0 = *reinterpret_cast<const uint4*>(S.bitmap + wb);
-    const uint4 q1 = *reinterpret_cast<const uint4*>(S.bitmap + wb + 4);
-    const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    if ((q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w) == 0) continue;
-    uint32_t before = 0, total = 0, mine = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t pk = __popc(wv[k]);
-      total += pk;
-      before += (k < wsel) ? pk : 0u;
-      mine = (k == wsel) ? wv[k] : mine;
-    }
-    before += __popc(mine & ((1u << (8 * sub)) - 1u));
-    const uint32_t bits = (mine >> (8 * sub)) & 0xffu;
-    const uint32_t b0 = (wb + wsel) * 32 + 8 * sub;
-    if (MODE == kFeatScoreExact) {
-      // zero-count buckets contribute +0.0, which never changes the chain
-      // (the running sum starts at +0.0 and can never become -0.0 under
-      // round-to-nearest), so no compaction is needed
-      uint32_t pos = before;
-      for (uint32_t m = bits; m; m &= m - 1) {
-        const uint32_t idx = b0 + __ffs(m) - 1;
-        const int cnt = count_of<WIDE>(S, idx);
-        const double v = c.norm ? __dmul_rn((double)cnt, inv) : (double)cnt;
-        S.prod[pos++] = cnt != 0 ? __dmul_rn(__ldg(a.w64 + idx), v) : 0.0;
-      }
-      if (bits) clear_group<WIDE>(S, b0);
-      __syncwarp();
-      if (lane == 0) {
-        uint32_t k = 0;
-        for (; k + 4 <= total; k += 4) {
-          const double2 p01 = *reinterpret_cast<const double2*>(S.prod + k);
-          const double2 p23 = *reinterpret_cast<const double2*>(S.prod + k + 2);
-          chain = __dadd_rn(chain, p01.x);
-          chain = __dadd_rn(chain, p01.y);
-          chain = __dadd_rn(chain, p23.x);
-          chain = __dadd_rn(chain, p23.y);
-        }
-        for (; k < total; ++k) chain = __dadd_rn(chain, S.prod[k]);
-      }
-    } else if (MODE == kFeatScoreFast) {
+    const Win w = window(S, wb, lane);
+    if (w.empty) continue;
+    if (MODE == kFeatScoreFast) {
       const float finv = (float)inv;
-      for (uint32_t m = bits; m; m &= m - 1) {
-        const uint32_t idx = b0 + __ffs(m) - 1;
+      for (uint32_t m = w.bits; m; m &= m - 1) {
+        const uint32_t idx = w.b0 + __ffs(m) - 1;
         facc += __ldg(a.w32 + idx) * ((float)count_of<WIDE>(S, idx) * finv);
       }
-      if (bits) clear_group<WIDE>(S, b0);
     } else {
       // CSR rows must not contain erased zeros (features.cpp:110): compact
       int cnt[8];
       uint32_t nz = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        cnt[j] = ((bits >> j) & 1u) ? count_of<WIDE>(S, b0 + j) : 0;
+        cnt[j] = ((w.bits >> j) & 1u) ? count_of<WIDE>(S, w.b0 + j) : 0;
         nz |= (cnt[j] != 0 ? 1u : 0u) << j;
       }
-      if (bits) clear_group<WIDE>(S, b0);
       int tot;
       const int pos = warp_excl_scan(__popc(nz), lane, &tot);
 #pragma unroll
@@ -369,17 +445,16 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
         if (nz & (1u << j)) {
           const double v = c.norm ? __dmul_rn((double)cnt[j], inv) : (double)cnt[j];
           const int64_t o = slot + row_pos + pos + __popc(nz & ((1u << j) - 1));
-          a.out_idx[o] = b0 + j;
+          a.out_idx[o] = w.b0 + j;
           a.out_val[o] = v;
         }
       row_pos += tot;
     }
+    if (w.bits) clear_group<WIDE>(S, w.b0);
     __syncwarp();
-    if (sub == 0) S.bitmap[wb + wsel] = 0u;
+    if ((lane & 3) == 0) S.bitmap[wb + (lane >> 2)] = 0u;
   }
-  if (MODE == kFeatScoreExact) {
-    if (lane == 0) a.scores[i] = __dadd_rn(chain, a.bias);
-  } else if (MODE == kFeatScoreFast) {
+  if (MODE == kFeatScoreFast) {
     facc = warp_sum_f32(facc);
     if (lane == 0) a.scores[i] = (double)facc + a.bias;
   } else {
@@ -388,79 +463,96 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
   __syncwarp();
 }
 
-__host__ __device__ inline size_t warp_smem_bytes(const FeatConfig& c, int mode, bool wide) {
-  size_t b = (size_t)count_words(c.dim, wide) * 4 + (size_t)bitmap_words_padded(c.dim) * 4 +
-             (size_t)kRing * 8;
-  b = (b + 15) & ~(size_t)15;
-  if (mode == kFeatScoreExact) b += (size_t)kProd * 8;
-  return b;
-}
-
-// G: the per-warp table lives in a global-memory scratch region instead of
-// shared memory (dimensions whose histogram does not fit on chip).
+// G: the per-warp tables live in global scratch (dims too large for smem).
 template <bool POW2, bool WIDE, bool DEF, int MODE, bool G>
 __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t per = warp_smem_bytes(c, MODE, WIDE);
-  unsigned char* my = G ? a.gscratch + per * ((size_t)blockIdx.x * (blockDim.x >> 5) + warp)
-                        : smem + per * warp;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const size_t per = warp_table_bytes(c, WIDE);
+  unsigned char* my = G ? a.gscratch + per * (size_t)gw : smem + per * warp;
   WarpSmem S;
   S.counts = reinterpret_cast<uint32_t*>(my);
   S.bitmap = S.counts + count_words(c.dim, WIDE);
-  S.tok_s = S.bitmap + bitmap_words_padded(c.dim);
-  S.tok_e = S.tok_s + kRing;
-  S.prod = reinterpret_cast<double*>(my + (((size_t)count_words(c.dim, WIDE) * 4 +
-                                            (size_t)bitmap_words_padded(c.dim) * 4 +
-                                            (size_t)kRing * 8 + 15) & ~(size_t)15));
-  const uint32_t cw = count_words(c.dim, WIDE);
-  for (uint32_t k = lane; k < cw; k += 32) S.counts[k] = WIDE ? 0u : kBias2;
-  for (uint32_t k = lane; k < bitmap_words_padded(c.dim); k += 32) S.bitmap[k] = 0u;
-  __syncwarp();
+  S.ring = S.bitmap + bitmap_words_padded(c.dim);
+  clear_all<WIDE>(S, c, lane);
 
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool packed = entry_words(c, WIDE) == 1;
+  uint32_t* lists = (MODE == kFeatScoreExact) ? a.lists + (size_t)gw * a.list_cap : nullptr;
+  // exact-mode group state: lane k holds member k
+  int gn = 0;
+  uint32_t used = 0;
+  int64_t g_prompt = 0;
+  uint32_t g_off = 0, g_cnt = 0;
+  double g_inv = 1.0;
+
   const int64_t count = WIDE ? (int64_t)*a.long_count : a.n;
   for (int64_t it = gw; it < count; it += nw) {
     const int64_t i = WIDE ? (int64_t)a.long_list[it] : it;
     const int64_t beg = a.offsets[i], end = a.offsets[i + 1];
+    const int64_t len = end - beg;
     if (!WIDE) {
-      const int64_t len = end - beg;
       const int64_t feats = (int64_t)c.n_word * ((len + 1) / 2) + (int64_t)c.n_char * len;
-      if (feats > kPackedMaxFeatures) {  // 16-bit counters could overflow
+      if (feats > kNarrowMaxFeatures) {
         if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
         continue;
       }
     }
-    const long long sq = hash_prompt<POW2, WIDE, DEF>(c, S, a.text, beg, end, lane);
-    finish_prompt<WIDE, MODE>(c, S, a, i, lane, sq);
+    const long long sq_lane = hash_prompt<POW2, WIDE, DEF>(c, S, a.text + beg, len, lane);
+    const long long sq = c.norm ? warp_sum_i64(sq_lane) : 0;  // exact sum(count^2)
+    const double inv = (c.norm && sq > 0) ? __ddiv_rn(1.0, __dsqrt_rn((double)sq)) : 1.0;
+    if (MODE == kFeatScoreExact) {
+      const uint32_t n_ent = touched_total(c, S, lane);
+      const uint32_t ew = packed ? 1u : 2u;
+      const uint32_t need = ((n_ent + 3) & ~3u) * ew;
+      if (gn == kGroup || used + need > a.list_cap) {
+        chain_group(c, a, lists, packed, lane, gn, g_prompt, g_off, g_cnt, g_inv);
+        gn = 0;
+        used = 0;
+      }
+      const uint32_t off = used / ew;
+      walk_to_list<WIDE>(c, S, lists + used, packed, lane);
+      if (lane == gn) {
+        g_prompt = i;
+        g_off = off;
+        g_cnt = n_ent;
+        g_inv = inv;
+      }
+      ++gn;
+      used += need;
+    } else {
+      finish_prompt<WIDE, MODE>(c, S, a, i, lane, inv);
+    }
   }
+  if (MODE == kFeatScoreExact && gn > 0)
+    chain_group(c, a, lists, packed, lane, gn, g_prompt, g_off, g_cnt, g_inv);
 }
 
-constexpr size_t kMaxSmemPerBlock = 200 * 1024;
+struct Plan {
+  bool global_tables;
+  int warps;
+  int64_t grid;
+  size_t smem;
+};
 
 template <bool POW2, bool WIDE, bool DEF, int MODE>
-int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st,
-               int64_t items_hint) {
-  const size_t per = warp_smem_bytes(c, MODE, WIDE);
+int plan_one(const FeatConfig& c, int64_t items, Plan* p) {
+  const size_t per = warp_table_bytes(c, WIDE);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (per > kMaxSmemPerBlock) {
-    // global-memory tables: fixed grid, region per warp provided by the caller
-    if (!a.gscratch || a.gscratch_bytes < per * (size_t)kGlobalWarps) {
-      set_error("featurize: global scratch missing for dimension %u", c.dim);
-      return PARS_ERR_INVALID;
-    }
-    auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, true>;
-    kern<<<kGlobalWarps / 4, 128, 0, st>>>(c, a);
-    count_launch(ctx);
-    PARS_CUDA_CHECK(cudaGetLastError());
+    p->global_tables = true;
+    p->warps = 4;
+    p->grid = (int64_t)sms * 4;
+    p->smem = 0;
     return PARS_OK;
   }
+  p->global_tables = false;
   auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, false>;
   // warps per CTA: the choice that keeps the most warps resident per SM
-  // (the per-warp histogram makes shared memory the occupancy limiter)
+  // (the per-warp table makes shared memory the occupancy limiter)
   int warps = 1, per_sm = 1, best = 0;
   for (int w : {8, 4, 2, 1}) {
     if (WIDE && w != 1) continue;
@@ -482,13 +574,35 @@ int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream
     set_error("featurize: no launchable configuration for dimension %u", c.dim);
     return PARS_ERR_UNSUPPORTED;
   }
-  const size_t smem = per * warps;
-  PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int64_t want = ceil_div(std::max<int64_t>(items_hint, 1), warps);
-  int64_t grid = std::min<int64_t>(want, (int64_t)sms * per_sm);
+  p->warps = warps;
+  p->smem = per * warps;
+  int64_t grid = std::min<int64_t>(ceil_div(std::max<int64_t>(items, 1), warps), (int64_t)sms * per_sm);
   if (WIDE) grid = (int64_t)sms * per_sm;  // count known only on device
-  if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, warps * 32, smem, st>>>(c, a);
+  p->grid = std::max<int64_t>(grid, 1);
+  return PARS_OK;
+}
+
+template <bool POW2, bool WIDE, bool DEF, int MODE>
+int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st,
+               int64_t items) {
+  Plan p;
+  PARS_TRY((plan_one<POW2, WIDE, DEF, MODE>(c, items, &p)));
+  const size_t total_warps = (size_t)p.grid * p.warps;
+  if (p.global_tables && a.gscratch_bytes < warp_table_bytes(c, WIDE) * total_warps) {
+    set_error("featurize: global table scratch too small");
+    return PARS_ERR_INVALID;
+  }
+  if (MODE == kFeatScoreExact && a.lists_bytes < (size_t)a.list_cap * 4 * total_warps) {
+    set_error("featurize: list scratch too small");
+    return PARS_ERR_INVALID;
+  }
+  if (p.global_tables) {
+    featurize_kernel<POW2, WIDE, DEF, MODE, true><<<(unsigned)p.grid, p.warps * 32, 0, st>>>(c, a);
+  } else {
+    auto kern = featurize_kernel<POW2, WIDE, DEF, MODE, false>;
+    PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a);
+  }
   count_launch(ctx);
   PARS_CUDA_CHECK(cudaGetLastError());
   return PARS_OK;
@@ -501,6 +615,21 @@ int launch_pair(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStrea
   return launch_one<POW2, true, DEF, MODE>(ctx, c, a, st, 0);
 }
 
+template <bool POW2, bool DEF, int MODE>
+int scratch_pair(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
+  *gs = 0;
+  *ls = 0;
+  for (int wide = 0; wide < 2; ++wide) {
+    Plan p;
+    int rc = wide ? plan_one<POW2, true, DEF, MODE>(c, 0, &p) : plan_one<POW2, false, DEF, MODE>(c, n, &p);
+    if (rc != PARS_OK) return rc;
+    const size_t tw = (size_t)p.grid * p.warps;
+    if (p.global_tables) *gs = std::max(*gs, warp_table_bytes(c, wide != 0) * tw);
+    if (MODE == kFeatScoreExact) *ls = std::max(*ls, (size_t)list_cap_words(c) * 4 * tw);
+  }
+  return PARS_OK;
+}
+
 template <int MODE>
 int launch_mode(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st) {
   if (c.pow2) {
@@ -508,6 +637,15 @@ int launch_mode(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStrea
     return launch_pair<true, false, MODE>(ctx, c, a, st);
   }
   return launch_pair<false, false, MODE>(ctx, c, a, st);
+}
+
+template <int MODE>
+int scratch_mode(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
+  if (c.pow2) {
+    if (c.default_orders) return scratch_pair<true, true, MODE>(c, n, gs, ls);
+    return scratch_pair<true, false, MODE>(c, n, gs, ls);
+  }
+  return scratch_pair<false, false, MODE>(c, n, gs, ls);
 }
 
 // ---- dense embeddings (features.cpp:67-76) -----------------------------
@@ -606,17 +744,19 @@ bool build_feat_config(const pars_extractor* ex, FeatConfig* c) {
   return true;
 }
 
-size_t feat_warp_smem(const FeatConfig& cfg, int mode, bool wide) {
-  return warp_smem_bytes(cfg, mode, wide);
-}
+uint32_t feat_list_cap_words(const FeatConfig& c) { return list_cap_words(c); }
 
-size_t feat_global_scratch_bytes(const FeatConfig& cfg, int mode) {
-  size_t need = 0;
-  for (int wide = 0; wide < 2; ++wide) {
-    const size_t per = warp_smem_bytes(cfg, mode, wide != 0);
-    if (per > kMaxSmemPerBlock) need = std::max(need, per * (size_t)kGlobalWarps);
+int feat_scratch_bytes(const FeatConfig& c, int mode, int64_t n, size_t* gscratch, size_t* lists) {
+  switch (mode) {
+    case kFeatScoreExact:
+      return scratch_mode<kFeatScoreExact>(c, n, gscratch, lists);
+    case kFeatScoreFast:
+      return scratch_mode<kFeatScoreFast>(c, n, gscratch, lists);
+    case kFeatCsr:
+      return scratch_mode<kFeatCsr>(c, n, gscratch, lists);
   }
-  return need;
+  set_error("unknown featurize mode %d", mode);
+  return PARS_ERR_INVALID;
 }
 
 int launch_featurize(pars_ctx* ctx, const FeatConfig& c, int mode, const FeatArgs& a,

@@ -46,14 +46,19 @@ struct FeatArgs {
   // per-warp tables in global memory for dimensions too large for smem
   unsigned char* gscratch;
   size_t gscratch_bytes;
+  // exact mode: per-warp (idx, count) list arenas, list_cap u32 words each
+  uint32_t* lists;
+  size_t lists_bytes;
+  uint32_t list_cap;
 };
 
 bool build_feat_config(const pars_extractor* ex, FeatConfig* cfg);
 
-// Per-warp shared-memory bytes for a configuration (0 if unsupported).
-size_t feat_warp_smem(const FeatConfig& cfg, int mode, bool wide);
-// Global scratch needed when a table does not fit in shared memory (else 0).
-size_t feat_global_scratch_bytes(const FeatConfig& cfg, int mode);
+// Scratch a launch over n prompts needs: global per-warp tables (dims too
+// large for shared memory) and exact-mode list arenas (bytes each).
+int feat_scratch_bytes(const FeatConfig& cfg, int mode, int64_t n, size_t* gscratch,
+                       size_t* lists);
+uint32_t feat_list_cap_words(const FeatConfig& cfg);
 
 // Launches the packed kernel over all prompts followed by the wide kernel
 // over prompts whose feature count may exceed the 16-bit counters.
