@@ -3,8 +3,8 @@
  * (libpars_cuda.so, sm_100a).
  *
  * This is the drop-in boundary underneath the reference's C++ predictor and
- * scheduler API (/root/reference/proj/include/pars/*.hpp). The C++ host shim
- * (paper_2510_03243_b200/host/*.cpp, compiled against those unmodified
+ * scheduler API (/root/reference/proj/include/pars/ headers). The C++ host shim
+ * (paper_2510_03243_b200/host/ sources, compiled against those unmodified
  * headers) and the Python bindings (paper_2510_03243_b200/_lib.py) both call
  * only the functions below. Plain pointers and sizes, no C++ or torch types.
  *
@@ -132,8 +132,8 @@ int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths,
 /* Device form over a slice [tile_begin, tile_end) of the upper-triangle tile
  * list (tile count from pars_allpairs_tiles); coeff/counters are ACCUMULATED
  * (int32 c[n]; uint64 counters[2] = kept, active; double loss partials[]
- * one per tile in the slice, reduced deterministically by the caller or by
- * pars_dev_allpairs_finish). d_lengths are int32. */
+ * one per tile in the slice, summed in a fixed order by the caller).
+ * d_lengths are int32; every length must be <= max_len. */
 int64_t pars_allpairs_tiles(int64_t n);
 int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores,
                       const int32_t* d_lengths, int64_t n, double delta,

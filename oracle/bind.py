@@ -449,7 +449,7 @@ class Ref:
 
     def simulate(self, ds, arrivals=None, policy="fcfs", ex=None, w=None, bias=0.0,
                  batch_limit=32, starvation_s=120.0):
-        pol = {"fcfs": 0, "pars": 1, "oracle": 2}[policy]
+        pol = {"fcfs": 0, "pars": 1, "oracle": 2, "scores": 3}[policy]
         arr = None if arrivals is None else np.ascontiguousarray(arrivals, np.float64)
         wc = None if w is None else np.ascontiguousarray(w, np.float64)
         h = self.L.ref_simulate(ds.h, _ptr(arr), pol, C.byref(ex) if ex is not None else None,

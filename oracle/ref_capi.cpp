@@ -71,6 +71,18 @@ int guard(F&& f) {
 struct SimHandle {
   SimResult res;
 };
+
+// Scores supplied by the caller (e.g. computed on the GPU), looked up by
+// record index: the "GPU-scored priorities" policy of config C3.
+class ArrayScorer : public Scorer {
+ public:
+  ArrayScorer(const Dataset& ds, const double* s) : ds_(ds), s_(s, s + ds.size()) {}
+  double score(const PromptRecord& r) const override { return s_[ds_.index_of(r.id)]; }
+
+ private:
+  const Dataset& ds_;
+  std::vector<double> s_;
+};
 }  // namespace
 
 extern "C" {
@@ -337,7 +349,8 @@ int ref_kendall(const double* x, const double* y, int64_t n, int serial,
 }
 
 // ---- simulation -----------------------------------------------------------
-// policy: 0 fcfs, 1 pars (linear scorer with w/bias), 2 oracle.
+// policy: 0 fcfs, 1 pars (linear scorer with w/bias), 2 oracle,
+//         3 precomputed scores (w = per-record scores).
 // arrivals: per-record times in dataset order (NULL -> burst at 0).
 void* ref_simulate(void* h, const double* arrivals, int policy,
                    const RefExtractor* e, const double* w, double bias,
@@ -359,8 +372,10 @@ void* ref_simulate(void* h, const double* arrivals, int policy,
       FeatureExtractor ex = to_ex(e);
       auto sc = std::make_shared<LinearScorer>(ex, std::vector<double>(w, w + ex.dim), bias);
       cfg.policy.policy = make_sjf_policy("pars", sc);
-    } else {
+    } else if (policy == 2) {
       cfg.policy.policy = make_sjf_policy("oracle", std::make_shared<OracleScorer>(*ds));
+    } else {
+      cfg.policy.policy = make_sjf_policy("pars-gpu", std::make_shared<ArrayScorer>(*ds, w));
     }
     auto* sh = new SimHandle();
     sh->res = run_simulation(tr, *ds, cfg);
