@@ -375,26 +375,14 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
     max_len = int(lens.max())
     d_s = torch.from_numpy(s).to(dev)
     d_L = torch.from_numpy(lens).to(dev)
-    d_c = torch.zeros(C5_N, dtype=torch.int32, device=dev)
-    d_cnt = torch.zeros(4, dtype=torch.int64, device=dev)
-    tiles = P.lib().pars_allpairs_tiles(C5_N)
-    t0, t1 = shard(tiles, world, rank)
-    d_part = torch.zeros(max(1, t1 - t0), dtype=torch.float64, device=dev)
-    L = P.lib()
+    from paper_2510_03243_b200 import distributed as D
     sh = stream.cuda_stream
+    res = {}
 
     def step():
-        d_c.zero_()
-        d_cnt.zero_()
-        rc = L.pars_dev_allpairs(ctx.h, d_s.data_ptr(), d_L.data_ptr(), C5_N, DELTA, MARGIN,
-                                 max_len, t0, t1, d_c.data_ptr(), d_cnt.data_ptr(),
-                                 d_part.data_ptr(), sh)
-        if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode())
-        if world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(d_c)  # integer coefficients: exact for any rank count
-            dist.all_reduce(d_cnt)
+        # this rank's tile slice on the GPU + NCCL all-reduce of the integer
+        # coefficients/counters + tile-ordered loss reduction
+        res["out"] = D.allpairs_step_gpu(ctx, d_s, d_L, C5_N, DELTA, MARGIN, max_len, stream=sh)
 
     for _ in range(3):
         step()
@@ -408,11 +396,11 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
     bb.record(stream)
     torch.cuda.synchronize()
     ms = barrier_max(world, a.elapsed_time(bb)) / k
-    kept = int(d_cnt[0].item())
-    active = int(d_cnt[1].item())
+    _, kept, active, loss = res["out"]
     # exactness check against the golden exhaustive count
     return {"metric": "filtered pairs/s", "value": kept / (ms / 1e3), "unit": "pairs/s",
             "ms_per_step": ms, "kept": kept, "kept_expected": 1920977782, "active": active,
+            "loss_sum": loss,
             "workload": "C5: all 2,147,450,880 unordered pairs of 65,536 prompts (seed 25), "
                         "Eq.1 mask delta=0.2 + hinge + integer grad coefficients (fp64 scores)",
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident"}

@@ -1,0 +1,132 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed / NCCL).
+
+Only the paths that shard naturally are partitioned:
+
+* scoring: contiguous prompt ranges per rank, no data-path collective
+  (`shard_range`, `score_shard`); an optional all-gather assembles the
+  global score vector for a global SJF order;
+* all-pairs loss (config C5): the upper-triangle tile list is split evenly
+  across ranks (`tile_range`); each rank accumulates integer gradient
+  coefficients, kept/active counts and per-tile loss partials; the exchange
+  is an all-reduce of the int32 coefficients and int64 counters (exact for
+  any rank count) and an all-gather of the per-tile partials, summed in tile
+  order so the loss is bit-identical for 1, 2, 4 or 8 ranks;
+* full-batch step: grad = X^T c over each rank's row shard, all-reduced
+  (D doubles), then the update.
+
+The per-rank compute is the CUDA kernel (`pars_dev_allpairs`); the CPU tests
+substitute a reference implementation of the same per-tile contract to check
+the partition and the collectives with the gloo backend.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional, Tuple
+
+import numpy as np
+
+TILE = 256  # pairs.cu kTile
+
+
+def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
+    per = (n + world - 1) // world
+    return min(n, rank * per), min(n, (rank + 1) * per)
+
+
+def tile_count(n: int) -> int:
+    nt = (n + TILE - 1) // TILE
+    return nt * (nt + 1) // 2
+
+
+def tile_range(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """Equal share of the upper-triangle tile list (tiles are equal-cost
+    except the diagonal ones, which are half-empty)."""
+    return shard_range(tile_count(n), world, rank)
+
+
+def tile_coords(t: int, n: int) -> Tuple[int, int]:
+    """Row-major upper-triangle enumeration (pairs.cu tile_of)."""
+    nt = (n + TILE - 1) // TILE
+    i = 0
+    while i + 1 < nt and (i + 1) * nt - (i + 1) * i // 2 <= t:
+        i += 1
+    start = i * nt - i * (i - 1) // 2
+    return i, i + (t - start)
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream):
+    """Per-rank compute on the GPU for tiles [t0, t1)."""
+    import torch
+    from ._lib import ParsError, lib
+
+    def run(t0: int, t1: int):
+        dev = d_scores.device
+        c = torch.zeros(n, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+        part = torch.zeros(max(1, t1 - t0), dtype=torch.float64, device=dev)
+        rc = lib().pars_dev_allpairs(ctx.h, d_scores.data_ptr(), d_lengths.data_ptr(), n, delta,
+                                     margin, max_len, t0, t1, c.data_ptr(), cnt.data_ptr(),
+                                     part.data_ptr(), stream)
+        if rc != 0:
+            raise ParsError(rc, lib().pars_last_error().decode())
+        return c, cnt[:2], part[: max(0, t1 - t0)]
+
+    return run
+
+
+def allpairs_dp(n: int, compute: Callable, group=None):
+    """All-pairs margin-ranking loss over n prompts split across the ranks of
+    `group` (or a single process when torch.distributed is not initialised).
+
+    compute(t0, t1) -> (coeff int32[n], counts int64[2] = kept, active,
+    loss partials float64[t1-t0]) for this rank's tile slice.
+    Returns (coeff, kept, active, loss_sum) identical on every rank."""
+    import torch
+    dist = _dist()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    t0, t1 = tile_range(n, world, rank)
+    c, cnt, part = compute(t0, t1)
+    if world > 1:
+        dist.all_reduce(c, group=group)
+        dist.all_reduce(cnt, group=group)
+        # per-tile partials, gathered into tile order, then one fixed-order sum
+        sizes = [tile_range(n, world, r) for r in range(world)]
+        width = max(b - a for a, b in sizes)
+        buf = torch.zeros(width, dtype=torch.float64, device=part.device)
+        buf[: part.numel()] = part
+        bufs = [torch.zeros_like(buf) for _ in range(world)]
+        dist.all_gather(bufs, buf, group=group)
+        part = torch.cat([bufs[r][: sizes[r][1] - sizes[r][0]] for r in range(world)])
+    loss = float(part.sum().item()) if part.numel() else 0.0
+    return c, int(cnt[0].item()), int(cnt[1].item()), loss
+
+
+def allpairs_step_gpu(ctx, d_scores, d_lengths, n: int, delta: float, margin: float, max_len: int,
+                      stream: int = 0, group=None):
+    """The C5 exchange step on GPUs (NCCL when the group is initialised)."""
+    return allpairs_dp(n, _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len,
+                                     stream or None), group)
+
+
+def grad_step_gpu(ctx, feats, d_coeff, scale: float, group=None, stream: int = 0):
+    """grad = scale * X^T c over this rank's row shard, all-reduced."""
+    import torch
+    from ._lib import ParsError, lib
+    dist = _dist()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    r0, r1 = shard_range(feats.rows, world, rank)
+    g = torch.zeros(feats.dim, dtype=torch.float64, device=d_coeff.device)
+    rc = lib().pars_dev_xt_c(ctx.h, C.c_void_p(feats.h), d_coeff.data_ptr(), r0, r1, g.data_ptr(),
+                             stream or None)
+    if rc != 0:
+        raise ParsError(rc, lib().pars_last_error().decode())
+    if world > 1:
+        dist.all_reduce(g, group=group)
+    return g * scale

@@ -269,3 +269,30 @@ def test_errors_are_loud(ctx):
         ctx.score_text(Extractor.make(word=(0,)), arena, offs, np.zeros(4096))
     with pytest.raises(ParsError, match=r"train: delta 1 outside \[0, 1\)"):
         ctx.train_pairwise(Extractor.make(), arena, offs, np.array([3]), delta=1.0)
+
+
+def test_distributed_allpairs_step_single_rank(ctx, oracle):
+    """distributed.allpairs_step_gpu (the C5 exchange step) on one rank equals
+    the all-pairs oracle; grad_step_gpu equals X^T c."""
+    import torch
+    from paper_2510_03243_b200 import Extractor, Workload
+    from paper_2510_03243_b200 import distributed as D
+    wl = Workload.synthesize(3000, 41)
+    e = Extractor.make()
+    w = np.random.default_rng(6).normal(size=4096) * 0.1
+    s = ctx.score_text(e, wl.text, wl.offsets, w)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        d_s = torch.from_numpy(s).to(dev)
+        d_L = torch.from_numpy(wl.output_len.astype(np.int32)).to(dev)
+        c, kept, act, loss = D.allpairs_step_gpu(ctx, d_s, d_L, len(s), 0.2, 1.0,
+                                                 int(wl.output_len.max()), stream=stream.cuda_stream)
+        oc, okept, oact, oloss = oracle.allpairs(s, wl.output_len, 0.2, 1.0)
+        assert (c.cpu().numpy() == oc).all() and kept == okept and act == oact
+        assert abs(loss - oloss) <= 1e-12 * max(1.0, oloss)
+        f = ctx.extract(e, wl.text, wl.offsets)
+        g = D.grad_step_gpu(ctx, f, c, 1.0, stream=stream.cuda_stream).cpu().numpy()
+    rp, idx, val = f.download()
+    og = oracle.xt_c(rp, idx, val, oc, 4096)
+    assert np.allclose(g, og, rtol=1e-12, atol=1e-12)
