@@ -82,21 +82,19 @@ __host__ inline uint32_t list_cap_words(const FeatConfig& c) {
   return (cap + 3u) & ~3u;
 }
 
-// One hashed feature. `sq` accumulates the exact change of sum(count^2):
-// (c+d)^2 - c^2 = 2cd + 1 with c the atomic's old value.
+// One hashed feature: +-1 into its bucket; the first touch of a bucket (old
+// count 0) sets its bit in the touched bitmap.
 template <bool WIDE>
-__device__ __forceinline__ void emit(const WarpSmem& S, uint32_t idx, bool pos, long long& sq) {
-  int oldc;
+__device__ __forceinline__ void emit(const WarpSmem& S, uint32_t idx, bool pos) {
+  bool first;
   if (WIDE) {
-    oldc = (int)atomicAdd(&S.counts[idx], pos ? 1u : 0xffffffffu);
+    first = atomicAdd(&S.counts[idx], pos ? 1u : 0xffffffffu) == 0u;
   } else {
     const uint32_t sh = (idx & 1u) << 4;
     const uint32_t d = pos ? (1u << sh) : (0u - (1u << sh));
-    const uint32_t old = atomicAdd(&S.counts[idx >> 1], d);
-    oldc = (int)((old >> sh) & 0xffffu) - 0x8000;
+    first = ((atomicAdd(&S.counts[idx >> 1], d) >> sh) & 0xffffu) == 0x8000u;
   }
-  sq += 2ll * (pos ? oldc : -oldc) + 1;
-  if (oldc == 0) atomicOr(&S.bitmap[idx >> 5], 1u << (idx & 31));
+  if (first) atomicOr(&S.bitmap[idx >> 5], 1u << (idx & 31));
 }
 
 template <bool WIDE>
@@ -148,11 +146,11 @@ struct H<false> {
 
 __device__ __forceinline__ uint32_t ld_byte(const uint8_t* p) { return __ldg(p); }
 
-// Hash token `t` and every n-gram that starts at it.
+// Hash token `t` (from the transition ring) and every n-gram that starts at
+// it: the general path for arbitrary word/char n-gram orders.
 template <bool POW2, bool WIDE, bool DEF>
 __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& S,
-                                           const uint8_t* base, uint32_t t, uint32_t ntok,
-                                           long long& sq) {
+                                           const uint8_t* base, uint32_t t, uint32_t ntok) {
   using HT = H<POW2>;
   using T = typename HT::T;
   const uint32_t s = S.ring[(2 * t) & (kRing - 1)], e = S.ring[(2 * t + 1) & (kRing - 1)];
@@ -170,9 +168,9 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
       hw = HT::step(HT::step(hw, x), y);
       if (i >= 2) {
         const T h = HT::step(HT::step(HT::step(hc0, b2), b1), x);
-        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
         const T g = HT::step(HT::step(HT::step(hc0, b1), x), y);
-        emit<WIDE>(S, HT::bucket(g, c), (g & 1) != 0, sq);
+        emit<WIDE>(S, HT::bucket(g, c), (g & 1) != 0);
       }
       b2 = x;
       b1 = y;
@@ -182,11 +180,11 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
       hw = HT::step(hw, x);
       if (i >= 2) {
         const T h = HT::step(HT::step(HT::step(hc0, b2), b1), x);
-        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+        emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
       }
     }
     hw = HT::step(hw, 0x1fu);
-    emit<WIDE>(S, HT::bucket(hw, c), (hw & 1) != 0, sq);
+    emit<WIDE>(S, HT::bucket(hw, c), (hw & 1) != 0);
     return;
   }
   for (int k = 0; k < c.n_word; ++k) {
@@ -199,7 +197,7 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
       for (uint32_t q = sj; q < ej; ++q) h = HT::step(h, ld_byte(base + q));
       h = HT::step(h, 0x1fu);
     }
-    emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+    emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
   }
   for (int k = 0; k < c.n_char; ++k) {
     const int order = c.chr[k];
@@ -207,9 +205,20 @@ __device__ __forceinline__ void hash_token(const FeatConfig& c, const WarpSmem& 
     for (int i = 0; i + order <= len; ++i) {
       T h = seed;
       for (int j = 0; j < order; ++j) h = HT::step(h, ld_byte(tp + i + j));
-      emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0, sq);
+      emit<WIDE>(S, HT::bucket(h, c), (h & 1) != 0);
     }
   }
+}
+
+// SWAR: bit k of the result = byte k of w is not C-locale whitespace.
+__device__ __forceinline__ uint32_t nonspace_nibble(uint32_t w) {
+  const uint32_t x = w ^ 0x20202020u;  // zero byte where ' '
+  const uint32_t not_blank = ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x;  // high bit: byte != ' '
+  // high bit: byte in [9, 13] (\t \n \v \f \r); bytes >= 0x80 are never spaces
+  const uint32_t lo7 = w & 0x7f7f7f7fu;
+  const uint32_t ctl = (0x8d8d8d8du - lo7) & ~w & (lo7 + 0x77777777u);
+  const uint32_t ns_hi = not_blank & ~ctl & 0x80808080u;
+  return ((ns_hi >> 7) * 0x01020408u) >> 24;
 }
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
@@ -234,14 +243,15 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t* base, int64_t p, in
   return word;
 }
 
-// Tokenise + hash one prompt into the warp's histogram; returns this lane's
-// share of sum(count^2).
+// Tokeniser + hasher: whitespace transitions (SWAR non-space nibble per
+// lane) are ranked with 4 ballots into the per-warp transition ring; lane t
+// hashes token t of each complete 32-token batch, so every lane has exactly
+// one token per batch whatever the token-length mix.
 template <bool POW2, bool WIDE, bool DEF>
-__device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const uint8_t* base,
+__device__ void hash_prompt_ring(const FeatConfig& c, const WarpSmem& S, const uint8_t* base,
                                  int64_t len, int lane) {
   uint32_t n_tr = 0, done = 0;
   uint32_t carry_ns = 0;
-  long long sq = 0;
   const uint32_t look = c.max_word > 1 ? (uint32_t)c.max_word - 1 : 0;
   const unsigned lt = (1u << lane) - 1u;
   // windows are aligned on the ABSOLUTE address so each lane's 4-byte load
@@ -252,9 +262,7 @@ __device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const u
     const int64_t p = wrel + 4 * lane;  // relative to base; may be negative
     const uint32_t word = next;
     if (wrel + 128 < len) next = load_word(base, p + 128, len);
-    uint32_t ns = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ns |= (is_space((word >> (8 * k)) & 0xffu) ? 0u : 1u) << k;
+    const uint32_t ns = nonspace_nibble(word);
     uint32_t prev = __shfl_up_sync(kFull, ns >> 3, 1);
     if (lane == 0) prev = carry_ns;
     const uint32_t trm = (ns ^ ((ns << 1) | prev)) & 0xfu;  // transitions at byte k
@@ -271,7 +279,7 @@ __device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const u
     n_tr += tot;
     __syncwarp();
     while ((n_tr >> 1) - done >= 32 + look) {
-      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_tr >> 1, sq);
+      hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, n_tr >> 1);
       done += 32;
       __syncwarp();
     }
@@ -283,11 +291,10 @@ __device__ long long hash_prompt(const FeatConfig& c, const WarpSmem& S, const u
   }
   const uint32_t ntok = n_tr >> 1;
   while (done < ntok) {
-    if (done + lane < ntok) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, ntok, sq);
+    if (done + lane < ntok) hash_token<POW2, WIDE, DEF>(c, S, base, done + lane, ntok);
     done += 32;
   }
   __syncwarp();
-  return sq;
 }
 
 __device__ __forceinline__ long long warp_sum_i64(long long v) {
@@ -334,10 +341,12 @@ __device__ __forceinline__ Win window(const WarpSmem& S, uint32_t wb, int lane) 
 
 // Exact mode: append the prompt's touched buckets, ascending, to `list`
 // (zero-count entries included: they add +0.0, a no-op on a chain that
-// starts at +0.0 under round-to-nearest). Clears the table. Returns count.
+// starts at +0.0 under round-to-nearest) and return the exact integer
+// sum(count^2) (features.cpp:113-116). Clears the table.
 template <bool WIDE>
-__device__ uint32_t walk_to_list(const FeatConfig& c, const WarpSmem& S, uint32_t* list,
-                                 bool packed, int lane) {
+__device__ long long walk_to_list(const FeatConfig& c, const WarpSmem& S, uint32_t* list,
+                                  bool packed, int lane) {
+  long long sq = 0;
   const uint32_t nbw = bitmap_words_padded(c.dim);
   uint32_t run = 0;
   for (uint32_t wb = 0; wb < nbw; wb += 8) {
@@ -347,6 +356,7 @@ __device__ uint32_t walk_to_list(const FeatConfig& c, const WarpSmem& S, uint32_
     for (uint32_t m = w.bits; m; m &= m - 1) {
       const uint32_t idx = w.b0 + __ffs(m) - 1;
       const int cnt = count_of<WIDE>(S, idx);
+      sq += (long long)cnt * cnt;
       if (packed) {
         list[pos] = (idx << 16) | (uint32_t)(cnt + 0x8000);
       } else {
@@ -361,7 +371,11 @@ __device__ uint32_t walk_to_list(const FeatConfig& c, const WarpSmem& S, uint32_
     run += w.total;
   }
   __syncwarp();
-  return run;
+  return warp_sum_i64(sq);
+}
+
+__device__ __forceinline__ double inv_norm(const FeatConfig& c, long long sq) {
+  return (c.norm && sq > 0) ? __ddiv_rn(1.0, __dsqrt_rn((double)sq)) : 1.0;
 }
 
 __device__ __forceinline__ uint32_t touched_total(const FeatConfig& c, const WarpSmem& S, int lane) {
@@ -415,8 +429,20 @@ __device__ void chain_group(const FeatConfig& c, const FeatArgs& a, const uint32
 // Fast fp32 mode and CSR mode finish one prompt in place.
 template <bool WIDE, int MODE>
 __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const FeatArgs& a, int64_t i,
-                              int lane, double inv) {
+                              int lane) {
   const uint32_t nbw = bitmap_words_padded(c.dim);
+  long long sq = 0;
+  if (MODE == kFeatCsr && c.norm) {  // values need inv before they are written
+    for (uint32_t wb = 0; wb < nbw; wb += 8) {
+      const Win w = window(S, wb, lane);
+      for (uint32_t m = w.bits; m; m &= m - 1) {
+        const int cnt = count_of<WIDE>(S, w.b0 + __ffs(m) - 1);
+        sq += (long long)cnt * cnt;
+      }
+    }
+    sq = warp_sum_i64(sq);
+  }
+  const double inv = inv_norm(c, sq);
   float facc = 0.f;
   int64_t row_pos = 0;
   const int64_t slot = (MODE == kFeatCsr) ? a.slot_base[i] : 0;
@@ -424,10 +450,11 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
     const Win w = window(S, wb, lane);
     if (w.empty) continue;
     if (MODE == kFeatScoreFast) {
-      const float finv = (float)inv;
       for (uint32_t m = w.bits; m; m &= m - 1) {
         const uint32_t idx = w.b0 + __ffs(m) - 1;
-        facc += __ldg(a.w32 + idx) * ((float)count_of<WIDE>(S, idx) * finv);
+        const int cnt = count_of<WIDE>(S, idx);
+        sq += (long long)cnt * cnt;
+        facc += __ldg(a.w32 + idx) * (float)cnt;
       }
     } else {
       // CSR rows must not contain erased zeros (features.cpp:110): compact
@@ -456,7 +483,8 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
   }
   if (MODE == kFeatScoreFast) {
     facc = warp_sum_f32(facc);
-    if (lane == 0) a.scores[i] = (double)facc + a.bias;
+    const float finv = (float)inv_norm(c, warp_sum_i64(sq));
+    if (lane == 0) a.scores[i] = (double)(facc * finv) + a.bias;
   } else {
     if (lane == 0) a.out_nnz[i] = (int32_t)row_pos;
   }
@@ -499,9 +527,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
         continue;
       }
     }
-    const long long sq_lane = hash_prompt<POW2, WIDE, DEF>(c, S, a.text + beg, len, lane);
-    const long long sq = c.norm ? warp_sum_i64(sq_lane) : 0;  // exact sum(count^2)
-    const double inv = (c.norm && sq > 0) ? __ddiv_rn(1.0, __dsqrt_rn((double)sq)) : 1.0;
+    hash_prompt_ring<POW2, WIDE, DEF>(c, S, a.text + beg, len, lane);
     if (MODE == kFeatScoreExact) {
       const uint32_t n_ent = touched_total(c, S, lane);
       const uint32_t ew = packed ? 1u : 2u;
@@ -512,7 +538,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
         used = 0;
       }
       const uint32_t off = used / ew;
-      walk_to_list<WIDE>(c, S, lists + used, packed, lane);
+      const double inv = inv_norm(c, walk_to_list<WIDE>(c, S, lists + used, packed, lane));
       if (lane == gn) {
         g_prompt = i;
         g_off = off;
@@ -522,7 +548,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
       ++gn;
       used += need;
     } else {
-      finish_prompt<WIDE, MODE>(c, S, a, i, lane, inv);
+      finish_prompt<WIDE, MODE>(c, S, a, i, lane);
     }
   }
   if (MODE == kFeatScoreExact && gn > 0)
