@@ -378,11 +378,15 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
     from paper_2510_03243_b200 import distributed as D
     sh = stream.cuda_stream
     res = {}
+    # per-dataset plan (lengths are fixed across steps): stable length order,
+    # first kept column per row, exact kept count
+    plan = ctx.pair_plan(wl.output_len, DELTA)
 
     def step():
         # this rank's tile slice on the GPU + NCCL all-reduce of the integer
         # coefficients/counters + tile-ordered loss reduction
-        res["out"] = D.allpairs_step_gpu(ctx, d_s, d_L, C5_N, DELTA, MARGIN, max_len, stream=sh)
+        res["out"] = D.allpairs_step_gpu(ctx, d_s, d_L, C5_N, DELTA, MARGIN, max_len, stream=sh,
+                                         plan=plan)
 
     for _ in range(3):
         step()
@@ -401,6 +405,7 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
     return {"metric": "filtered pairs/s", "value": kept / (ms / 1e3), "unit": "pairs/s",
             "ms_per_step": ms, "kept": kept, "kept_expected": 1920977782, "active": active,
             "loss_sum": loss,
+            "plan_sorted": plan.sorted,
             "workload": "C5: all 2,147,450,880 unordered pairs of 65,536 prompts (seed 25), "
                         "Eq.1 mask delta=0.2 + hinge + integer grad coefficients (fp64 scores)",
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident"}

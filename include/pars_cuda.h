@@ -129,6 +129,16 @@ int pars_length_gap_table(double delta, int64_t max_len, int32_t* dmin);
 int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths,
                   int64_t n, double delta, double margin, int32_t* coeff,
                   uint64_t* kept, uint64_t* active, double* loss_sum);
+/* Same, choosing the kernel: PARS_ALLPAIRS_SORTED (length-sorted plan, the
+ * default) or PARS_ALLPAIRS_GENERAL (unsorted tiles, per-pair table mask).
+ * Identical masks, coefficients and counts; the loss sums differ only in
+ * rounding order. */
+#define PARS_ALLPAIRS_SORTED 0
+#define PARS_ALLPAIRS_GENERAL 1
+int pars_allpairs_algo(pars_ctx* ctx, const double* scores,
+                       const int64_t* lengths, int64_t n, double delta,
+                       double margin, int algo, int32_t* coeff, uint64_t* kept,
+                       uint64_t* active, double* loss_sum);
 /* Device form over a slice [tile_begin, tile_end) of the upper-triangle tile
  * list (tile count from pars_allpairs_tiles); coeff/counters are ACCUMULATED
  * (int32 c[n]; uint64 counters[2] = kept, active; double loss partials[]
@@ -141,6 +151,21 @@ int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores,
                       int64_t tile_end, int32_t* d_coeff,
                       unsigned long long* d_counters, double* d_loss_partials,
                       void* stream);
+/* Per-dataset plan for the length-sorted kernel (lengths are fixed across
+ * training steps): stable length order, per-row first kept column, exact
+ * kept-pair count. Sharded callers pass [tile_begin, tile_end) slices as
+ * for pars_dev_allpairs; outputs are in input order and accumulated. */
+typedef struct pars_pair_plan pars_pair_plan;
+int pars_pair_plan_create(pars_ctx* ctx, const int64_t* lengths, int64_t n,
+                          double delta, pars_pair_plan** out);
+uint64_t pars_pair_plan_kept(const pars_pair_plan* plan);
+int pars_pair_plan_sorted(const pars_pair_plan* plan);
+void pars_pair_plan_free(pars_pair_plan* plan);
+int pars_dev_allpairs_plan(pars_ctx* ctx, const pars_pair_plan* plan,
+                           const double* d_scores, double margin,
+                           int64_t tile_begin, int64_t tile_end,
+                           int32_t* d_coeff, unsigned long long* d_counters,
+                           double* d_loss_partials, void* stream);
 /* grad[d] = sum_i c_i x_i[d] (fp64) for rows [row_begin,row_end) of f. */
 int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
                   int64_t row_begin, int64_t row_end, double* d_grad,

@@ -91,6 +91,12 @@ def _load() -> C.CDLL:
         "pars_length_gap_table": (C.c_int, [dbl, i64, vp]),
         "pars_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, vp, vp, vp, vp]),
         "pars_allpairs_tiles": (i64, [i64]),
+        "pars_allpairs_algo": (C.c_int, [vp, vp, vp, i64, dbl, dbl, C.c_int, vp, vp, vp, vp]),
+        "pars_pair_plan_create": (C.c_int, [vp, vp, i64, dbl, vp]),
+        "pars_pair_plan_kept": (u64, [vp]),
+        "pars_pair_plan_sorted": (C.c_int, [vp]),
+        "pars_pair_plan_free": (None, [vp]),
+        "pars_dev_allpairs_plan": (C.c_int, [vp, vp, vp, dbl, i64, i64, vp, vp, vp, vp]),
         "pars_dev_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, i64, i64, i64, vp, vp, vp, vp]),
         "pars_dev_xt_c": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
         "pars_sgd_epoch": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp]),
@@ -283,6 +289,40 @@ class Features:
             pass
 
 
+class PairPlan:
+    """Per-dataset plan of the length-sorted all-pairs kernel (pars_pair_plan*)."""
+
+    def __init__(self, ctx: "Context", lengths, delta: float):
+        L = _c(lengths, np.int64)
+        h = C.c_void_p()
+        _check(lib().pars_pair_plan_create(ctx.h, _p(L), len(L), delta, C.byref(h)))
+        self.ctx, self.h, self.n, self.delta = ctx, h.value, len(L), delta
+
+    @property
+    def kept(self) -> int:
+        return lib().pars_pair_plan_kept(C.c_void_p(self.h))
+
+    @property
+    def sorted(self) -> bool:
+        return bool(lib().pars_pair_plan_sorted(C.c_void_p(self.h)))
+
+    def run(self, d_scores: int, margin: float, t0: int, t1: int, d_coeff: int, d_counters: int,
+            d_partials: int, stream: int = 0):
+        _check(lib().pars_dev_allpairs_plan(self.ctx.h, C.c_void_p(self.h), d_scores, margin, t0,
+                                            t1, d_coeff, d_counters, d_partials, stream or None))
+
+    def free(self):
+        if self.h:
+            lib().pars_pair_plan_free(C.c_void_p(self.h))
+            self.h = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Context:
     """One CUDA device + its scratch (pars_ctx*)."""
 
@@ -364,15 +404,21 @@ class Context:
         return Features(self, h.value, dim)
 
     # -- pairs / training ----------------------------------------------------
-    def allpairs(self, scores, lengths, delta: float = 0.2, margin: float = 1.0):
-        """All-pairs margin ranking loss: (coeff int32[n], kept, active, loss_sum)."""
+    def allpairs(self, scores, lengths, delta: float = 0.2, margin: float = 1.0,
+                 algo: str = "sorted"):
+        """All-pairs margin ranking loss: (coeff int32[n], kept, active, loss_sum).
+        algo: "sorted" (length-sorted plan, default) or "general" (unsorted tiles)."""
         s = _c(scores, np.float64)
         L = _c(lengths, np.int64)
         c = np.zeros(len(s), np.int32)
         kept, act, loss = C.c_uint64(), C.c_uint64(), C.c_double()
-        _check(lib().pars_allpairs(self.h, _p(s), _p(L), len(s), delta, margin, _p(c),
-                                   C.byref(kept), C.byref(act), C.byref(loss)))
+        _check(lib().pars_allpairs_algo(self.h, _p(s), _p(L), len(s), delta, margin,
+                                        0 if algo == "sorted" else 1, _p(c), C.byref(kept),
+                                        C.byref(act), C.byref(loss)))
         return c, kept.value, act.value, loss.value
+
+    def pair_plan(self, lengths, delta: float = 0.2) -> "PairPlan":
+        return PairPlan(self, lengths, delta)
 
     def sgd_epoch(self, feats: Features, a, b, y, batch: int, lr: float, margin: float, w,
                   bias: float = 0.0):

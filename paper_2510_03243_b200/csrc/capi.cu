@@ -50,7 +50,7 @@ struct pars_ctx {
   std::atomic<uint64_t> launches{0};
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
-      gscratch, lists;
+      gscratch, lists, plan_buf;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -300,7 +300,7 @@ void pars_ctx_destroy(pars_ctx* c) {
   cudaStreamSynchronize(c->copy_stream);
   DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
                     &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
-                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists};
+                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists, &c->plan_buf};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (int k = 0; k < 2; ++k) {
@@ -657,7 +657,18 @@ int64_t pars_allpairs_tiles(int64_t n) { return allpairs_tile_count(n); }
 int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths, int64_t n,
                   double delta, double margin, int32_t* coeff, uint64_t* kept, uint64_t* active,
                   double* loss_sum) {
+  return pars_allpairs_algo(ctx, scores, lengths, n, delta, margin, PARS_ALLPAIRS_SORTED, coeff,
+                            kept, active, loss_sum);
+}
+
+int pars_allpairs_algo(pars_ctx* ctx, const double* scores, const int64_t* lengths, int64_t n,
+                       double delta, double margin, int algo, int32_t* coeff, uint64_t* kept,
+                       uint64_t* active, double* loss_sum) {
   PARS_TRY(check_ctx(ctx));
+  if (algo != PARS_ALLPAIRS_SORTED && algo != PARS_ALLPAIRS_GENERAL) {
+    set_error("all-pairs: unknown algorithm %d", algo);
+    return PARS_ERR_INVALID;
+  }
   if (delta < 0.0 || delta >= 1.0) {
     set_error("all-pairs: delta %g outside [0, 1)", delta);
     return PARS_ERR_INVALID;
@@ -695,8 +706,17 @@ int pars_allpairs(pars_ctx* ctx, const double* scores, const int64_t* lengths, i
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_L, L.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemsetAsync(d_c, 0, (size_t)n * 4, st));
   PARS_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 32, st));
-  PARS_TRY(launch_allpairs(ctx, d_s, d_L, (const int32_t*)ctx->dmin_buf.p, n, margin, 0, tiles,
-                           d_c, d_cnt, d_part, st));
+  PairPlanDev plan;
+  if (algo == PARS_ALLPAIRS_SORTED) {
+    PARS_TRY(ensure(ctx->plan_buf, pair_plan_scratch_bytes(n)));
+    PARS_TRY(build_pair_plan(ctx, d_L, (const int32_t*)ctx->dmin_buf.p, n, &plan, ctx->plan_buf.p, st));
+  }
+  if (algo == PARS_ALLPAIRS_SORTED && plan.monotone) {
+    PARS_TRY(launch_allpairs_sorted(ctx, plan, d_s, margin, 0, tiles, d_c, d_cnt, d_part, st));
+  } else {
+    PARS_TRY(launch_allpairs(ctx, d_s, d_L, (const int32_t*)ctx->dmin_buf.p, n, margin, 0, tiles,
+                             d_c, d_cnt, d_part, st));
+  }
   PARS_TRY(launch_sum_partials(ctx, d_part, tiles, d_loss, st));
   unsigned long long cnt[2];
   PARS_CUDA_CHECK(cudaMemcpyAsync(coeff, d_c, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
@@ -727,6 +747,104 @@ int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores, const int32_t* d_le
   PARS_TRY(ensure_dmin(ctx, delta, max_len, st));
   return launch_allpairs(ctx, d_scores, d_lengths, (const int32_t*)ctx->dmin_buf.p, n, margin,
                          tile_begin, tile_end, d_coeff, d_counters, d_loss_partials, st);
+}
+
+}  // extern "C"
+
+struct pars_pair_plan {
+  pars_ctx* ctx = nullptr;
+  PairPlanDev dev;
+  void* scratch = nullptr;
+  int32_t* d_L = nullptr;     // lengths in input order (general-kernel fallback)
+  int32_t* d_dmin = nullptr;  // Eq. 1 table for this plan's delta
+  int64_t max_len = 0;
+  double delta = 0.0;
+};
+
+extern "C" {
+
+// Per-dataset plan of the length-sorted all-pairs kernel (lengths do not
+// change across training steps; scores do).
+int pars_pair_plan_create(pars_ctx* ctx, const int64_t* lengths, int64_t n, double delta,
+                          pars_pair_plan** out) {
+  *out = nullptr;
+  PARS_TRY(check_ctx(ctx));
+  if (delta < 0.0 || delta >= 1.0) {
+    set_error("all-pairs: delta %g outside [0, 1)", delta);
+    return PARS_ERR_INVALID;
+  }
+  std::vector<int32_t> L((size_t)std::max<int64_t>(n, 1));
+  int64_t max_len = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (lengths[i] < 0 || lengths[i] > kMaxLengthTable) {
+      set_error("all-pairs: length %lld outside [0, %lld]", (long long)lengths[i],
+                (long long)kMaxLengthTable);
+      return PARS_ERR_UNSUPPORTED;
+    }
+    L[i] = (int32_t)lengths[i];
+    max_len = std::max<int64_t>(max_len, lengths[i]);
+  }
+  std::vector<int32_t> table((size_t)max_len + 1);
+  PARS_TRY(pars_length_gap_table(delta, max_len, table.data()));
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  auto* p = new pars_pair_plan();
+  p->ctx = ctx;
+  p->max_len = max_len;
+  p->delta = delta;
+  auto fail = [&](int rc) {
+    if (p->scratch) cudaFree(p->scratch);
+    if (p->d_L) cudaFree(p->d_L);
+    if (p->d_dmin) cudaFree(p->d_dmin);
+    delete p;
+    return rc;
+  };
+  if (cudaMalloc(&p->scratch, pair_plan_scratch_bytes(n)) != cudaSuccess ||
+      cudaMalloc(&p->d_L, L.size() * 4) != cudaSuccess ||
+      cudaMalloc(&p->d_dmin, table.size() * 4) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed (pair plan)");
+    return fail(PARS_ERR_OOM);
+  }
+  if (cudaMemcpyAsync(p->d_L, L.data(), L.size() * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(p->d_dmin, table.data(), table.size() * 4, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess) {
+    set_error("CUDA error uploading the pair plan");
+    return fail(PARS_ERR_CUDA);
+  }
+  int rc = build_pair_plan(ctx, p->d_L, p->d_dmin, n, &p->dev, p->scratch, st);
+  if (rc != PARS_OK) return fail(rc);
+  *out = p;
+  return PARS_OK;
+}
+
+uint64_t pars_pair_plan_kept(const pars_pair_plan* p) { return p ? p->dev.kept : 0; }
+int pars_pair_plan_sorted(const pars_pair_plan* p) { return p && p->dev.monotone ? 1 : 0; }
+
+void pars_pair_plan_free(pars_pair_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  cudaFree(p->scratch);
+  cudaFree(p->d_L);
+  cudaFree(p->d_dmin);
+  delete p;
+}
+
+int pars_dev_allpairs_plan(pars_ctx* ctx, const pars_pair_plan* p, const double* d_scores,
+                           double margin, int64_t tile_begin, int64_t tile_end, int32_t* d_coeff,
+                           unsigned long long* d_counters, double* d_loss_partials, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  if (!p) {
+    set_error("null pair plan");
+    return PARS_ERR_INVALID;
+  }
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  if (p->dev.monotone)
+    return launch_allpairs_sorted(ctx, p->dev, d_scores, margin, tile_begin, tile_end, d_coeff,
+                                  d_counters, d_loss_partials, st);
+  return launch_allpairs(ctx, d_scores, p->d_L, p->d_dmin, p->dev.n, margin, tile_begin, tile_end,
+                         d_coeff, d_counters, d_loss_partials, st);
 }
 
 int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff, int64_t row_begin,

@@ -25,42 +25,14 @@
 
 #include "common.cuh"
 #include "pairs.cuh"
+#include "tiles.cuh"
 
 namespace pars_b200 {
 
 namespace {
 
-constexpr int kTile = 256;
+constexpr int kTile = kPairTile;
 constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ void tile_of(int64_t t, int64_t nt, int64_t* I, int64_t* J) {
-  // row-major enumeration of the upper triangle (J >= I)
-  // rows start at s(I) = I*nt - I*(I-1)/2
-  double b = 2.0 * (double)nt + 1.0;
-  int64_t i = (int64_t)floor((b - sqrt(b * b - 8.0 * (double)t)) / 2.0);
-  if (i < 0) i = 0;
-  if (i > nt - 1) i = nt - 1;
-  auto start = [&](int64_t r) { return r * nt - r * (r - 1) / 2; };
-  while (i > 0 && start(i) > t) --i;
-  while (i + 1 < nt && start(i + 1) <= t) ++i;
-  *I = i;
-  *J = i + (t - start(i));
-}
-
-template <typename T>
-__device__ __forceinline__ T block_sum_fixed(T v, T* red) {
-  // fixed-order block reduction (deterministic for floating point)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(kFull, v, o);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  T r = 0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[w];
-  __syncthreads();
-  return r;
-}
 
 __global__ void __launch_bounds__(kTile) allpairs_kernel(
     const double* __restrict__ s, const int32_t* __restrict__ L,

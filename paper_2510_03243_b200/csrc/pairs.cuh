@@ -18,6 +18,25 @@ int launch_xtc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const doub
                const int32_t* c, int64_t r0, int64_t r1, uint32_t dim, double* partial,
                double* grad, cudaStream_t st);
 
+// length-sorted all-pairs plan (pairs_sorted.cu)
+struct PairPlanDev {
+  int64_t n = 0;
+  uint32_t* perm = nullptr;  // sorted position -> input index (stable by length)
+  int32_t* Ls = nullptr;     // sorted lengths
+  int32_t* f = nullptr;      // first kept column of each sorted row
+  double* ss = nullptr;      // per call: sorted scores
+  double* T = nullptr;       // per call: hinge thresholds
+  int32_t* cs = nullptr;     // per call: coefficients in sorted order
+  unsigned long long kept = 0;
+  bool monotone = true;  // g_j = L_j - dmin[L_j] non-decreasing (suffix masks valid)
+};
+size_t pair_plan_scratch_bytes(int64_t n);
+int build_pair_plan(pars_ctx* ctx, const int32_t* d_L, const int32_t* d_dmin, int64_t n,
+                    PairPlanDev* p, void* scratch, cudaStream_t st);
+int launch_allpairs_sorted(pars_ctx* ctx, const PairPlanDev& p, const double* d_scores,
+                           double margin, int64_t t0, int64_t t1, int32_t* d_coeff,
+                           unsigned long long* d_counters, double* d_loss_part, cudaStream_t st);
+
 // priority sort (sort.cu)
 struct SortBuffers {
   uint64_t* khi[2];

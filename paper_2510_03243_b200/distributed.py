@@ -59,8 +59,9 @@ def _dist():
     return dist
 
 
-def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream):
-    """Per-rank compute on the GPU for tiles [t0, t1)."""
+def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream, plan=None):
+    """Per-rank compute on the GPU for tiles [t0, t1): the length-sorted
+    kernel when a PairPlan is given, else the general tiled kernel."""
     import torch
     from ._lib import ParsError, lib
 
@@ -69,11 +70,15 @@ def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream):
         c = torch.zeros(n, dtype=torch.int32, device=dev)
         cnt = torch.zeros(4, dtype=torch.int64, device=dev)
         part = torch.zeros(max(1, t1 - t0), dtype=torch.float64, device=dev)
-        rc = lib().pars_dev_allpairs(ctx.h, d_scores.data_ptr(), d_lengths.data_ptr(), n, delta,
-                                     margin, max_len, t0, t1, c.data_ptr(), cnt.data_ptr(),
-                                     part.data_ptr(), stream)
-        if rc != 0:
-            raise ParsError(rc, lib().pars_last_error().decode())
+        if plan is not None:
+            plan.run(d_scores.data_ptr(), margin, t0, t1, c.data_ptr(), cnt.data_ptr(),
+                     part.data_ptr(), stream or 0)
+        else:
+            rc = lib().pars_dev_allpairs(ctx.h, d_scores.data_ptr(), d_lengths.data_ptr(), n, delta,
+                                         margin, max_len, t0, t1, c.data_ptr(), cnt.data_ptr(),
+                                         part.data_ptr(), stream)
+            if rc != 0:
+                raise ParsError(rc, lib().pars_last_error().decode())
         return c, cnt[:2], part[: max(0, t1 - t0)]
 
     return run
@@ -108,10 +113,11 @@ def allpairs_dp(n: int, compute: Callable, group=None):
 
 
 def allpairs_step_gpu(ctx, d_scores, d_lengths, n: int, delta: float, margin: float, max_len: int,
-                      stream: int = 0, group=None):
-    """The C5 exchange step on GPUs (NCCL when the group is initialised)."""
+                      stream: int = 0, group=None, plan=None):
+    """The C5 exchange step on GPUs (NCCL when the group is initialised).
+    `plan` (Context.pair_plan(lengths, delta)) selects the length-sorted kernel."""
     return allpairs_dp(n, _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len,
-                                     stream or None), group)
+                                     stream or None, plan), group)
 
 
 def grad_step_gpu(ctx, feats, d_coeff, scale: float, group=None, stream: int = 0):

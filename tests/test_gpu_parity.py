@@ -142,15 +142,46 @@ def test_priority_order_large_random_with_ties(ctx, oracle):
     assert (got == want).all()
 
 
-def test_allpairs_matches_oracle(ctx, oracle):
+@pytest.mark.parametrize("algo", ["sorted", "general"])
+def test_allpairs_matches_oracle(ctx, oracle, algo):
     rng = np.random.default_rng(3)
     for n in (1, 2, 255, 256, 257, 3001):
         lens = rng.integers(1, 400, size=n)
         s = rng.normal(size=n)
-        c, kept, act, loss = ctx.allpairs(s, lens, 0.2, 1.0)
+        c, kept, act, loss = ctx.allpairs(s, lens, 0.2, 1.0, algo=algo)
         oc, okept, oact, oloss = oracle.allpairs(s, lens, 0.2, 1.0)
         assert (c == oc).all() and kept == okept and act == oact
         assert abs(loss - oloss) <= 1e-12 * max(1.0, abs(oloss))
+
+
+@pytest.mark.parametrize("algo", ["sorted", "general"])
+def test_allpairs_hinge_edge_cases(ctx, oracle, algo):
+    """Ties in scores and lengths, +-0.0, scores exactly margin apart, tiny
+    and huge magnitudes, margin 0: the active set must match bit-exactly."""
+    rng = np.random.default_rng(11)
+    n = 1500
+    base = np.array([0.0, -0.0, 1.0, -1.0, 0.5, 1e-300, -1e-300, 3.0, 2.0, 1e15, -1e15,
+                     0.1, 0.2, 0.30000000000000004, np.nextafter(1.0, 2.0)])
+    s = rng.choice(base, size=n) + rng.choice([0.0, 1.0, -1.0], size=n)
+    lens = rng.choice([1, 2, 3, 5, 8, 10, 12, 50, 51, 60, 1000], size=n)
+    for margin in (1.0, 0.0, 0.5):
+        for delta in (0.2, 0.0, 0.5):
+            c, kept, act, loss = ctx.allpairs(s, lens, delta, margin, algo=algo)
+            oc, okept, oact, oloss = oracle.allpairs(s, lens, delta, margin)
+            assert (c == oc).all() and kept == okept and act == oact, (margin, delta)
+            assert abs(loss - oloss) <= 1e-9 * max(1.0, abs(oloss))
+
+
+def test_pair_plan_kept_counts_match_exhaustive_goldens(ctx):
+    """The plan's exact kept count equals the exhaustive Eq. 1 counts of
+    SURVEY Appendix B (C2: 30,028,032; C5: 1,920,977,782)."""
+    from paper_2510_03243_b200 import Workload
+    g = golden("mask_counts.json")
+    for key in ("8192_21", "65536_25", "1024_22"):
+        e = g[key]
+        wl = Workload.synthesize(e["n"], e["seed"], mu=e["mu"], sigma=e["sigma"])
+        plan = ctx.pair_plan(wl.output_len, e["delta"])
+        assert plan.sorted and plan.kept == e["kept"]
 
 
 def test_allpairs_c2_mask_count(ctx):
@@ -286,8 +317,14 @@ def test_distributed_allpairs_step_single_rank(ctx, oracle):
     with torch.cuda.stream(stream):
         d_s = torch.from_numpy(s).to(dev)
         d_L = torch.from_numpy(wl.output_len.astype(np.int32)).to(dev)
+        plan = ctx.pair_plan(wl.output_len, 0.2)
         c, kept, act, loss = D.allpairs_step_gpu(ctx, d_s, d_L, len(s), 0.2, 1.0,
-                                                 int(wl.output_len.max()), stream=stream.cuda_stream)
+                                                 int(wl.output_len.max()), stream=stream.cuda_stream,
+                                                 plan=plan)
+        c2, kept2, act2, loss2 = D.allpairs_step_gpu(ctx, d_s, d_L, len(s), 0.2, 1.0,
+                                                     int(wl.output_len.max()),
+                                                     stream=stream.cuda_stream)
+        assert (c2.cpu().numpy() == c.cpu().numpy()).all() and (kept2, act2) == (kept, act)
         oc, okept, oact, oloss = oracle.allpairs(s, wl.output_len, 0.2, 1.0)
         assert (c.cpu().numpy() == oc).all() and kept == okept and act == oact
         assert abs(loss - oloss) <= 1e-12 * max(1.0, oloss)
