@@ -16,7 +16,10 @@
 //                   digit — typically the constant high exponent bytes and the
 //                   unused high bytes of tie_rank);
 //   radix_hist      per-CTA digit counts of the current order (digit-major);
-//   radix_scan      exclusive scan of the [256][ctas] table (one CTA);
+//   radix_scan_digits  per digit, the exclusive scan of its per-CTA counts
+//                   (one warp per digit, global base from the all-digit
+//                   histogram); tie-rank digits are skipped when the ranks
+//                   are already non-decreasing in input order;
 //   radix_scatter   stable rank within the CTA via warp __match_any_sync +
 //                   per-warp digit counters, then a scattered write.
 #include <cuda_runtime.h>
@@ -61,6 +64,9 @@ __global__ void radix_init(const double* __restrict__ score, const uint8_t* __re
     khi[i] = hi;
     klo[i] = lo;
     val[i] = (uint32_t)i;
+    // tie ranks already non-decreasing in input order -> the stable sort
+    // by score alone yields the (score, tie, index) order: skip tie digits
+    if (i > 0 && tie[i] < tie[i - 1]) dh[12 * 256] = 1u;
 #pragma unroll
     for (int p = 0; p < 12; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, p)], 1u);
   }
@@ -85,26 +91,27 @@ __global__ void __launch_bounds__(kThreads) radix_hist(const uint64_t* __restric
   hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(1024) radix_scan(uint32_t* __restrict__ a, int64_t m) {
-  __shared__ uint32_t part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (m + 1023) / 1024;
-  const int64_t b = t * per, e = min(m, b + per);
-  uint32_t s = 0;
-  for (int64_t i = b; i < e; ++i) s += a[i];
-  part[t] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    uint32_t v = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
-  }
-  uint32_t run = part[t] - s;
-  for (int64_t i = b; i < e; ++i) {
-    const uint32_t v = a[i];
-    a[i] = run;
-    run += v;
+// Exclusive offsets of one digit position: block d (one warp) scans digit
+// d's per-CTA counts in CTA order, starting from the digit's global base
+// (sum of the all-digit histogram's counts of smaller digits).
+__global__ void __launch_bounds__(32) radix_scan_digits(uint32_t* __restrict__ hist, int nblocks,
+                                                        const uint32_t* __restrict__ dh_pos) {
+  const int d = blockIdx.x, lane = threadIdx.x;
+  uint32_t base = 0;
+  for (int k = lane; k < d; k += 32) base += dh_pos[k];
+  base = __reduce_add_sync(0xffffffffu, base);
+  uint32_t* row = hist + (int64_t)d * nblocks;
+  for (int b0 = 0; b0 < nblocks; b0 += 32) {
+    const int b = b0 + lane;
+    const uint32_t v = b < nblocks ? row[b] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b < nblocks) row[b] = base + x - v;
+    base += __shfl_sync(0xffffffffu, x, 31);
   }
 }
 
@@ -190,8 +197,8 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   uint32_t* klo[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
   uint32_t* val[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
   uint32_t* hist = (uint32_t*)take((size_t)nb * 256 * 4);
-  uint32_t* dh = (uint32_t*)take(12 * 256 * 4);
-  PARS_CUDA_CHECK(cudaMemsetAsync(dh, 0, 12 * 256 * 4, st));
+  uint32_t* dh = (uint32_t*)take(12 * 256 * 4 + 16);
+  PARS_CUDA_CHECK(cudaMemsetAsync(dh, 0, 12 * 256 * 4 + 16, st));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -199,17 +206,18 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   radix_init<<<(unsigned)ig, 256, 0, st>>>(score, boosted, tie, n, khi[0], klo[0], val[0], dh);
   count_launch(ctx);
   PARS_CUDA_CHECK(cudaGetLastError());
-  std::vector<uint32_t> hh(12 * 256);
+  std::vector<uint32_t> hh(12 * 256 + 1);
   PARS_CUDA_CHECK(cudaMemcpyAsync(hh.data(), dh, hh.size() * 4, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  const bool tie_sorted = hh[12 * 256] == 0;
   int cur = 0;
-  for (int pos = 0; pos < 12; ++pos) {
+  for (int pos = tie_sorted ? 4 : 0; pos < 12; ++pos) {
     bool trivial = false;
     for (int d = 0; d < 256; ++d)
       if (hh[pos * 256 + d] == (uint32_t)n) trivial = true;
     if (trivial) continue;
     radix_hist<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], n, pos, nb, hist);
-    radix_scan<<<1, 1024, 0, st>>>(hist, (int64_t)nb * 256);
+    radix_scan_digits<<<256, 32, 0, st>>>(hist, nb, dh + pos * 256);
     radix_scatter<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], val[cur], khi[cur ^ 1],
                                            klo[cur ^ 1], val[cur ^ 1], n, pos, nb, hist);
     count_launch(ctx, 3);
