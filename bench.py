@@ -138,27 +138,31 @@ def shard(n, world, rank):
     return min(n, rank * per), min(n, (rank + 1) * per)
 
 
-def cpu_reference_scoring(wl, w, sample_n, threads):
+class CpuReferenceScoring:
     """The reference library (oracle/_ref, compiled from /root/reference) on
-    the host cores: Scorer::score_batch (OpenMP) + select_batch over a
-    bounded sample of the same workload."""
-    from oracle.bind import Extractor as OEx
-    from oracle.bind import Ref
-    R = Ref()
-    R.set_threads(threads)
-    b, e = 0, sample_n
-    offs = wl.offsets[b:e + 1] - wl.offsets[b]
-    text = wl.text[wl.offsets[b]:wl.offsets[e]]
-    ds = R.from_arrays(text, offs, wl.output_len[b:e], wl.prompt_len[b:e])
-    ids = ["p%06d" % i for i in range(sample_n)]
-    ex = OEx.make()
-    R.score_batch(ex, ds, w)  # warm
-    t0 = time.perf_counter()
-    s = R.score_batch(ex, ds, w)
-    t1 = time.perf_counter()
-    R.select_batch(np.zeros(sample_n), ids, s, np.zeros(sample_n, np.uint8), 0.0, sample_n)
-    t2 = time.perf_counter()
-    return sample_n / (t2 - t0), (t1 - t0), (t2 - t1), s
+    the host cores: Scorer::score_batch (OpenMP, all threads) + select_batch
+    over a bounded sample of the same workload."""
+
+    def __init__(self, wl, w, sample_n, threads):
+        from oracle.bind import Extractor as OEx
+        from oracle.bind import Ref
+        self.R = R = Ref()
+        R.set_threads(threads)
+        self.n = n = min(sample_n, len(wl))
+        offs = wl.offsets[: n + 1] - wl.offsets[0]
+        text = wl.text[wl.offsets[0]:wl.offsets[n]]
+        self.ds = R.from_arrays(text, offs, wl.output_len[:n], wl.prompt_len[:n])
+        self.ids = ["p%06d" % i for i in range(n)]
+        self.ex = OEx.make()
+        self.w = w
+
+    def step(self):
+        t0 = time.perf_counter()
+        s = self.R.score_batch(self.ex, self.ds, self.w)
+        t1 = time.perf_counter()
+        self.R.select_batch(np.zeros(self.n), self.ids, s, np.zeros(self.n, np.uint8), 0.0, self.n)
+        t2 = time.perf_counter()
+        return self.n / (t2 - t0), t1 - t0, t2 - t1
 
 
 def host_threads():
@@ -180,12 +184,12 @@ def run_reference(args):
     wl = Workload.synthesize(sample, SEED, pad_tokens=PAD_TOKENS, pad_seed=PAD_SEED)
     w = np.random.default_rng(1234).normal(size=DIM) * 0.05
     threads = host_threads()
+    ref = CpuReferenceScoring(wl, w, sample, threads)
     vals = []
     for _ in range(args.warmup):
-        cpu_reference_scoring(wl, w, sample, threads)
+        ref.step()
     for _ in range(args.steps):
-        v, _, _, _ = cpu_reference_scoring(wl, w, sample, threads)
-        vals.append(v)
+        vals.append(ref.step()[0])
     value = float(np.median(vals))
     line = {
         "impl": "reference", "metric": "prompts scored/s", "value": value, "unit": "prompts/s",
@@ -320,6 +324,9 @@ def run_ours(args):
     d2h = 8 * n + 4 * n
 
     # secondary: C5 all-pairs step (filtered pairs/s)
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = bench_configs(P, ctx, args)
     pairs = None
     if not args.no_pairs:
         pairs = bench_pairs(P, ctx, torch, dev, stream, world, rank, args)
@@ -329,10 +336,12 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu:
             thr = host_threads()
-            v, ts, tsel, _ = cpu_reference_scoring(wl, w, args.cpu_sample, thr)
+            ref = CpuReferenceScoring(wl, w, args.cpu_sample, thr)
+            ref.step()  # warm
+            v, ts, tsel = ref.step()
             cpu = {"value": v, "unit": "prompts/s", "cores": thr, "kind": "reference",
-                   "sample": f"first {args.cpu_sample} prompts of the same C4 workload: "
-                             f"score_batch ({ts:.2f} s, OpenMP {thr} threads) + select_batch ({tsel:.3f} s)"}
+                   "sample": f"first {ref.n} prompts of the same C4 workload: score_batch "
+                             f"({ts:.2f} s, OpenMP {thr} threads) + select_batch ({tsel:.3f} s)"}
         line = {
             "metric": "prompts scored/s", "value": value, "unit": "prompts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -355,6 +364,7 @@ def run_ours(args):
             "clocks": clk,
             "parity": {"scores_bitexact_sample": parity_ok, "sample": chk},
             "pairs": pairs,
+            "configs": configs,
             "workload_gen_s": t_gen,
         }
         print(json.dumps(line))
@@ -411,6 +421,100 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident"}
 
 
+def fnv64(a: np.ndarray) -> str:
+    h = 0xCBF29CE484222325
+    for b in a.astype("<u8" if a.dtype != np.float64 else "<f8").tobytes():
+        h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def bench_configs(P, ctx, args):
+    """BASELINE configs C1 and C2 (1 GPU, host-buffer API, latency-bound) and
+    the CPU side of C5, each next to the reference CPU path on this host and
+    with its golden parity anchor."""
+    out = {}
+    thr = host_threads()
+    ex = P.Extractor.make()
+    have_ref = not args.no_cpu
+    if have_ref:
+        from oracle.bind import Extractor as OEx
+        from oracle.bind import Oracle, Ref
+        R = Ref()
+        R.set_threads(thr)
+    # ---- C1: README model, score 1,024 prompts (<=128 tokens) + SJF order
+    full = P.Workload.synthesize(4000, 21)
+    # split_dataset(0.2, 21) of the reference: train part, restated through the
+    # reference library when available (the model itself is trained on the GPU)
+    if have_ref:
+        rfull = R.synthesize(4000, 21)
+        tr, _ = R.split(rfull, 0.2, 21)
+        t0 = time.perf_counter()
+        w, _, lt = ctx.train_pairwise(ex, tr.text, tr.offs, tr.output_len, seed=21)
+        t_train = time.perf_counter() - t0
+        g = P.Workload.synthesize(2048, 22)
+        sel = np.nonzero(g.prompt_len <= 128)[0][:1024]
+        arena, offs = P.pack_texts([g.prompt(i) for i in sel])
+        ids = ["p%06d" % i for i in sel]
+        tie = P.tie_ranks(np.zeros(len(sel)), ids)
+        lat = []
+        for k in range(13):
+            t0 = time.perf_counter()
+            sc = ctx.score_text(ex, arena, offs, w)
+            order = ctx.priority_order(sc, tie)
+            lat.append(time.perf_counter() - t0)
+        gpu_ms = 1e3 * float(np.median(lat[3:]))
+        c1 = R.subset(g_ref := R.synthesize(2048, 22), sel)
+        R.score_batch(OEx.make(), c1, w)
+        cl = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            rs = R.score_batch(OEx.make(), c1, w)
+            R.select_batch(np.zeros(len(sel)), ids, rs, np.zeros(len(sel), np.uint8), 0.0, len(sel))
+            cl.append(time.perf_counter() - t0)
+        out["c1"] = {"workload": "score 1,024 prompts (<=128 tokens) + SJF order, README model",
+                     "gpu_ms": gpu_ms, "gpu_prompts_per_s": len(sel) / (gpu_ms / 1e3),
+                     "cpu_ms": 1e3 * float(np.median(cl)), "cpu_threads": thr,
+                     "scores_fnv": fnv64(sc), "order_fnv": fnv64(order.astype(np.uint64)),
+                     "parity_bitexact": fnv64(sc) == "5548c3b3d81d615d"
+                     and fnv64(order.astype(np.uint64)) == "e6e78f54425df769",
+                     "readme_model_train_ms": 1e3 * t_train,
+                     "readme_weights_fnv": fnv64(w),
+                     "readme_weights_bitexact": fnv64(w) == "db7217cbd5a86b9b"}
+    # ---- C2: one training epoch on 8,192 samples
+    d2 = P.Workload.synthesize(8192, 21)
+    ts = []
+    for k in range(4):
+        t0 = time.perf_counter()
+        w2, _, lt2 = ctx.train_pairwise(ex, d2.text, d2.offsets, d2.output_len, seed=21, epochs=1)
+        ts.append(time.perf_counter() - t0)
+    gpu_epoch_ms = 1e3 * float(np.median(ts[1:]))
+    c2 = {"workload": "one margin-ranking epoch, 8,192 samples, 100k pairs, delta 0.2 "
+                      "(extract_all + build_pairs + 782 SGD steps)",
+          "gpu_epoch_ms": gpu_epoch_ms, "gpu_pairs_per_s": 100000 / (gpu_epoch_ms / 1e3),
+          "loss0": float(lt2[0]).hex(), "weights_fnv": fnv64(w2),
+          "parity_bitexact": fnv64(w2) == "f97c96a353829ee2"
+          and float(lt2[0]).hex() == "0x1.1b1e92d7700cap-1"}
+    if have_ref:
+        rd2 = R.synthesize(8192, 21)
+        t0 = time.perf_counter()
+        R.train(rd2, OEx.make(), seed=21, epochs=1)
+        c2["cpu_epoch_ms"] = 1e3 * (time.perf_counter() - t0)
+        c2["cpu_threads"] = thr
+    out["c2"] = c2
+    # ---- C5, CPU side: all-pairs mask + hinge over a bounded sample
+    if have_ref:
+        O = Oracle()
+        nS = 16384
+        wl = P.Workload.synthesize(nS, 25)
+        s = np.random.default_rng(99).normal(size=nS) * 0.05
+        t0 = time.perf_counter()
+        _, kept, _, _ = O.allpairs(s, wl.output_len, DELTA, MARGIN, threads=thr)
+        dt = time.perf_counter() - t0
+        out["c5_cpu"] = {"kind": "port", "sample": f"all pairs of the first {nS} C5-style prompts",
+                         "filtered_pairs_per_s": kept / dt, "threads": thr}
+    return out
+
+
 def main():
     global N_PROMPTS
     ap = argparse.ArgumentParser()
@@ -418,11 +522,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=20000)
+    ap.add_argument("--cpu-sample", type=int, default=200000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-pairs", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--prompts", type=int, default=N_PROMPTS, help="(profiling only) fewer prompts")
     args = ap.parse_args()
     N_PROMPTS = args.prompts
