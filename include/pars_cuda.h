@@ -178,6 +178,18 @@ int pars_sgd_epoch(pars_ctx* ctx, const pars_features* f, const uint32_t* a,
                    const uint32_t* b, const int32_t* y, int64_t npairs,
                    int32_t batch, double lr, double margin, double* w,
                    double bias, double* epoch_loss, uint64_t* active);
+/* Same, choosing the kernel: PARS_SGD_AUTO (cluster kernel when the
+ * features allow it), PARS_SGD_CLUSTER (8-CTA cluster, compact rows staged in
+ * shared memory; hashed features, dim <= 65536), PARS_SGD_SINGLE_CTA (one
+ * persistent CTA, any features). All are bit-identical to the reference. */
+#define PARS_SGD_AUTO 0
+#define PARS_SGD_CLUSTER 1
+#define PARS_SGD_SINGLE_CTA 2
+int pars_sgd_epoch_algo(pars_ctx* ctx, const pars_features* f,
+                        const uint32_t* a, const uint32_t* b, const int32_t* y,
+                        int64_t npairs, int32_t batch, double lr, double margin,
+                        double* w, double bias, double* epoch_loss,
+                        uint64_t* active, int algo);
 /* train() for Objective::Pairwise from all-zero weights: extract_all on the
  * GPU, per-epoch build_pairs with derive_seed(seed, 0x10000+e), SGD epochs.
  * loss_trace has `epochs` slots. */

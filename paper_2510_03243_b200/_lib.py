@@ -16,7 +16,8 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libpars_cuda.so"
+LIB_PATH = Path(os.environ.get("PARS_CUDA_LIB", "") or
+                (Path(__file__).resolve().parent / "libpars_cuda.so"))
 
 MODE_EXACT = 0  # PARS_MODE_EXACT_F64
 MODE_FAST = 1  # PARS_MODE_FAST_F32
@@ -100,6 +101,8 @@ def _load() -> C.CDLL:
         "pars_dev_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, i64, i64, i64, vp, vp, vp, vp]),
         "pars_dev_xt_c": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
         "pars_sgd_epoch": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp]),
+        "pars_sgd_epoch_algo": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp,
+                                          C.c_int]),
         "pars_train_pairwise": (C.c_int, [vp, vp, vp, vp, vp, i64, dbl, dbl, i32, i32, dbl, u64,
                                           u64, vp, vp, vp]),
         "pars_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp]),
@@ -421,12 +424,16 @@ class Context:
         return PairPlan(self, lengths, delta)
 
     def sgd_epoch(self, feats: Features, a, b, y, batch: int, lr: float, margin: float, w,
-                  bias: float = 0.0):
+                  bias: float = 0.0, algo: str = "auto"):
+        """One pairwise SGD epoch (train.cpp:154-166). algo: "auto", "cluster"
+        (8-CTA cluster kernel) or "single" (one persistent CTA)."""
         w = np.array(w, np.float64, copy=True)
         a, b, y = _c(a, np.uint32), _c(b, np.uint32), _c(y, np.int32)
         el, act = C.c_double(), C.c_uint64()
-        _check(lib().pars_sgd_epoch(self.h, C.c_void_p(feats.h), _p(a), _p(b), _p(y), len(a), batch,
-                                    lr, margin, _p(w), bias, C.byref(el), C.byref(act)))
+        code = {"auto": 0, "cluster": 1, "single": 2}[algo]
+        _check(lib().pars_sgd_epoch_algo(self.h, C.c_void_p(feats.h), _p(a), _p(b), _p(y), len(a),
+                                         batch, lr, margin, _p(w), bias, C.byref(el),
+                                         C.byref(act), code))
         return w, el.value, act.value
 
     def train_pairwise(self, ex: Extractor, text, offsets, lengths, delta=0.2, margin=1.0,

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "featurize.cuh"
 #include "pairs.cuh"
+#include "sgd_cluster.cuh"
 
 namespace pars_b200 {
 
@@ -65,6 +66,14 @@ struct pars_features {
   uint32_t* d_idx = nullptr;
   double* d_val = nullptr;
   std::vector<int64_t> h_rp;  // host mirror of the row pointers
+  // hashed features only: integer bucket counts and per-row L2 factors
+  // (val = count * inv exactly) — the compact form the SGD cluster kernel reads
+  int32_t* d_cnt = nullptr;
+  double* d_inv = nullptr;
+  uint32_t* d_cpk = nullptr;      // rows of (idx << 16 | count16), 4-entry aligned
+  uint32_t* d_cpk_off = nullptr;  // row offsets into d_cpk (entries)
+  std::vector<uint32_t> h_cpk_off;
+  int cpk_state = 0;  // 0 not built, 1 built, -1 not representable
 };
 
 namespace pars_b200 {
@@ -134,14 +143,16 @@ __global__ void csr_score_kernel(const int64_t* __restrict__ rp, const uint32_t*
 // Compact per-prompt slots into a CSR.
 __global__ void compact_kernel(const int64_t* __restrict__ slot, const int64_t* __restrict__ rp,
                                int64_t n, const uint32_t* __restrict__ sidx,
-                               const double* __restrict__ sval, uint32_t* __restrict__ idx,
-                               double* __restrict__ val) {
+                               const double* __restrict__ sval, const int32_t* __restrict__ scnt,
+                               uint32_t* __restrict__ idx, double* __restrict__ val,
+                               int32_t* __restrict__ cnt) {
   const int64_t i = blockIdx.x;
   if (i >= n) return;
   const int64_t s = slot[i], b = rp[i], e = rp[i + 1];
   for (int64_t k = threadIdx.x; k < e - b; k += blockDim.x) {
     idx[b + k] = sidx[s + k];
     val[b + k] = sval[s + k];
+    cnt[b + k] = scnt[s + k];
   }
 }
 
@@ -472,10 +483,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   f->rows = n;
   f->h_rp.assign((size_t)n + 1, 0);
   auto fail_free = [&](int rc) {
-    if (f->d_rp) cudaFree(f->d_rp);
-    if (f->d_idx) cudaFree(f->d_idx);
-    if (f->d_val) cudaFree(f->d_val);
-    delete f;
+    pars_features_free(f);
     return rc;
   };
   if (ex->kind == 1) {
@@ -516,7 +524,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   int rc = PARS_OK;
   if ((rc = ensure(ctx->text[0], (size_t)tb + 16)) != PARS_OK ||
       (rc = ensure(ctx->offs[0], (size_t)(n + 1) * 8)) != PARS_OK ||
-      (rc = ensure(ctx->misc, (size_t)std::max<int64_t>(cap_total, 1) * 12 + (size_t)(n + 1) * 8 * 2 + 1024)) != PARS_OK ||
+      (rc = ensure(ctx->misc, (size_t)std::max<int64_t>(cap_total, 1) * 16 + (size_t)(n + 1) * 8 * 2 + 1024)) != PARS_OK ||
       (rc = ensure(ctx->longl, (size_t)std::max<int64_t>(n, 1) * 4 + 16)) != PARS_OK ||
       (rc = ensure(ctx->scores[0], (size_t)std::max<int64_t>(n, 1) * 8)) != PARS_OK)
     return fail_free(rc);
@@ -525,7 +533,13 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   int64_t* d_rp_tmp = d_slot + (n + 1);
   uint32_t* s_idx = (uint32_t*)(d_rp_tmp + (n + 1));
   double* s_val = (double*)(((uintptr_t)(s_idx + cap_total) + 15) & ~(uintptr_t)15);
+  int32_t* s_cnt = (int32_t*)(s_val + cap_total);
   int32_t* d_nnz = (int32_t*)ctx->scores[0].p;
+  if (cudaMalloc(&f->d_inv, (size_t)std::max<int64_t>(n, 1) * 8) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed (extract)");
+    return fail_free(PARS_ERR_OOM);
+  }
   if (n > 0) {
     cudaMemcpyAsync(ctx->text[0].p, text + t0, (size_t)tb, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(ctx->offs[0].p, offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
@@ -538,6 +552,8 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
     a.out_idx = s_idx;
     a.out_val = s_val;
     a.out_nnz = d_nnz;
+    a.out_cnt = s_cnt;
+    a.out_inv = f->d_inv;
     a.long_count = (int32_t*)ctx->longl.p;
     a.long_list = (int32_t*)ctx->longl.p + 4;
     if ((rc = attach_scratch(ctx, cfg, kFeatCsr, n, &a)) != PARS_OK) return fail_free(rc);
@@ -553,14 +569,16 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   f->nnz = f->h_rp[n];
   if (cudaMalloc(&f->d_rp, (size_t)(n + 1) * 8) != cudaSuccess ||
       cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess ||
-      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess) {
+      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess ||
+      cudaMalloc(&f->d_cnt, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess) {
     cudaGetLastError();
     set_error("device allocation failed (extract)");
     return fail_free(PARS_ERR_OOM);
   }
   cudaMemcpyAsync(f->d_rp, f->h_rp.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st);
   if (n > 0) {
-    compact_kernel<<<(unsigned)n, 128, 0, st>>>(d_slot, f->d_rp, n, s_idx, s_val, f->d_idx, f->d_val);
+    compact_kernel<<<(unsigned)n, 128, 0, st>>>(d_slot, f->d_rp, n, s_idx, s_val, s_cnt, f->d_idx,
+                                                f->d_val, f->d_cnt);
     count_launch(ctx);
   }
   if (cudaStreamSynchronize(st) != cudaSuccess) {
@@ -625,9 +643,9 @@ int pars_features_download(pars_ctx* ctx, const pars_features* f, int64_t* row_p
 void pars_features_free(pars_features* f) {
   if (!f) return;
   cudaSetDevice(f->ctx->device);
-  if (f->d_rp) cudaFree(f->d_rp);
-  if (f->d_idx) cudaFree(f->d_idx);
-  if (f->d_val) cudaFree(f->d_val);
+  void* ptrs[] = {f->d_rp, f->d_idx, f->d_val, f->d_cnt, f->d_inv, f->d_cpk, f->d_cpk_off};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
   delete f;
 }
 
@@ -869,9 +887,43 @@ int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
 namespace pars_b200 {
 namespace capi_detail {
 
-int sgd_epoch_impl(pars_ctx* ctx, const pars_features* f, const uint32_t* a, const uint32_t* b,
+// Compact (idx << 16 | count16) rows for the cluster SGD kernel, built once
+// per feature set; -1 when the features are not representable that way.
+int ensure_compact(pars_ctx* ctx, pars_features* f, cudaStream_t st) {
+  if (f->cpk_state != 0) return PARS_OK;
+  f->cpk_state = -1;
+  if (!f->d_cnt || !f->d_inv || f->dim > 65536u) return PARS_OK;
+  f->h_cpk_off.assign((size_t)f->rows + 1, 0);
+  for (int64_t r = 0; r < f->rows; ++r) {
+    const int64_t len = f->h_rp[r + 1] - f->h_rp[r];
+    const uint64_t next = (uint64_t)f->h_cpk_off[r] + (uint64_t)((len + 3) & ~3ll);
+    if (next > 0xffffffffull) return PARS_OK;
+    f->h_cpk_off[r + 1] = (uint32_t)next;
+  }
+  const size_t words = std::max<size_t>(f->h_cpk_off[f->rows], 4);
+  if (cudaMalloc(&f->d_cpk, words * 4) != cudaSuccess ||
+      cudaMalloc(&f->d_cpk_off, f->h_cpk_off.size() * 4 + 16) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed (compact rows)");
+    return PARS_ERR_OOM;
+  }
+  int32_t* d_bad = reinterpret_cast<int32_t*>(f->d_cpk_off + f->h_cpk_off.size());
+  PARS_CUDA_CHECK(cudaMemcpyAsync(f->d_cpk_off, f->h_cpk_off.data(), f->h_cpk_off.size() * 4,
+                                  cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemsetAsync(d_bad, 0, 4, st));
+  PARS_TRY(build_compact_rows(ctx, f->d_rp, f->d_idx, f->d_cnt, f->rows, f->d_cpk_off, f->d_cpk,
+                              d_bad, st));
+  int32_t bad = 0;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  f->cpk_state = bad ? -1 : 1;
+  return PARS_OK;
+}
+
+int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uint32_t* b,
                    const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,
-                   double* d_w, double bias, double* epoch_loss, uint64_t* active) {
+                   double* d_w, double bias, double* epoch_loss, uint64_t* active,
+                   int algo = PARS_SGD_AUTO) {
   if (batch < 1 || batch > 32767) {
     set_error("sgd: batch size %d outside [1, 32767]", batch);
     return PARS_ERR_UNSUPPORTED;
@@ -905,14 +957,33 @@ int sgd_epoch_impl(pars_ctx* ctx, const pars_features* f, const uint32_t* a, con
   int32_t* d_y = (int32_t*)(d_b + npairs);
   double* d_loss = (double*)(((uintptr_t)(d_y + npairs) + 15) & ~(uintptr_t)15);
   unsigned long long* d_act = (unsigned long long*)(d_loss + 1);
-  const size_t sb = sgd_scratch_bytes(nb, batch, f->dim, total) + 4096;
+  bool cluster = false;
+  if (algo != PARS_SGD_SINGLE_CTA && 2 * (int64_t)batch <= 65535 &&
+      sgd_cluster_smem(f->dim, batch) <= 227 * 1024) {
+    PARS_TRY(ensure_compact(ctx, f, st));
+    cluster = f->cpk_state == 1;
+  }
+  if (algo == PARS_SGD_CLUSTER && !cluster) {
+    set_error("sgd: the cluster kernel needs hashed features with dim <= 65536 and batch <= %d",
+              32767);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  const size_t sb = (cluster ? sgd_cluster_scratch_bytes(nb, f->dim, total, npairs)
+                             : sgd_scratch_bytes(nb, batch, f->dim, total)) + 4096;
   PARS_TRY(ensure(ctx->sgd, sb));
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_a, a, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, b, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_y, y, (size_t)npairs * 4, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->sgd.p, ent_off.data(), ent_off.size() * 8, cudaMemcpyHostToDevice, st));
-  PARS_TRY(launch_sgd_epoch(ctx, f->d_rp, f->d_idx, f->d_val, f->dim, d_a, d_b, d_y, npairs, batch,
-                            lr, margin, bias, d_w, d_loss, d_act, total, ctx->sgd.p, sb, st));
+  if (cluster) {
+    PARS_TRY(launch_sgd_cluster(ctx, f->d_rp, f->d_cpk, f->d_cpk_off, f->d_inv, f->dim, d_a, d_b,
+                                d_y, npairs, batch, lr, margin, bias, d_w, d_loss, d_act, total,
+                                ctx->sgd.p, st));
+  } else {
+    PARS_TRY(launch_sgd_epoch(ctx, f->d_rp, f->d_idx, f->d_val, f->dim, d_a, d_b, d_y, npairs,
+                              batch, lr, margin, bias, d_w, d_loss, d_act, total, ctx->sgd.p, sb,
+                              st));
+  }
   unsigned long long act = 0;
   PARS_CUDA_CHECK(cudaMemcpyAsync(epoch_loss, d_loss, 8, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(&act, d_act, 8, cudaMemcpyDeviceToHost, st));
@@ -927,12 +998,26 @@ int sgd_epoch_impl(pars_ctx* ctx, const pars_features* f, const uint32_t* a, con
 int pars_sgd_epoch(pars_ctx* ctx, const pars_features* f, const uint32_t* a, const uint32_t* b,
                    const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,
                    double* w, double bias, double* epoch_loss, uint64_t* active) {
+  return pars_sgd_epoch_algo(ctx, f, a, b, y, npairs, batch, lr, margin, w, bias, epoch_loss,
+                             active, PARS_SGD_AUTO);
+}
+
+int pars_sgd_epoch_algo(pars_ctx* ctx, const pars_features* fc, const uint32_t* a,
+                        const uint32_t* b, const int32_t* y, int64_t npairs, int32_t batch,
+                        double lr, double margin, double* w, double bias, double* epoch_loss,
+                        uint64_t* active, int algo) {
   PARS_TRY(check_ctx(ctx));
+  if (algo < PARS_SGD_AUTO || algo > PARS_SGD_SINGLE_CTA) {
+    set_error("sgd: unknown algorithm %d", algo);
+    return PARS_ERR_INVALID;
+  }
+  pars_features* f = const_cast<pars_features*>(fc);  // compact rows are a lazily built cache
   Guard g(ctx);
   PARS_TRY(ensure(ctx->misc2, (size_t)f->dim * 8));
   double* d_w = (double*)ctx->misc2.p;
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_w, w, (size_t)f->dim * 8, cudaMemcpyHostToDevice, ctx->stream));
-  PARS_TRY(sgd_epoch_impl(ctx, f, a, b, y, npairs, batch, lr, margin, d_w, bias, epoch_loss, active));
+  PARS_TRY(sgd_epoch_impl(ctx, f, a, b, y, npairs, batch, lr, margin, d_w, bias, epoch_loss, active,
+                          algo));
   PARS_CUDA_CHECK(cudaMemcpyAsync(w, d_w, (size_t)f->dim * 8, cudaMemcpyDeviceToHost, ctx->stream));
   PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   return PARS_OK;

@@ -474,6 +474,7 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
           const int64_t o = slot + row_pos + pos + __popc(nz & ((1u << j) - 1));
           a.out_idx[o] = w.b0 + j;
           a.out_val[o] = v;
+          if (a.out_cnt) a.out_cnt[o] = cnt[j];
         }
       row_pos += tot;
     }
@@ -486,7 +487,10 @@ __device__ void finish_prompt(const FeatConfig& c, const WarpSmem& S, const Feat
     const float finv = (float)inv_norm(c, warp_sum_i64(sq));
     if (lane == 0) a.scores[i] = (double)(facc * finv) + a.bias;
   } else {
-    if (lane == 0) a.out_nnz[i] = (int32_t)row_pos;
+    if (lane == 0) {
+      a.out_nnz[i] = (int32_t)row_pos;
+      if (a.out_inv) a.out_inv[i] = inv;  // v = count * inv, exactly
+    }
   }
   __syncwarp();
 }

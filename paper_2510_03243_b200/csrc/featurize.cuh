@@ -40,6 +40,8 @@ struct FeatArgs {
   uint32_t* out_idx;
   double* out_val;
   int32_t* out_nnz;
+  int32_t* out_cnt;  // optional: the integer bucket count behind each value
+  double* out_inv;   // optional: per prompt, the L2 factor (1.0 without norm)
   // long-prompt hand-off (packed kernel -> wide kernel)
   int32_t* long_list;
   int32_t* long_count;

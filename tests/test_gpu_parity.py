@@ -213,7 +213,8 @@ def test_kendall_degenerate_error(ctx):
         ctx.kendall_tau(np.ones(10), np.arange(10.0))
 
 
-def test_sgd_epoch_bit_identical(ctx, oracle):
+@pytest.mark.parametrize("algo", ["cluster", "single"])
+def test_sgd_epoch_bit_identical(ctx, oracle, algo):
     from paper_2510_03243_b200 import Extractor, Workload, build_pairs
     wl = Workload.synthesize(1500, 12)
     e = Extractor.make()
@@ -221,8 +222,8 @@ def test_sgd_epoch_bit_identical(ctx, oracle):
     rp, idx, val = f.download()
     a, b, y, _ = build_pairs(wl.output_len, 0.2, 20000, 99)
     w0 = np.random.default_rng(1).normal(size=4096) * 0.01
-    for batch in (128, 1, 7, 4096):
-        w, el, act = ctx.sgd_epoch(f, a, b, y, batch, 0.1, 1.0, w0)
+    for batch in ((128, 1, 7, 4096) if algo == "single" else (128, 1, 7, 96, 200)):
+        w, el, act = ctx.sgd_epoch(f, a, b, y, batch, 0.1, 1.0, w0, algo=algo)
         ow, oel, oact = oracle.sgd_epoch(rp, idx, val, 4096, a, b, y, batch, 0.1, 1.0, w0)
         assert act == oact
         assert el.hex() == oel.hex()
@@ -333,3 +334,19 @@ def test_distributed_allpairs_step_single_rank(ctx, oracle):
     rp, idx, val = f.download()
     og = oracle.xt_c(rp, idx, val, oc, 4096)
     assert np.allclose(g, og, rtol=1e-12, atol=1e-12)
+
+
+def test_sgd_cluster_long_prompts_use_global_fallback(ctx, oracle):
+    """Rows too large for the staged buffers (2,048-token prompts) are read
+    from global memory by the cluster kernel: still bit-identical."""
+    from paper_2510_03243_b200 import Extractor, Workload, build_pairs
+    wl = Workload.synthesize(300, 14, pad_tokens=2048, pad_seed=3)
+    e = Extractor.make()
+    f = ctx.extract(e, wl.text, wl.offsets)
+    rp, idx, val = f.download()
+    a, b, y, _ = build_pairs(wl.output_len, 0.2, 3000, 5)
+    w0 = np.random.default_rng(2).normal(size=4096) * 0.01
+    w, el, act = ctx.sgd_epoch(f, a, b, y, 128, 0.1, 1.0, w0, algo="cluster")
+    ow, oel, oact = oracle.sgd_epoch(rp, idx, val, 4096, a, b, y, 128, 0.1, 1.0, w0)
+    assert act == oact and el.hex() == oel.hex()
+    assert (w.view(np.uint64) == ow.view(np.uint64)).all()
