@@ -43,6 +43,13 @@ struct DevBuf {
   size_t cap = 0;
 };
 
+// pinned host staging (grow-only): lets the chunked host-buffer calls keep
+// every copy asynchronous, so chunk k+1's upload overlaps chunk k's kernel
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
 struct pars_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -52,6 +59,7 @@ struct pars_ctx {
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
       gscratch, lists, plan_buf;
+  HostBuf h_offs[2], h_scores;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -100,6 +108,21 @@ int ensure(DevBuf& b, size_t bytes) {
       return PARS_ERR_OOM;
     }
     want = bytes;
+  }
+  b.cap = want;
+  return PARS_OK;
+}
+
+int ensure_host(HostBuf& b, size_t bytes) {
+  if (bytes <= b.cap) return PARS_OK;
+  if (b.p) cudaFreeHost(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  const size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
+  if (cudaHostAlloc(&b.p, want, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("pinned host allocation of %zu bytes failed", want);
+    return PARS_ERR_OOM;
   }
   b.cap = want;
   return PARS_OK;
@@ -314,6 +337,8 @@ void pars_ctx_destroy(pars_ctx* c) {
                     &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists, &c->plan_buf};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
+  for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores})
+    if (b->p) cudaFreeHost(b->p);
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(c->ev_copy[k]);
     cudaEventDestroy(c->ev_done[k]);
@@ -386,14 +411,26 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
     PARS_TRY(ensure(ctx->offs[b], (size_t)(max_n + 1) * 8));
     PARS_TRY(ensure(ctx->scores[b], (size_t)max_n * 8));
   }
+  // Every copy stays asynchronous: offsets go through pinned staging, scores
+  // land in pinned staging and are handed over once at the end, so the host
+  // never blocks inside the loop and chunk k+1's upload (copy stream)
+  // overlaps chunk k's kernel (compute stream). Text that is not pinned is
+  // copied as given (the driver stages it).
+  for (int b = 0; b < 2; ++b) PARS_TRY(ensure_host(ctx->h_offs[b], (size_t)(max_n + 1) * 8));
+  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
+  double* h_sc = static_cast<double*>(ctx->h_scores.p);
   // the weights upload (on st) must land before any kernel: already ordered on st
   for (int k = 0; k < nchunks; ++k) {
     const int b = k & 1;
     const int64_t i0 = starts[k], i1 = starts[k + 1], m = i1 - i0;
     const int64_t t0 = offsets[i0], tb = offsets[i1] - t0;
-    if (k >= 2) PARS_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
+    if (k >= 2) {
+      PARS_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
+      PARS_CUDA_CHECK(cudaEventSynchronize(ctx->ev_copy[b]));  // staging b is free again
+    }
+    std::memcpy(ctx->h_offs[b].p, offsets + i0, (size_t)(m + 1) * 8);
     PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->text[b].p, text + t0, (size_t)tb, cudaMemcpyHostToDevice, cs));
-    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->offs[b].p, offsets + i0, (size_t)(m + 1) * 8,
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->offs[b].p, ctx->h_offs[b].p, (size_t)(m + 1) * 8,
                                     cudaMemcpyHostToDevice, cs));
     PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_copy[b], cs));
     PARS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copy[b], 0));
@@ -401,11 +438,12 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
     const uint8_t* base = static_cast<const uint8_t*>(ctx->text[b].p) - t0;
     PARS_TRY(score_chunk(ctx, cfg, mode, base, (const int64_t*)ctx->offs[b].p, m, bias,
                          (double*)ctx->scores[b].p, st));
-    PARS_CUDA_CHECK(cudaMemcpyAsync(scores + i0, ctx->scores[b].p, (size_t)m * 8,
+    PARS_CUDA_CHECK(cudaMemcpyAsync(h_sc + i0, ctx->scores[b].p, (size_t)m * 8,
                                     cudaMemcpyDeviceToHost, st));
     PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_done[b], st));
   }
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::memcpy(scores, h_sc, (size_t)n * 8);
   return PARS_OK;
 }
 

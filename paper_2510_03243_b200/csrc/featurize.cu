@@ -42,7 +42,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRing = 256;                   // transition ring entries per warp
-constexpr int kGroup = 16;                   // prompts per exact chain group
+constexpr int kGroup = 32;                   // prompts per exact chain group (one per lane)
 constexpr uint32_t kBias2 = 0x80008000u;     // two biased 16-bit zero counters
 constexpr int64_t kNarrowMaxFeatures = 32767;  // |count| <= features: 16 bits cannot wrap
 constexpr size_t kMaxSmemPerBlock = 200 * 1024;
@@ -559,6 +559,194 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
     chain_group(c, a, lists, packed, lane, gn, g_prompt, g_off, g_cnt, g_inv);
 }
 
+// ---- sequential-lane front end (word {1} + char {3}, power-of-two dims) ----
+//
+// The prompt is cut into 32 word-aligned byte ranges, one per lane; lane l
+// owns every token that STARTS in its range (features.cpp:36-49 tokens) and
+// runs the reference's per-byte loop over it sequentially — word FNV state
+// plus the three rolling states whose last one is the char trigram ending at
+// the byte (features.cpp:80-101) — reading the text straight from global
+// memory 4 bytes at a time. Per 4-byte word the token structure comes from
+// bit masks: non-space bits (SWAR), run starts, and token ownership by the
+// carry-propagation identity ((ns + starts) ^ ns), which marks each owned run
+// plus the space that ends it. Each byte emits at most one feature: the
+// trigram ending at it (non-space byte, two non-space predecessors) or the
+// word ending just before it (space byte). No shuffles, no ring, no
+// per-token divergence beyond a lane's own range.
+constexpr uint32_t kSeqMinDim = 1024, kSeqMaxDim = 16384;
+
+__host__ __device__ inline size_t seq_table_bytes(uint32_t dim) {
+  return (size_t)dim * 2 + (size_t)dim / 8;  // biased u16 counters + touched bitmap
+}
+
+__host__ inline bool use_seq(const FeatConfig& c) {
+  return c.default_orders && c.pow2 && c.dim >= kSeqMinDim && c.dim <= kSeqMaxDim;
+}
+
+// 4 bytes at aligned position r of the aligned base a0; the prompt occupies
+// [lo, hi), bytes outside it read as ' '.
+__device__ __forceinline__ uint32_t seq_word(const uint8_t* a0, int r, int lo, int hi) {
+  if (r >= lo && r + 4 <= hi) return __ldg(reinterpret_cast<const uint32_t*>(a0 + r));
+  uint32_t w = 0x20202020u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (r + k >= lo && r + k < hi) w = (w & ~(0xffu << (8 * k))) | ((uint32_t)a0[r + k] << (8 * k));
+  return w;
+}
+
+__device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpSmem& S,
+                                                const uint8_t* base, int len, int lane) {
+  if (len <= 0) return;
+  const int mis = (int)(reinterpret_cast<uintptr_t>(base) & 3u);
+  const uint8_t* a0 = base - mis;
+  const int lo = mis, hi = mis + len;
+  const int wpl = (((hi + 3) >> 2) + 31) >> 5;  // words per lane
+  const int cs = lane * wpl * 4, ce = cs + wpl * 4;
+  if (cs >= hi) return;
+  const uint32_t sw = (uint32_t)c.word_salt[0], sc = (uint32_t)c.char_salt[0];
+  uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi)) >> 2 : 0u;
+  uint32_t hw = sw, A = 0, B = 0, carry = 0;
+  uint32_t w = seq_word(a0, cs, lo, hi);
+  for (int r = cs;; r += 4) {
+    const uint32_t nxt = seq_word(a0, r + 4, lo, hi);
+    const uint32_t ns = nonspace_nibble(w);
+    const uint32_t E = (ns << 2) | prev2;  // bit k+2: byte r+k is not a space
+    const uint32_t start = ns & ~(E >> 1);
+    const uint32_t own = (ns + ((r < ce ? start : 0u) | carry)) ^ ns;
+    carry = own >> 4;
+    const uint32_t ev_tri = ns & (E >> 1) & E & own;
+    const uint32_t ev = ev_tri | (~ns & (E >> 1) & own & 0xfu);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t b = (w >> (8 * k)) & 0xffu;
+      const uint32_t hin = ((start >> k) & 1u) ? sw : hw;
+      uint32_t e = (hw ^ 0x1fu) * 0x1b3u;  // the word that ends at this space
+      const uint32_t tri = (B ^ b) * 0x1b3u;
+      B = (A ^ b) * 0x1b3u;
+      A = (sc ^ b) * 0x1b3u;
+      hw = (hin ^ b) * 0x1b3u;
+      if ((ev_tri >> k) & 1u) e = tri;
+      if ((ev >> k) & 1u) emit<false>(S, (e >> 1) & c.mask, (e & 1u) != 0);
+    }
+    prev2 = ns >> 2;
+    if (!carry && (r + 4 >= ce || r + 4 >= hi)) break;
+    w = nxt;
+  }
+}
+
+// Lane l owns buckets [l*dim/32, (l+1)*dim/32): bitmap words [l*nb, (l+1)*nb).
+template <int MODE>
+__global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, const FeatArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  WarpSmem S;
+  S.counts = reinterpret_cast<uint32_t*>(smem + seq_table_bytes(c.dim) * warp);
+  S.bitmap = S.counts + c.dim / 2;
+  S.ring = nullptr;
+  for (uint32_t k = lane; k < c.dim / 2; k += 32) S.counts[k] = kBias2;
+  for (uint32_t k = lane; k < c.dim / 32; k += 32) S.bitmap[k] = 0u;
+  __syncwarp();
+  const uint32_t nb = c.dim >> 10;
+  uint32_t* bm = S.bitmap + lane * nb;
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(S.counts);
+
+  uint32_t* lists = (MODE == kFeatScoreExact) ? a.lists + (size_t)gw * a.list_cap : nullptr;
+  int gn = 0;
+  uint32_t used = 0;
+  int64_t g_prompt = 0;
+  uint32_t g_off = 0, g_cnt = 0;
+  double g_inv = 1.0;
+
+  for (int64_t i = gw; i < a.n; i += nw) {
+    const int64_t beg = a.offsets[i], len = a.offsets[i + 1] - beg;
+    if (((len + 1) / 2) + len > kNarrowMaxFeatures) {  // 16-bit counters could wrap
+      if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
+      continue;
+    }
+    hash_prompt_seq(c, S, a.text + beg, (int)len, lane);
+    __syncwarp();
+    // pass 1: this lane's entry count (CSR: non-zero counts, and sum(count^2))
+    uint32_t mine = 0;
+    long long sq = 0;
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint32_t m = bm[j];
+      if (MODE == kFeatCsr) {
+        for (uint32_t t = m; t; t &= t - 1) {
+          const int cnt = (int)c16[(lane * nb + j) * 32 + __ffs(t) - 1] - 0x8000;
+          mine += cnt != 0;
+          sq += (long long)cnt * cnt;
+        }
+      } else {
+        mine += __popc(m);
+      }
+    }
+    int tot;
+    const uint32_t off = (uint32_t)warp_excl_scan((int)mine, lane, &tot);
+    double inv = 1.0;
+    if (MODE == kFeatCsr) inv = inv_norm(c, warp_sum_i64(sq));
+    uint32_t* L = nullptr;
+    if (MODE == kFeatScoreExact) {
+      const uint32_t need = ((uint32_t)tot + 3u) & ~3u;
+      if (gn == kGroup || used + need > a.list_cap) {
+        chain_group(c, a, lists, true, lane, gn, g_prompt, g_off, g_cnt, g_inv);
+        gn = 0;
+        used = 0;
+      }
+      L = lists + used;
+    }
+    const int64_t slot = (MODE == kFeatCsr) ? a.slot_base[i] : 0;
+    // pass 2: ascending entries (lane-major = bucket order); resets the table
+    uint32_t pos = off;
+    float facc = 0.f;
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint32_t m = bm[j];
+      if (!m) continue;
+      bm[j] = 0u;
+      const uint32_t b0 = (lane * nb + j) * 32;
+      for (uint32_t t = m; t; t &= t - 1) {
+        const uint32_t idx = b0 + __ffs(t) - 1;
+        const int cnt = (int)c16[idx] - 0x8000;
+        c16[idx] = 0x8000;
+        if (MODE == kFeatScoreExact) {
+          L[pos++] = (idx << 16) | (uint32_t)(cnt + 0x8000);
+          sq += (long long)cnt * cnt;
+        } else if (MODE == kFeatScoreFast) {
+          facc += __ldg(a.w32 + idx) * (float)cnt;
+          sq += (long long)cnt * cnt;
+        } else if (cnt != 0) {
+          a.out_idx[slot + pos] = idx;
+          a.out_val[slot + pos] = c.norm ? __dmul_rn((double)cnt, inv) : (double)cnt;
+          if (a.out_cnt) a.out_cnt[slot + pos] = cnt;
+          ++pos;
+        }
+      }
+    }
+    if (MODE == kFeatScoreExact) {
+      inv = inv_norm(c, warp_sum_i64(sq));
+      if (lane == gn) {
+        g_prompt = i;
+        g_off = used;
+        g_cnt = (uint32_t)tot;
+        g_inv = inv;
+      }
+      ++gn;
+      used += ((uint32_t)tot + 3u) & ~3u;
+    } else if (MODE == kFeatScoreFast) {
+      facc = warp_sum_f32(facc);
+      const float finv = (float)inv_norm(c, warp_sum_i64(sq));
+      if (lane == 0) a.scores[i] = (double)(facc * finv) + a.bias;
+    } else if (lane == 0) {
+      a.out_nnz[i] = tot;
+      if (a.out_inv) a.out_inv[i] = inv;
+    }
+    __syncwarp();
+  }
+  if (MODE == kFeatScoreExact && gn > 0)
+    chain_group(c, a, lists, true, lane, gn, g_prompt, g_off, g_cnt, g_inv);
+}
+
 struct Plan {
   bool global_tables;
   int warps;
@@ -638,10 +826,65 @@ int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream
   return PARS_OK;
 }
 
+template <int MODE>
+int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
+  const size_t per = seq_table_bytes(c.dim);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto kern = featurize_seq_kernel<MODE>;
+  int warps = 1, per_sm = 1, best = 0;
+  for (int w : {8, 4, 2, 1}) {
+    const size_t sm_bytes = per * w;
+    if (sm_bytes > kMaxSmemPerBlock) continue;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes) !=
+        cudaSuccess)
+      continue;
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32, sm_bytes);
+    if (b * w > best) {
+      best = b * w;
+      warps = w;
+      per_sm = b;
+    }
+  }
+  cudaGetLastError();
+  if (best == 0) {
+    set_error("featurize: no launchable configuration for dimension %u", c.dim);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  p->global_tables = false;
+  p->warps = warps;
+  p->smem = per * warps;
+  p->grid = std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(std::max<int64_t>(items, 1), warps), (int64_t)sms * per_sm));
+  return PARS_OK;
+}
+
+template <int MODE>
+int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st) {
+  Plan p;
+  PARS_TRY(plan_seq<MODE>(c, a.n, &p));
+  if (MODE == kFeatScoreExact && a.lists_bytes < (size_t)a.list_cap * 4 * (size_t)p.grid * p.warps) {
+    set_error("featurize: list scratch too small");
+    return PARS_ERR_INVALID;
+  }
+  auto kern = featurize_seq_kernel<MODE>;
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  return PARS_OK;
+}
+
 template <bool POW2, bool DEF, int MODE>
 int launch_pair(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st) {
   PARS_CUDA_CHECK(cudaMemsetAsync(a.long_count, 0, sizeof(int32_t), st));
-  PARS_TRY((launch_one<POW2, false, DEF, MODE>(ctx, c, a, st, a.n)));
+  if (POW2 && DEF && use_seq(c)) {
+    PARS_TRY(launch_seq<MODE>(ctx, c, a, st));
+  } else {
+    PARS_TRY((launch_one<POW2, false, DEF, MODE>(ctx, c, a, st, a.n)));
+  }
   return launch_one<POW2, true, DEF, MODE>(ctx, c, a, st, 0);
 }
 
@@ -656,6 +899,12 @@ int scratch_pair(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
     const size_t tw = (size_t)p.grid * p.warps;
     if (p.global_tables) *gs = std::max(*gs, warp_table_bytes(c, wide != 0) * tw);
     if (MODE == kFeatScoreExact) *ls = std::max(*ls, (size_t)list_cap_words(c) * 4 * tw);
+  }
+  if (POW2 && DEF && use_seq(c)) {
+    Plan p;
+    PARS_TRY(plan_seq<MODE>(c, n, &p));
+    if (MODE == kFeatScoreExact)
+      *ls = std::max(*ls, (size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps);
   }
   return PARS_OK;
 }
