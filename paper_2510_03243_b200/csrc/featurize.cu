@@ -594,6 +594,22 @@ __device__ __forceinline__ uint32_t seq_word(const uint8_t* a0, int r, int lo, i
   return w;
 }
 
+// One feature into the per-warp table, branch-free: +-1 into the bucket's
+// biased 16-bit half (idx = (e >> 1) & mask, sign = e & 1, features.cpp:29-34)
+// and its touched bit. Lanes without a feature add 0 and OR 0 (no branch, no
+// predicate); neither op needs the old value, so both are `red` operations.
+__device__ __forceinline__ void seq_emit(uint32_t cbase, uint32_t bbase, uint32_t e, uint32_t m1,
+                                         uint32_t m2, bool p) {
+  const uint32_t caddr = cbase + (e & m1);           // counter word of bucket (e >> 1)
+  const uint32_t sh = (e << 3) & 16u;                // its half
+  const uint32_t d = p ? (((e & 1u) << 1) - 1u) << sh : 0u;  // +-1 in that half
+  const uint32_t baddr = bbase + ((e >> 4) & m2);    // touched-bitmap word
+  const uint32_t bit = p ? 1u << ((e >> 1) & 31u) : 0u;
+  asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.or.b32 [%2], %3;" ::"r"(caddr), "r"(d),
+               "r"(baddr), "r"(bit)
+               : "memory");
+}
+
 __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpSmem& S,
                                                 const uint8_t* base, int len, int lane) {
   if (len <= 0) return;
@@ -604,6 +620,9 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
   const int cs = lane * wpl * 4, ce = cs + wpl * 4;
   if (cs >= hi) return;
   const uint32_t sw = (uint32_t)c.word_salt[0], sc = (uint32_t)c.char_salt[0];
+  const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(S.counts);
+  const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(S.bitmap);
+  const uint32_t m1 = (c.dim / 2 - 1) << 2, m2 = (c.dim / 32 - 1) << 2;
   uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi)) >> 2 : 0u;
   uint32_t hw = sw, A = 0, B = 0, carry = 0;
   uint32_t w = seq_word(a0, cs, lo, hi);
@@ -620,13 +639,12 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
     for (int k = 0; k < 4; ++k) {
       const uint32_t b = (w >> (8 * k)) & 0xffu;
       const uint32_t hin = ((start >> k) & 1u) ? sw : hw;
-      uint32_t e = (hw ^ 0x1fu) * 0x1b3u;  // the word that ends at this space
+      const uint32_t wend = (hw ^ 0x1fu) * 0x1b3u;  // the word that ends at this space
       const uint32_t tri = (B ^ b) * 0x1b3u;
       B = (A ^ b) * 0x1b3u;
       A = (sc ^ b) * 0x1b3u;
       hw = (hin ^ b) * 0x1b3u;
-      if ((ev_tri >> k) & 1u) e = tri;
-      if ((ev >> k) & 1u) emit<false>(S, (e >> 1) & c.mask, (e & 1u) != 0);
+      seq_emit(cbase, bbase, ((ev_tri >> k) & 1u) ? tri : wend, m1, m2, ((ev >> k) & 1u) != 0);
     }
     prev2 = ns >> 2;
     if (!carry && (r + 4 >= ce || r + 4 >= hi)) break;
