@@ -575,8 +575,10 @@ __global__ void __launch_bounds__(256) featurize_kernel(const FeatConfig c, cons
 // per-token divergence beyond a lane's own range.
 constexpr uint32_t kSeqMinDim = 1024, kSeqMaxDim = 16384;
 
+// biased u16 counters + touched bitmap + one dummy word per lane (the target
+// of lanes without a feature)
 __host__ __device__ inline size_t seq_table_bytes(uint32_t dim) {
-  return (size_t)dim * 2 + (size_t)dim / 8;  // biased u16 counters + touched bitmap
+  return (size_t)dim * 2 + (size_t)dim / 8 + 128;
 }
 
 __host__ inline bool use_seq(const FeatConfig& c) {
@@ -596,15 +598,15 @@ __device__ __forceinline__ uint32_t seq_word(const uint8_t* a0, int r, int lo, i
 
 // One feature into the per-warp table, branch-free: +-1 into the bucket's
 // biased 16-bit half (idx = (e >> 1) & mask, sign = e & 1, features.cpp:29-34)
-// and its touched bit. Lanes without a feature add 0 and OR 0 (no branch, no
-// predicate); neither op needs the old value, so both are `red` operations.
-__device__ __forceinline__ void seq_emit(uint32_t cbase, uint32_t bbase, uint32_t e, uint32_t m1,
-                                         uint32_t m2, bool p) {
-  const uint32_t caddr = cbase + (e & m1);           // counter word of bucket (e >> 1)
-  const uint32_t sh = (e << 3) & 16u;                // its half
-  const uint32_t d = p ? (((e & 1u) << 1) - 1u) << sh : 0u;  // +-1 in that half
-  const uint32_t baddr = bbase + ((e >> 4) & m2);    // touched-bitmap word
-  const uint32_t bit = p ? 1u << ((e >> 1) & 31u) : 0u;
+// and its touched bit, both fire-and-forget `red` operations. A lane without
+// a feature targets its own dummy word instead (bank = lane, never read), so
+// it neither branches nor adds bank conflicts.
+__device__ __forceinline__ void seq_emit(uint32_t cbase, uint32_t bbase, uint32_t dummy, uint32_t e,
+                                         uint32_t m1, uint32_t m2, bool p) {
+  const uint32_t caddr = p ? cbase + (e & m1) : dummy;
+  const uint32_t d = ((e & 1u) * 2u - 1u) << ((e << 3) & 16u);  // +-1 in the bucket's half
+  const uint32_t baddr = p ? bbase + ((e >> 4) & m2) : dummy;
+  const uint32_t bit = 1u << ((e >> 1) & 31u);
   asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.or.b32 [%2], %3;" ::"r"(caddr), "r"(d),
                "r"(baddr), "r"(bit)
                : "memory");
@@ -622,6 +624,7 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
   const uint32_t sw = (uint32_t)c.word_salt[0], sc = (uint32_t)c.char_salt[0];
   const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(S.counts);
   const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(S.bitmap);
+  const uint32_t dummy = bbase + (c.dim / 8) + 4u * lane;
   const uint32_t m1 = (c.dim / 2 - 1) << 2, m2 = (c.dim / 32 - 1) << 2;
   uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi)) >> 2 : 0u;
   uint32_t hw = sw, A = 0, B = 0, carry = 0;
@@ -644,7 +647,7 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
       B = (A ^ b) * 0x1b3u;
       A = (sc ^ b) * 0x1b3u;
       hw = (hin ^ b) * 0x1b3u;
-      seq_emit(cbase, bbase, ((ev_tri >> k) & 1u) ? tri : wend, m1, m2, ((ev >> k) & 1u) != 0);
+      seq_emit(cbase, bbase, dummy, ((ev_tri >> k) & 1u) ? tri : wend, m1, m2, ((ev >> k) & 1u) != 0);
     }
     prev2 = ns >> 2;
     if (!carry && (r + 4 >= ce || r + 4 >= hi)) break;
