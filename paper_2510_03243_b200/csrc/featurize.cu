@@ -393,6 +393,10 @@ __device__ void chain_group(const FeatConfig& c, const FeatArgs& a, const uint32
     const double* __restrict__ w = a.w64;
     if (packed) {
       const uint32_t* L = lists + off;
+      // the whole list into L1 first (it was written long enough ago to have
+      // left L1), so the sequential chain below does not wait on L2 per load
+      for (uint32_t q = 0; q < cnt_entries; q += 32)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(L + q));
       uint32_t k = 0;
       for (; k + 4 <= cnt_entries; k += 4) {
         const uint4 e = *reinterpret_cast<const uint4*>(L + k);
@@ -685,6 +689,20 @@ __global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, 
     if (((len + 1) / 2) + len > kNarrowMaxFeatures) {  // 16-bit counters could wrap
       if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
       continue;
+    }
+    {
+      // every 128-byte line of this prompt into L1 at once (lane l: lines l,
+      // l+32, ...), and the warp's next prompt into L2, so the lanes'
+      // sequential word loads do not each expose a miss
+      const uintptr_t l0 = reinterpret_cast<uintptr_t>(a.text + beg) & ~(uintptr_t)127;
+      for (uintptr_t q = l0 + 128u * lane; q < reinterpret_cast<uintptr_t>(a.text + beg + len); q += 4096u)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+      if (i + nw < a.n) {
+        const int64_t nb = a.offsets[i + nw], ne = a.offsets[i + nw + 1];
+        const uintptr_t n0 = reinterpret_cast<uintptr_t>(a.text + nb) & ~(uintptr_t)127;
+        for (uintptr_t q = n0 + 128u * lane; q < reinterpret_cast<uintptr_t>(a.text + ne); q += 4096u)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+      }
     }
     hash_prompt_seq(c, S, a.text + beg, (int)len, lane);
     __syncwarp();
