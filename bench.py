@@ -294,14 +294,21 @@ def run_ours(args):
     alg_bytes = text_bytes + 8 * (n + 1) + 8 * n + 8 * DIM
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (feat_ms / 1e3) / 1e9
-    traffic = None
+    # traffic and pipe utilisation from the committed ncu capture of this
+    # kernel (tools/profile_round.sh -> tools/ncu_to_json.py), scaled to this
+    # launch's prompt count
+    traffic, issue = None, None
     prof = ROOT / "profiles" / "featurize_ncu.json"
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
-            traffic = pj.get("dram_bytes_per_launch_scaled")
+            traffic = pj["dram_bytes_per_prompt"] * n
+            issue = {k: pj[k] for k in ("alu_pipe_pct_active", "fma_pipe_pct_active",
+                                        "lsu_wavefronts_pct", "issue_active_pct",
+                                        "dram_throughput_pct")}
+            issue["source"] = "profiles/featurize_ncu.json (ncu --set full, %d prompts)" % pj["prompts"]
         except Exception:
-            traffic = None
+            traffic, issue = None, None
 
     # e2e through the host-buffer C ABI (H2D text+offsets, D2H scores+order)
     ids_rank = np.arange(b, e, dtype=np.uint32)
@@ -352,9 +359,9 @@ def run_ours(args):
                        "global_batch": N_PROMPTS, "seq_len": PAD_TOKENS,
                        "parallelism": f"shard{world}", "extractor": "hashed word{1}+char{3}, D=4096, L2",
                        "l2_flush": "inputs larger than L2 (%.2f GB text per rank)" % (text_bytes / 1e9)},
-            "roofline": {"bound": "hbm", "kernel": "featurize_kernel (fused tokenise+hash+histogram+L2+dot)",
+            "roofline": {"bound": "hbm", "kernel": "featurize_seq_kernel (fused tokenise+hash+histogram+L2+dot)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_kind": peak_kind, "traffic": traffic,
+                         "peak_kind": peak_kind, "traffic": traffic, "issue_bound_evidence": issue,
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": feat_ms,
                          "sort_ms": sort_ms},
             "cpu_baseline": cpu,

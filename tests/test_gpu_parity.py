@@ -350,3 +350,41 @@ def test_sgd_cluster_long_prompts_use_global_fallback(ctx, oracle):
     ow, oel, oact = oracle.sgd_epoch(rp, idx, val, 4096, a, b, y, 128, 0.1, 1.0, w0)
     assert act == oact and el.hex() == oel.hex()
     assert (w.view(np.uint64) == ow.view(np.uint64)).all()
+
+
+def _random_texts(n, seed):
+    rng = np.random.default_rng(seed)
+    alpha = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz0123456789  \t\n\v\f\r\x80\xc3\xa9\xff\x1f", np.uint8)
+    out = []
+    for k in range(n):
+        L = int(rng.choice([0, 1, 2, 3, 4, 5, 7, 31, 32, 33, 64, 127, 128, 129, 500, 2170, 5000]))
+        t = alpha[rng.integers(0, len(alpha), L)].tobytes()
+        if k % 7 == 0 and L > 10:  # a long token across several lane ranges
+            t = t[:3] + b"q" * (L // 2) + t[3 + L // 2:]
+        out.append(t)
+    return out
+
+
+@pytest.mark.parametrize("dim", [512, 1024, 4096, 16384])
+def test_sequential_lane_kernel_random_texts(ctx, oracle, dim):
+    """Ragged prompts (empty, 1-byte, lane-boundary lengths, every C-locale
+    space, bytes >= 0x80, tokens spanning many lane ranges) at unaligned
+    offsets: exact scores and CSR rows bit-identical, fast mode in tolerance.
+    dim 512 exercises the general kernel, the rest the sequential-lane one."""
+    from paper_2510_03243_b200 import MODE_EXACT, MODE_FAST, pack_texts
+    e = extractor_from(dict(kind=0, dim=dim, norm=1, word=[1], char=[3]))
+    texts = _random_texts(600, dim)
+    arena, offs = pack_texts([b"##"] + texts)
+    offs = offs[1:]
+    w = np.random.default_rng(dim + 1).normal(size=dim)
+    got = ctx.score_text(e, arena, offs, w, -0.25, MODE_EXACT)
+    want = oracle.score_batch(oex(e), arena, offs, w, -0.25)
+    assert (got.view(np.uint64) == want.view(np.uint64)).all()
+    f = ctx.extract(e, arena, offs)
+    rp, idx, val = f.download()
+    orp, oidx, oval = oracle.extract_all(oex(e), arena, offs)
+    assert (rp == orp).all() and (idx == oidx).all() and (val.view(np.uint64) == oval.view(np.uint64)).all()
+    fast = ctx.score_text(e, arena, offs, w, -0.25, MODE_FAST)
+    scale = np.array([np.abs(w[oidx[orp[i]:orp[i + 1]]] * oval[orp[i]:orp[i + 1]]).sum() + 0.25
+                      for i in range(len(texts))])
+    assert (np.abs(fast - want) / scale).max() <= 1e-5
