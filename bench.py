@@ -109,11 +109,20 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PARS_DIST_BACKEND", "nccl") != "nccl":
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PARS_DIST_BACKEND=gloo: exercise the N>1 path with several ranks on
+        # one GPU (NCCL refuses duplicate devices); the timed runs use NCCL
+        backend = os.environ.get("PARS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
