@@ -346,6 +346,9 @@ def run_ours(args):
     pairs = None
     if not args.no_pairs:
         pairs = bench_pairs(P, ctx, torch, dev, stream, world, rank, args)
+    embed = None
+    if world == 1 and not args.no_configs:
+        embed = bench_embeddings(P, ctx, torch, dev, stream, args)
 
     line = None
     if rank == 0:
@@ -380,6 +383,7 @@ def run_ours(args):
             "clocks": clk,
             "parity": {"scores_bitexact_sample": parity_ok, "sample": chk},
             "pairs": pairs,
+            "embeddings": embed,
             "configs": configs,
             "workload_gen_s": t_gen,
         }
@@ -435,6 +439,58 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
             "workload": "C5: all 2,147,450,880 unordered pairs of 65,536 prompts (seed 25), "
                         "Eq.1 mask delta=0.2 + hinge + integer grad coefficients (fp64 scores)",
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident"}
+
+
+def bench_embeddings(P, ctx, torch, dev, stream, args):
+    """PrecomputedEmbedding scoring (features.cpp:67-76 + L2 + dot), exact
+    fp64 mode, device-resident rows: 65,536 prompts x 4,096 dims (2.1 GB,
+    larger than L2). HBM-bound: algorithmic bytes = the rows once + weights +
+    scores; the exact path streams the rows twice (sum of squares first, then
+    the dot, both in index order), so its ceiling is 0.5 of the roofline."""
+    import ctypes as C
+    n, dim = 65536, DIM
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    X = torch.randn(n, dim, dtype=torch.float64, device=dev, generator=g)
+    w = torch.randn(dim, dtype=torch.float64, device=dev, generator=g)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    ex = P.Extractor.make(dim=dim, kind="embedding", norm="l2")
+    L = P.lib()
+    sh = stream.cuda_stream
+
+    def step():
+        rc = L.pars_dev_score_embeddings(ctx.h, C.byref(ex), X.data_ptr(), n, w.data_ptr(), 0.0,
+                                         P.MODE_EXACT, out.data_ptr(), sh)
+        if rc != 0:
+            raise P.ParsError(rc, L.pars_last_error().decode())
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    # parity spot check against the oracle on the first rows (untimed)
+    from oracle.bind import Extractor as OEx
+    from oracle.bind import Oracle
+    chk = 256
+    want = Oracle().score_dense(OEx.make(dim=dim, kind="embedding", norm="l2"),
+                                X[:chk].cpu().numpy(), w.cpu().numpy(), 0.0)
+    ok = bool((out[:chk].cpu().numpy().view(np.uint64) == want.view(np.uint64)).all())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(3, args.steps)
+    a.record(stream)
+    for _ in range(k):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / k
+    alg = n * dim * 8 + dim * 8 + n * 8
+    hbm, _ = peaks()
+    ach = alg / (ms / 1e3) / 1e9
+    return {"metric": "prompts scored/s", "value": n / (ms / 1e3), "unit": "prompts/s",
+            "ms_per_step": ms, "parity_bitexact_sample": ok, "sample": chk,
+            "workload": "PrecomputedEmbedding: 65,536 prompts x 4,096 fp64 dims, L2 norm, exact",
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "algorithmic_bytes_per_launch": alg,
+                         "note": "exact mode reads the rows twice (norm chain, then dot chain)"}}
 
 
 def fnv64(a: np.ndarray) -> str:

@@ -91,6 +91,12 @@ int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex,
 int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex,
                           const double* X, int64_t n, const double* weights,
                           double bias, int mode, double* scores);
+/* Same, device-resident X / weights / scores, asynchronous on `stream`
+ * (NULL: the context's stream). */
+int pars_dev_score_embeddings(pars_ctx* ctx, const pars_extractor* ex,
+                              const double* d_X, int64_t n,
+                              const double* d_weights, double bias, int mode,
+                              double* d_scores, void* stream);
 
 /* ---- features (extract_all, features.cpp:124-150) -------------------- */
 int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text,

@@ -81,6 +81,7 @@ def _load() -> C.CDLL:
         "pars_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
         "pars_dev_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
         "pars_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
+        "pars_dev_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
         "pars_extract": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
         "pars_features_upload": (C.c_int, [vp, u32, i64, vp, vp, vp, vp]),
         "pars_features_rows": (i64, [vp]),

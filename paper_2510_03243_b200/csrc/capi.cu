@@ -500,6 +500,27 @@ int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex, const double*
   return PARS_OK;
 }
 
+int pars_dev_score_embeddings(pars_ctx* ctx, const pars_extractor* ex, const double* d_X, int64_t n,
+                              const double* d_weights, double bias, int mode, double* d_scores,
+                              void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  const float* w32 = nullptr;
+  if (mode == PARS_MODE_FAST_F32) {
+    PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
+    f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(d_weights, (float*)ctx->w32.p,
+                                                                         cfg.dim);
+    count_launch(ctx);
+    w32 = (const float*)ctx->w32.p;
+  }
+  return launch_score_dense(ctx, cfg, mode, d_X, n, d_weights, w32, bias, d_scores, st);
+}
+
 // ---- features ------------------------------------------------------------
 
 // extract_all (features.cpp:124-141) into a device-resident CSR.

@@ -29,6 +29,7 @@
 //     bit-exact chains proceed in parallel instead of one lane at a time.
 //     Fast fp32 mode reduces lane-parallel products with a warp tree; CSR
 //     mode compacts (idx, value) rows.
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -967,11 +968,139 @@ int scratch_mode(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
 }
 
 // ---- dense embeddings (features.cpp:67-76) -----------------------------
-// Exact: one thread per prompt keeps the reference's two sequential chains
-// (sum of squares in index order, then the dot in index order).
-__global__ void dense_exact_kernel(const double* __restrict__ X, int64_t n, uint32_t dim,
-                                   int norm, const double* __restrict__ w, double bias,
-                                   double* __restrict__ out) {
+// Exact: the reference's two sequential chains per prompt — sum of squares in
+// index order (features.cpp:113-116), then the dot in index order
+// (features.hpp:31-35) — one thread per prompt, the rows reaching it through
+// shared memory by TMA bulk copies (cp.async.bulk, one 256-byte row segment
+// per copy, completion on an mbarrier). A persistent CTA walks blocks of 128
+// prompts; its job stream is (block, pass, 32-column tile) and warp 0 keeps
+// kDenseStages tiles in flight ahead of the chains, across pass and block
+// boundaries. Rows land with a 272-byte pitch so each quarter-warp's 16-byte
+// loads hit distinct banks. With L2 normalisation every row is streamed
+// twice (the dot needs the norm first). Requires 16-byte aligned rows (even
+// dim, aligned base); otherwise dense_exact_simple_kernel runs.
+constexpr int kDenseRows = 64, kDenseCols = 64, kDenseStages = 3;
+constexpr int kDensePitch = kDenseCols * 8 + 16;  // bytes per row in a stage
+constexpr size_t kDenseStageBytes = (size_t)kDenseRows * kDensePitch;
+constexpr size_t kDenseSmem = kDenseStages * kDenseStageBytes + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kDenseRows) dense_exact_kernel(
+    const double* __restrict__ X, int64_t n, uint32_t dim, int norm, const double* __restrict__ w,
+    double bias, double* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kDenseStages * kDenseStageBytes);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t ntiles = (dim + kDenseCols - 1) / kDenseCols;
+  const int npass = norm ? 2 : 1;
+  const int64_t nblocks = (n + kDenseRows - 1) / kDenseRows;
+  const int64_t my_blocks = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t njobs = my_blocks * npass * ntiles;
+  if (t == 0) {
+    for (int st = 0; st < kDenseStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + st)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // job j -> (block, tile); warp 0 copies it into stage j % kDenseStages
+  auto issue = [&](int64_t j) {
+    const int64_t b = blockIdx.x + (j / (npass * ntiles)) * (int64_t)gridDim.x;
+    const uint32_t kt = (uint32_t)(j % ntiles);
+    const int64_t r0 = b * kDenseRows;
+    const int rows = (int)imin64(kDenseRows, n - r0);
+    const uint32_t k0 = kt * kDenseCols;
+    const uint32_t seg = min((uint32_t)kDenseCols, dim - k0) * 8u;
+    const int st = (int)(j % kDenseStages);
+    const uint32_t bar = smem_u32(full + st);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(seg * (uint32_t)rows)
+                   : "memory");
+    __syncwarp();
+    unsigned char* stage = dsm + st * kDenseStageBytes;
+    for (int r = lane; r < rows; r += 32)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(stage + r * kDensePitch)),
+          "l"(X + (r0 + r) * (int64_t)dim + k0), "r"(seg), "r"(bar)
+          : "memory");
+  };
+  if (warp == 0)
+    for (int64_t j = 0; j < imin64(njobs, kDenseStages); ++j) issue(j);
+  double acc = 0.0, inv = 1.0;
+  bool scale = false;
+  int64_t j = 0;
+  for (int64_t bi = 0; bi < my_blocks; ++bi) {
+    const int64_t r0 = (blockIdx.x + bi * (int64_t)gridDim.x) * kDenseRows;
+    inv = 1.0;
+    scale = false;
+    for (int pass = 2 - npass; pass < 2; ++pass) {
+      acc = 0.0;
+      for (uint32_t kt = 0; kt < ntiles; ++kt, ++j) {
+        const int st = (int)(j % kDenseStages);
+        mbar_wait(smem_u32(full + st), (uint32_t)((j / kDenseStages) & 1));
+        const double* row = reinterpret_cast<const double*>(dsm + st * kDenseStageBytes + t * kDensePitch);
+        const uint32_t k0 = kt * kDenseCols;
+        if (k0 + kDenseCols <= dim) {
+          if (pass == 0) {
+#pragma unroll
+            for (int k = 0; k < kDenseCols; k += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(row + k);
+              acc = __dadd_rn(acc, __dmul_rn(v.x, v.x));
+              acc = __dadd_rn(acc, __dmul_rn(v.y, v.y));
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kDenseCols; k += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(row + k);
+              const double2 wk = __ldg(reinterpret_cast<const double2*>(w + k0 + k));
+              const double a = scale ? __dmul_rn(v.x, inv) : v.x;
+              const double b = scale ? __dmul_rn(v.y, inv) : v.y;
+              acc = __dadd_rn(acc, __dmul_rn(wk.x, a));
+              acc = __dadd_rn(acc, __dmul_rn(wk.y, b));
+            }
+          }
+        } else {
+          for (uint32_t k = 0; k < dim - k0; ++k) {
+            const double x = row[k];
+            if (pass == 0) {
+              acc = __dadd_rn(acc, __dmul_rn(x, x));
+            } else {
+              const double v = scale ? __dmul_rn(x, inv) : x;
+              acc = __dadd_rn(acc, __dmul_rn(__ldg(w + k0 + k), v));
+            }
+          }
+        }
+        __syncthreads();  // every chain is done with stage st
+        if (warp == 0 && j + kDenseStages < njobs) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(j + kDenseStages);
+        }
+      }
+      if (pass == 0 && acc > 0.0) {
+        inv = __ddiv_rn(1.0, __dsqrt_rn(acc));
+        scale = true;
+      }
+    }
+    if (r0 + t < n) out[r0 + t] = __dadd_rn(acc, bias);
+  }
+}
+
+// Rows that are not 16-byte aligned (odd dim or unaligned base): the same
+// two chains straight from global memory, one thread per prompt.
+__global__ void dense_exact_simple_kernel(const double* __restrict__ X, int64_t n, uint32_t dim,
+                                          int norm, const double* __restrict__ w, double bias,
+                                          double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double* x = X + i * (int64_t)dim;
@@ -979,10 +1108,7 @@ __global__ void dense_exact_kernel(const double* __restrict__ X, int64_t n, uint
   bool scale = false;
   if (norm) {
     double sq = 0.0;
-    for (uint32_t k = 0; k < dim; ++k) {
-      double v = x[k];
-      sq = __dadd_rn(sq, __dmul_rn(v, v));
-    }
+    for (uint32_t k = 0; k < dim; ++k) sq = __dadd_rn(sq, __dmul_rn(x[k], x[k]));
     if (sq > 0.0) {
       inv = __ddiv_rn(1.0, __dsqrt_rn(sq));
       scale = true;
@@ -990,7 +1116,7 @@ __global__ void dense_exact_kernel(const double* __restrict__ X, int64_t n, uint
   }
   double s = 0.0;
   for (uint32_t k = 0; k < dim; ++k) {
-    double v = scale ? __dmul_rn(x[k], inv) : x[k];
+    const double v = scale ? __dmul_rn(x[k], inv) : x[k];
     s = __dadd_rn(s, __dmul_rn(w[k], v));
   }
   out[i] = __dadd_rn(s, bias);
@@ -1097,8 +1223,24 @@ int launch_score_dense(pars_ctx* ctx, const FeatConfig& c, int mode, const doubl
                        cudaStream_t st) {
   if (n == 0) return PARS_OK;
   if (mode == PARS_MODE_EXACT_F64) {
-    dense_exact_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(X, n, c.dim, c.norm, w64, bias,
-                                                                   scores);
+    const bool aligned = (c.dim % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(w64) % 16 == 0);
+    if (!aligned) {
+      dense_exact_simple_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(X, n, c.dim, c.norm, w64,
+                                                                           bias, scores);
+    } else {
+      PARS_CUDA_CHECK(cudaFuncSetAttribute(dense_exact_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem));
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_exact_kernel, kDenseRows, kDenseSmem);
+      const int64_t blocks = ceil_div(n, kDenseRows);
+      const int64_t grid =
+          std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sms * std::max(per_sm, 1)));
+      dense_exact_kernel<<<(unsigned)grid, kDenseRows, kDenseSmem, st>>>(X, n, c.dim, c.norm, w64,
+                                                                       bias, scores);
+    }
   } else {
     dense_fast_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, st>>>(X, n, c.dim, c.norm, w32,
                                                                        bias, scores);

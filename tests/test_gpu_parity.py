@@ -266,19 +266,24 @@ def test_c2_epoch_bit_identical(ctx):
     assert fnv64_array(w) == m["c2"]["weights_fnv"] == "f97c96a353829ee2"
 
 
-def test_embedding_scores_exact(ctx, oracle):
+@pytest.mark.parametrize("n,dim", [(300, 64), (1000, 100), (129, 7), (1, 4096)])
+def test_embedding_scores_exact(ctx, oracle, n, dim):
+    """Tiled dense kernel: row tails (n % 128), column tails (dim % 16)."""
     from paper_2510_03243_b200 import MODE_EXACT, MODE_FAST, Extractor
     rng = np.random.default_rng(4)
     for norm in ("l2", "none"):
-        e = Extractor.make(dim=64, kind="embedding", norm=norm)
-        X = rng.normal(size=(300, 64))
+        e = Extractor.make(dim=dim, kind="embedding", norm=norm)
+        X = rng.normal(size=(n, dim))
         X[0] = 0.0
-        w = rng.normal(size=64)
+        w = rng.normal(size=dim)
         got = ctx.score_embeddings(e, X, w, 0.25, MODE_EXACT)
         want = oracle.score_dense(oex(e), X, w, 0.25)
         assert [x.hex() for x in got] == [x.hex() for x in want]
         fast = ctx.score_embeddings(e, X, w, 0.25, MODE_FAST)
-        assert np.allclose(fast, want, rtol=0, atol=1e-4)
+        nrm = np.sqrt((X * X).sum(1, keepdims=True)) if norm == "l2" else 1.0
+        V = X / np.where(nrm > 0, nrm, 1.0)
+        scale = np.abs(V * w).sum(1) + 0.25  # sum |w_i v_i| + |bias|
+        assert (np.abs(fast - want) / scale).max() <= 1e-5
 
 
 def test_features_score_matches_linear_scorer(ctx, oracle):
