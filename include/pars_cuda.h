@@ -87,6 +87,16 @@ int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex,
                         const char* d_text, const int64_t* d_offsets,
                         int64_t n, const double* d_weights, double bias,
                         int mode, double* d_scores, void* stream);
+/* enqueue + select_batch in one call (scheduler.cpp:17-31 scores every
+ * waiting request, scheduler.cpp:33-60 orders them): score the prompts and
+ * return both the scores and the full priority order (order[k] = index of
+ * the k-th request to admit; truncate to the free slots). The scores stay on
+ * the device between the two steps; one synchronisation. boosted may be
+ * NULL. tie_rank as for pars_priority_order. */
+int pars_score_order(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                     const int64_t* offsets, int64_t n, const double* weights,
+                     double bias, int mode, const uint32_t* tie_rank,
+                     const uint8_t* boosted, double* scores, int64_t* order);
 /* PrecomputedEmbedding branch (features.cpp:67-76): X is n x dim row-major. */
 int pars_score_embeddings(pars_ctx* ctx, const pars_extractor* ex,
                           const double* X, int64_t n, const double* weights,

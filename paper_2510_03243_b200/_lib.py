@@ -107,6 +107,7 @@ def _load() -> C.CDLL:
         "pars_train_pairwise": (C.c_int, [vp, vp, vp, vp, vp, i64, dbl, dbl, i32, i32, dbl, u64,
                                           u64, vp, vp, vp]),
         "pars_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+        "pars_score_order": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp, vp, vp]),
         "pars_dev_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
         "pars_tie_ranks": (C.c_int, [vp, vp, vp, i64, vp]),
         "pars_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp]),
@@ -366,6 +367,20 @@ class Context:
         _check(lib().pars_score_text(self.h, C.byref(ex), _p(t), _p(offs), n,
                                      _p(_c(weights, np.float64)), bias, mode, _p(out)))
         return out
+
+    def score_order(self, ex: Extractor, text: np.ndarray, offsets: np.ndarray, weights,
+                    tie_rank, boosted=None, bias: float = 0.0, mode: int = MODE_EXACT):
+        """enqueue + select_batch in one call: (scores, full admission order)."""
+        offs = _c(offsets, np.int64)
+        n = len(offs) - 1
+        scores = np.zeros(max(n, 0), np.float64)
+        order = np.zeros(max(n, 0), np.int64)
+        t = text if isinstance(text, np.ndarray) else np.frombuffer(bytes(text), np.uint8)
+        bst = None if boosted is None else _c(boosted, np.uint8)
+        _check(lib().pars_score_order(self.h, C.byref(ex), _p(t), _p(offs), n,
+                                      _p(_c(weights, np.float64)), bias, mode,
+                                      _p(_c(tie_rank, np.uint32)), _p(bst), _p(scores), _p(order)))
+        return scores, order
 
     def score_texts(self, ex: Extractor, texts: Sequence[bytes], weights, bias=0.0,
                     mode=MODE_EXACT) -> np.ndarray:

@@ -370,26 +370,16 @@ void pars_host_free(void* p) {
 // Scorer::score_batch fused with extract_features (scorer.cpp:9-24,
 // features.cpp:62-122). Host buffers; the text is streamed to the device in
 // chunks on a copy stream, overlapped with the kernel of the previous chunk.
-int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
-                    const int64_t* offsets, int64_t n, const double* weights, double bias, int mode,
-                    double* scores) {
-  PARS_TRY(check_ctx(ctx));
-  PARS_TRY(check_mode(mode));
-  FeatConfig cfg;
-  if (!build_feat_config(ex, &cfg)) return PARS_ERR_INVALID;
-  if (ex->kind != 0) {
-    set_error("pars_score_text: extractor kind is precomputed_embedding; use pars_score_embeddings");
-    return PARS_ERR_INVALID;
-  }
-  if (n < 0) {
-    set_error("negative prompt count");
-    return PARS_ERR_INVALID;
-  }
-  if (n == 0) return PARS_OK;
-  Guard g(ctx);
+namespace {
+// The chunked host-buffer scoring pipeline behind pars_score_text and
+// pars_score_order: text and offsets stream to the device in ~64 MB chunks on
+// the copy stream, overlapped with the previous chunk's kernel; scores go
+// either to pinned host staging (h_out) or stay on the device (d_out).
+int score_text_pipeline(pars_ctx* ctx, const FeatConfig& cfg, const char* text,
+                        const int64_t* offsets, int64_t n, const double* weights, double bias,
+                        int mode, double* d_out, double* h_out) {
   cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
   PARS_TRY(upload_weights(ctx, cfg, weights, mode, st));
-  // chunk by text bytes (~64 MB) and prompt count
   const int64_t kChunkBytes = 64ll << 20, kChunkPrompts = 1 << 18;
   std::vector<int64_t> starts;
   for (int64_t i = 0; i < n;) {
@@ -400,7 +390,6 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   }
   starts.push_back(n);
   const int nchunks = (int)starts.size() - 1;
-  // worst-case buffers
   int64_t max_bytes = 0, max_n = 0;
   for (int k = 0; k < nchunks; ++k) {
     max_bytes = std::max(max_bytes, offsets[starts[k + 1]] - offsets[starts[k]]);
@@ -409,17 +398,11 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   for (int b = 0; b < 2; ++b) {
     PARS_TRY(ensure(ctx->text[b], (size_t)max_bytes + 16));
     PARS_TRY(ensure(ctx->offs[b], (size_t)(max_n + 1) * 8));
-    PARS_TRY(ensure(ctx->scores[b], (size_t)max_n * 8));
+    if (!d_out) PARS_TRY(ensure(ctx->scores[b], (size_t)max_n * 8));
+    PARS_TRY(ensure_host(ctx->h_offs[b], (size_t)(max_n + 1) * 8));
   }
-  // Every copy stays asynchronous: offsets go through pinned staging, scores
-  // land in pinned staging and are handed over once at the end, so the host
-  // never blocks inside the loop and chunk k+1's upload (copy stream)
-  // overlaps chunk k's kernel (compute stream). Text that is not pinned is
-  // copied as given (the driver stages it).
-  for (int b = 0; b < 2; ++b) PARS_TRY(ensure_host(ctx->h_offs[b], (size_t)(max_n + 1) * 8));
-  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
-  double* h_sc = static_cast<double*>(ctx->h_scores.p);
-  // the weights upload (on st) must land before any kernel: already ordered on st
+  // Every copy stays asynchronous (offsets through pinned staging, scores into
+  // pinned staging or device memory), so the host never blocks inside the loop.
   for (int k = 0; k < nchunks; ++k) {
     const int b = k & 1;
     const int64_t i0 = starts[k], i1 = starts[k + 1], m = i1 - i0;
@@ -436,14 +419,86 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
     PARS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copy[b], 0));
     // offsets are absolute: shift the device text base so text[offsets[i]] is valid
     const uint8_t* base = static_cast<const uint8_t*>(ctx->text[b].p) - t0;
-    PARS_TRY(score_chunk(ctx, cfg, mode, base, (const int64_t*)ctx->offs[b].p, m, bias,
-                         (double*)ctx->scores[b].p, st));
-    PARS_CUDA_CHECK(cudaMemcpyAsync(h_sc + i0, ctx->scores[b].p, (size_t)m * 8,
-                                    cudaMemcpyDeviceToHost, st));
+    double* dst = d_out ? d_out + i0 : (double*)ctx->scores[b].p;
+    PARS_TRY(score_chunk(ctx, cfg, mode, base, (const int64_t*)ctx->offs[b].p, m, bias, dst, st));
+    if (!d_out)
+      PARS_CUDA_CHECK(cudaMemcpyAsync(h_out + i0, dst, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
     PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_done[b], st));
   }
+  return PARS_OK;
+}
+
+int check_text_call(const pars_extractor* ex, int64_t n, FeatConfig* cfg, const char* fn) {
+  if (!build_feat_config(ex, cfg)) return PARS_ERR_INVALID;
+  if (ex->kind != 0) {
+    set_error("%s: extractor kind is precomputed_embedding; use pars_score_embeddings", fn);
+    return PARS_ERR_INVALID;
+  }
+  if (n < 0) {
+    set_error("negative prompt count");
+    return PARS_ERR_INVALID;
+  }
+  return PARS_OK;
+}
+}  // namespace
+
+// Scorer::score_batch fused with extract_features (scorer.cpp:9-24,
+// features.cpp:62-122). Host buffers.
+int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                    const int64_t* offsets, int64_t n, const double* weights, double bias, int mode,
+                    double* scores) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  PARS_TRY(check_text_call(ex, n, &cfg, "pars_score_text"));
+  if (n == 0) return PARS_OK;
+  Guard g(ctx);
+  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
+  double* h_sc = static_cast<double*>(ctx->h_scores.p);
+  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, nullptr, h_sc));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(scores, h_sc, (size_t)n * 8);
+  return PARS_OK;
+}
+
+// enqueue (scheduler.cpp:17-31: score every waiting request) + select_batch
+// (scheduler.cpp:33-60: full priority order) in one call: the scores never
+// leave the device between the two, and both results come back with one
+// synchronisation. Host buffers; boosted may be NULL.
+int pars_score_order(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                     const int64_t* offsets, int64_t n, const double* weights, double bias,
+                     int mode, const uint32_t* tie_rank, const uint8_t* boosted, double* scores,
+                     int64_t* order) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  PARS_TRY(check_text_call(ex, n, &cfg, "pars_score_order"));
+  if (n == 0) return PARS_OK;
+  if (n > 0x7fffffffLL) {
+    set_error("priority order: n=%lld exceeds 2^31-1", (long long)n);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  // device layout: scores[n] | tie[n] | order[n] | boosted[n]
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * (8 + 4 + 4 + 1) + 64));
+  double* d_s = (double*)ctx->pairs_in.p;
+  uint32_t* d_t = (uint32_t*)(d_s + n);
+  uint32_t* d_o = d_t + n;
+  uint8_t* d_b = (uint8_t*)(d_o + n);
+  PARS_TRY(ensure(ctx->sort, sort_scratch_bytes(n) + 4096));
+  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 16));
+  double* h_sc = static_cast<double*>(ctx->h_scores.p);
+  uint32_t* h_o = reinterpret_cast<uint32_t*>(h_sc + n);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, tie_rank, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+  if (boosted) PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, boosted, (size_t)n, cudaMemcpyHostToDevice, st));
+  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, d_s, nullptr));
+  PARS_TRY(launch_priority_sort(ctx, d_s, boosted ? d_b : nullptr, d_t, n, d_o, ctx->sort.p, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(h_sc, d_s, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(h_o, d_o, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
   std::memcpy(scores, h_sc, (size_t)n * 8);
+  for (int64_t i = 0; i < n; ++i) order[i] = h_o[i];
   return PARS_OK;
 }
 

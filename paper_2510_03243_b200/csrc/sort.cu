@@ -168,6 +168,50 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
   }
 }
 
+// Small queues (n <= kSmallSort): one CTA, one launch, no host round trip.
+// The key (ordered score bits or 0 if boosted, tie rank, input index) is
+// unique, so ANY correct sort of it yields the stable order the radix path
+// produces; a shared-memory bitonic network sorts it (padding keys are all
+// ones and sink to the end).
+constexpr int kSmallSort = 4096, kSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallThreads) small_sort_kernel(
+    const double* __restrict__ score, const uint8_t* __restrict__ boosted,
+    const uint32_t* __restrict__ tie, int n, int n2, uint32_t* __restrict__ order) {
+  extern __shared__ uint64_t ks[];  // hi[n2], lo[n2] (lo = tie << 32 | index)
+  uint64_t* hi = ks;
+  uint64_t* lo = ks + n2;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < n) {
+      hi[i] = (boosted && boosted[i]) ? 0ull : ordered_bits(score[i]);
+      lo[i] = ((uint64_t)tie[i] << 32) | (uint32_t)i;
+    } else {
+      hi[i] = ~0ull;
+      lo[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (j - 1));  // lower index of the pair (bit j clear)
+        const int p = i + j;
+        const bool up = (i & k) == 0;
+        const uint64_t ah = hi[i], al = lo[i], bh = hi[p], bl = lo[p];
+        const bool gt = ah > bh || (ah == bh && al > bl);
+        if (gt == up) {
+          hi[i] = bh;
+          lo[i] = bl;
+          hi[p] = ah;
+          lo[p] = al;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)lo[i];
+}
+
 }  // namespace
 
 size_t sort_scratch_bytes(int64_t n) {
@@ -185,6 +229,18 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   if (n > 0x7fffffffLL) {
     set_error("priority order: n=%lld exceeds 2^31-1", (long long)n);
     return PARS_ERR_UNSUPPORTED;
+  }
+  if (n <= kSmallSort) {
+    int n2 = 2;
+    while (n2 < n) n2 <<= 1;
+    const size_t sm = (size_t)n2 * 16;
+    PARS_CUDA_CHECK(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm));
+    small_sort_kernel<<<1, std::min(kSmallThreads, std::max(32, n2 / 2)), sm, st>>>(score, boosted, tie,
+                                                                                  (int)n, n2, order);
+    count_launch(ctx);
+    PARS_CUDA_CHECK(cudaGetLastError());
+    return PARS_OK;
   }
   const int nb = (int)ceil_div(n, kTileKeys);
   char* p = static_cast<char*>(scratch);

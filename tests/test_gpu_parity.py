@@ -393,3 +393,35 @@ def test_sequential_lane_kernel_random_texts(ctx, oracle, dim):
     scale = np.array([np.abs(w[oidx[orp[i]:orp[i + 1]]] * oval[orp[i]:orp[i + 1]]).sum() + 0.25
                       for i in range(len(texts))])
     assert (np.abs(fast - want) / scale).max() <= 1e-5
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 1000, 1024, 4095, 4096, 4097, 9000])
+def test_priority_order_sizes(ctx, oracle, n):
+    """The single-CTA bitonic path (n <= 4096) and the radix path on either
+    side of the switch: ties in score and (arrival, id), -0.0 vs +0.0, boosts."""
+    from paper_2510_03243_b200 import tie_ranks
+    rng = np.random.default_rng(n)
+    score = rng.choice(np.concatenate([rng.normal(size=7), [0.0, -0.0]]), size=n)
+    arrival = rng.choice(np.arange(5) * 0.5, size=n)
+    ids = ["r%d" % rng.integers(0, 9) for _ in range(n)]
+    boosted = (rng.random(n) < 0.1).astype(np.uint8)
+    got = ctx.priority_order(score, tie_ranks(arrival, ids), boosted)
+    want = oracle.select_order(arrival, ids, score, boosted, 1e9)
+    assert (got == want).all()
+
+
+def test_score_order_fused_matches_two_calls_and_oracle(ctx, oracle):
+    """pars_score_order == pars_score_text + pars_priority_order == the
+    reference's score_batch + select_batch (C1-shaped: 1,024 prompts)."""
+    from paper_2510_03243_b200 import Extractor, Workload, tie_ranks
+    wl = Workload.synthesize(1024, 22)
+    w = golden("readme_model.npz")["weights"]
+    ids = ["p%06d" % i for i in range(len(wl))]
+    arrival = np.zeros(len(wl))
+    tie = tie_ranks(arrival, ids)
+    boosted = (np.arange(len(wl)) % 97 == 0).astype(np.uint8)
+    s, order = ctx.score_order(Extractor.make(), wl.text, wl.offsets, w, tie, boosted)
+    s2 = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w)
+    assert (s.view(np.uint64) == s2.view(np.uint64)).all()
+    assert (order == ctx.priority_order(s2, tie, boosted)).all()
+    assert (order == oracle.select_order(arrival, ids, s2, boosted, 0.0)).all()
