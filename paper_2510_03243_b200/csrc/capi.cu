@@ -68,6 +68,7 @@ struct pars_ctx {
 
 struct pars_features {
   pars_ctx* ctx = nullptr;
+  int device = 0;
   uint32_t dim = 0;
   int64_t rows = 0, nnz = 0;
   int64_t* d_rp = nullptr;
@@ -126,6 +127,32 @@ int ensure_host(HostBuf& b, size_t bytes) {
   }
   b.cap = want;
   return PARS_OK;
+}
+
+// Per-object device memory (features, pair plans) comes from the device's
+// stream-ordered pool on the context stream: after warm-up an allocation or
+// release costs a few microseconds instead of cudaMalloc/cudaFree's
+// milliseconds (cudaFree synchronises the device and unmaps).
+bool pool_alloc(pars_ctx* ctx, void** p, size_t bytes) {
+  if (cudaMallocAsync(p, std::max<size_t>(bytes, 16), ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return false;
+  }
+  return true;
+}
+void pool_free(pars_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+// Releasing an object may happen after its context is gone (language
+// bindings free in any order): wait for the device, then return the blocks
+// to the pool through the legacy stream. No context dereference.
+void pool_release(int device, void* const* ptrs, int k) {
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < k; ++i)
+    if (ptrs[i]) cudaFreeAsync(ptrs[i], 0);
+  cudaGetLastError();
 }
 
 struct Guard {
@@ -319,6 +346,15 @@ int pars_ctx_create(int device, pars_ctx** out) {
   c->device = device;
   PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  {
+    // keep released pool memory cached (features / plans are re-created per call)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   for (int k = 0; k < 2; ++k) {
     PARS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_copy[k], cudaEventDisableTiming));
     PARS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
@@ -593,6 +629,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   cudaStream_t st = ctx->stream;
   auto* f = new pars_features();
   f->ctx = ctx;
+  f->device = ctx->device;
   f->dim = cfg.dim;
   f->rows = n;
   f->h_rp.assign((size_t)n + 1, 0);
@@ -608,9 +645,9 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
     const int64_t nnz = n * (int64_t)cfg.dim;
     for (int64_t i = 0; i <= n; ++i) f->h_rp[i] = i * (int64_t)cfg.dim;
     f->nnz = nnz;
-    if (cudaMalloc(&f->d_rp, (size_t)(n + 1) * 8) != cudaSuccess ||
-        cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(nnz, 1) * 4) != cudaSuccess ||
-        cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(nnz, 1) * 8) != cudaSuccess) {
+    if (!pool_alloc(ctx, (void**)&f->d_rp, (size_t)(n + 1) * 8) ||
+        !pool_alloc(ctx, (void**)&f->d_idx, (size_t)std::max<int64_t>(nnz, 1) * 4) ||
+        !pool_alloc(ctx, (void**)&f->d_val, (size_t)std::max<int64_t>(nnz, 1) * 8)) {
       cudaGetLastError();
       set_error("device allocation failed (extract, embeddings)");
       return fail_free(PARS_ERR_OOM);
@@ -649,7 +686,7 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
   double* s_val = (double*)(((uintptr_t)(s_idx + cap_total) + 15) & ~(uintptr_t)15);
   int32_t* s_cnt = (int32_t*)(s_val + cap_total);
   int32_t* d_nnz = (int32_t*)ctx->scores[0].p;
-  if (cudaMalloc(&f->d_inv, (size_t)std::max<int64_t>(n, 1) * 8) != cudaSuccess) {
+  if (!pool_alloc(ctx, (void**)&f->d_inv, (size_t)std::max<int64_t>(n, 1) * 8)) {
     cudaGetLastError();
     set_error("device allocation failed (extract)");
     return fail_free(PARS_ERR_OOM);
@@ -681,10 +718,10 @@ int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text, cons
     for (int64_t i = 0; i < n; ++i) f->h_rp[i + 1] = f->h_rp[i] + nnz[i];
   }
   f->nnz = f->h_rp[n];
-  if (cudaMalloc(&f->d_rp, (size_t)(n + 1) * 8) != cudaSuccess ||
-      cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess ||
-      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess ||
-      cudaMalloc(&f->d_cnt, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess) {
+  if (!pool_alloc(ctx, (void**)&f->d_rp, (size_t)(n + 1) * 8) ||
+      !pool_alloc(ctx, (void**)&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) ||
+      !pool_alloc(ctx, (void**)&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) ||
+      !pool_alloc(ctx, (void**)&f->d_cnt, (size_t)std::max<int64_t>(f->nnz, 1) * 4)) {
     cudaGetLastError();
     set_error("device allocation failed (extract)");
     return fail_free(PARS_ERR_OOM);
@@ -710,6 +747,7 @@ int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows, const int64_
   Guard g(ctx);
   auto* f = new pars_features();
   f->ctx = ctx;
+  f->device = ctx->device;
   f->dim = dim;
   f->rows = rows;
   f->h_rp.assign(row_ptr, row_ptr + rows + 1);
@@ -722,9 +760,9 @@ int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows, const int64_
       delete f;
       return PARS_ERR_INVALID;
     }
-  if (cudaMalloc(&f->d_rp, (size_t)(rows + 1) * 8) != cudaSuccess ||
-      cudaMalloc(&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) != cudaSuccess ||
-      cudaMalloc(&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8) != cudaSuccess) {
+  if (!pool_alloc(ctx, (void**)&f->d_rp, (size_t)(rows + 1) * 8) ||
+      !pool_alloc(ctx, (void**)&f->d_idx, (size_t)std::max<int64_t>(f->nnz, 1) * 4) ||
+      !pool_alloc(ctx, (void**)&f->d_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8)) {
     cudaGetLastError();
     set_error("device allocation failed (features upload)");
     delete f;
@@ -756,10 +794,8 @@ int pars_features_download(pars_ctx* ctx, const pars_features* f, int64_t* row_p
 
 void pars_features_free(pars_features* f) {
   if (!f) return;
-  cudaSetDevice(f->ctx->device);
   void* ptrs[] = {f->d_rp, f->d_idx, f->d_val, f->d_cnt, f->d_inv, f->d_cpk, f->d_cpk_off};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  pool_release(f->device, ptrs, 7);
   delete f;
 }
 
@@ -885,6 +921,7 @@ int pars_dev_allpairs(pars_ctx* ctx, const double* d_scores, const int32_t* d_le
 
 struct pars_pair_plan {
   pars_ctx* ctx = nullptr;
+  int device = 0;
   PairPlanDev dev;
   void* scratch = nullptr;
   int32_t* d_L = nullptr;     // lengths in input order (general-kernel fallback)
@@ -922,18 +959,19 @@ int pars_pair_plan_create(pars_ctx* ctx, const int64_t* lengths, int64_t n, doub
   cudaStream_t st = ctx->stream;
   auto* p = new pars_pair_plan();
   p->ctx = ctx;
+  p->device = ctx->device;
   p->max_len = max_len;
   p->delta = delta;
   auto fail = [&](int rc) {
-    if (p->scratch) cudaFree(p->scratch);
-    if (p->d_L) cudaFree(p->d_L);
-    if (p->d_dmin) cudaFree(p->d_dmin);
+    pool_free(ctx, p->scratch);
+    pool_free(ctx, p->d_L);
+    pool_free(ctx, p->d_dmin);
     delete p;
     return rc;
   };
-  if (cudaMalloc(&p->scratch, pair_plan_scratch_bytes(n)) != cudaSuccess ||
-      cudaMalloc(&p->d_L, L.size() * 4) != cudaSuccess ||
-      cudaMalloc(&p->d_dmin, table.size() * 4) != cudaSuccess) {
+  if (!pool_alloc(ctx, (void**)&p->scratch, pair_plan_scratch_bytes(n)) ||
+      !pool_alloc(ctx, (void**)&p->d_L, L.size() * 4) ||
+      !pool_alloc(ctx, (void**)&p->d_dmin, table.size() * 4)) {
     cudaGetLastError();
     set_error("device allocation failed (pair plan)");
     return fail(PARS_ERR_OOM);
@@ -955,10 +993,8 @@ int pars_pair_plan_sorted(const pars_pair_plan* p) { return p && p->dev.monotone
 
 void pars_pair_plan_free(pars_pair_plan* p) {
   if (!p) return;
-  cudaSetDevice(p->ctx->device);
-  cudaFree(p->scratch);
-  cudaFree(p->d_L);
-  cudaFree(p->d_dmin);
+  void* ptrs[] = {p->scratch, p->d_L, p->d_dmin};
+  pool_release(p->device, ptrs, 3);
   delete p;
 }
 
@@ -1015,8 +1051,8 @@ int ensure_compact(pars_ctx* ctx, pars_features* f, cudaStream_t st) {
     f->h_cpk_off[r + 1] = (uint32_t)next;
   }
   const size_t words = std::max<size_t>(f->h_cpk_off[f->rows], 4);
-  if (cudaMalloc(&f->d_cpk, words * 4) != cudaSuccess ||
-      cudaMalloc(&f->d_cpk_off, f->h_cpk_off.size() * 4 + 16) != cudaSuccess) {
+  if (!pool_alloc(ctx, (void**)&f->d_cpk, words * 4) ||
+      !pool_alloc(ctx, (void**)&f->d_cpk_off, f->h_cpk_off.size() * 4 + 16)) {
     cudaGetLastError();
     set_error("device allocation failed (compact rows)");
     return PARS_ERR_OOM;
