@@ -633,19 +633,22 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
   const uint32_t m1 = (c.dim / 2 - 1) << 2, m2 = (c.dim / 32 - 1) << 2;
   uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi)) >> 2 : 0u;
   uint32_t hw = sw, A = 0, B = 0, carry = 0;
-  uint32_t w = seq_word(a0, cs, lo, hi);
-  for (int r = cs;; r += 4) {
-    const uint32_t nxt = seq_word(a0, r + 4, lo, hi);
-    const uint32_t ns = nonspace_nibble(w);
+  // two words (8 bytes) per iteration: the mask logic runs once per 8 bytes
+  uint32_t w0 = seq_word(a0, cs, lo, hi), w1 = seq_word(a0, cs + 4, lo, hi);
+  for (int r = cs;; r += 8) {
+    const uint32_t n0 = seq_word(a0, r + 8, lo, hi), n1 = seq_word(a0, r + 12, lo, hi);
+    const uint32_t ns = nonspace_nibble(w0) | (nonspace_nibble(w1) << 4);
     const uint32_t E = (ns << 2) | prev2;  // bit k+2: byte r+k is not a space
     const uint32_t start = ns & ~(E >> 1);
-    const uint32_t own = (ns + ((r < ce ? start : 0u) | carry)) ^ ns;
-    carry = own >> 4;
+    // tokens may start only inside [cs, ce): the second word can lie beyond ce
+    const uint32_t inr = r < ce ? (r + 4 < ce ? 0xffu : 0x0fu) : 0u;
+    const uint32_t own = (ns + ((start & inr) | carry)) ^ ns;
+    carry = own >> 8;
     const uint32_t ev_tri = ns & (E >> 1) & E & own;
-    const uint32_t ev = ev_tri | (~ns & (E >> 1) & own & 0xfu);
+    const uint32_t ev = ev_tri | (~ns & (E >> 1) & own & 0xffu);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t b = (w >> (8 * k)) & 0xffu;
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t b = ((k < 4 ? w0 : w1) >> (8 * (k & 3))) & 0xffu;
       const uint32_t hin = ((start >> k) & 1u) ? sw : hw;
       const uint32_t wend = (hw ^ 0x1fu) * 0x1b3u;  // the word that ends at this space
       const uint32_t tri = (B ^ b) * 0x1b3u;
@@ -654,9 +657,10 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
       hw = (hin ^ b) * 0x1b3u;
       seq_emit(cbase, bbase, dummy, ((ev_tri >> k) & 1u) ? tri : wend, m1, m2, ((ev >> k) & 1u) != 0);
     }
-    prev2 = ns >> 2;
-    if (!carry && (r + 4 >= ce || r + 4 >= hi)) break;
-    w = nxt;
+    prev2 = ns >> 6;
+    if (!carry && (r + 8 >= ce || r + 8 >= hi)) break;
+    w0 = n0;
+    w1 = n1;
   }
 }
 
