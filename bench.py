@@ -583,6 +583,29 @@ def bench_configs(P, ctx, args):
         c2["cpu_epoch_ms"] = 1e3 * (time.perf_counter() - t0)
         c2["cpu_threads"] = thr
     out["c2"] = c2
+    # ---- C3: 100k-request Poisson simulation, FCFS vs PARS (C1 model), the
+    # reference's own driver linked with the drop-in vs with the reference
+    c3b, c3r = ROOT / "oracle" / "_ref" / "c3_b200", ROOT / "oracle" / "_ref" / "c3_ref"
+    if c3b.exists():
+        import subprocess
+        env = dict(os.environ, OMP_NUM_THREADS="1")
+        rb = json.loads(subprocess.run([str(c3b)], capture_output=True, text=True, env=env,
+                                       timeout=900).stdout.strip().splitlines()[-1])
+        c3 = {"workload": "run_simulation of 100,000 Poisson requests (5 req/s, batch 32) with "
+                          "FCFS and PARS (README model) priorities; tools/c3_main.cpp linked with "
+                          "the drop-in (GPU-scored priorities, incremental queue)",
+              "gpu_pars_sim_s": rb["pars"]["wall_s"], "gpu_fcfs_sim_s": rb["fcfs"]["wall_s"],
+              "pars_completion_fnv": rb["pars"]["completion_fnv"],
+              "fcfs_completion_fnv": rb["fcfs"]["completion_fnv"],
+              "parity_bitexact": rb["pars"]["completion_fnv"] == "322bc376a55e1141"
+              and rb["fcfs"]["completion_fnv"] == "7be6c188801b08ca"}
+        if have_ref and c3r.exists():
+            rr = json.loads(subprocess.run([str(c3r)], capture_output=True, text=True, env=env,
+                                           timeout=900).stdout.strip().splitlines()[-1])
+            c3["cpu_pars_sim_s"] = rr["pars"]["wall_s"]
+            c3["cpu_fcfs_sim_s"] = rr["fcfs"]["wall_s"]
+            c3["cpu_threads"] = 1
+        out["c3"] = c3
     # ---- C5, CPU side: all-pairs mask + hinge over a bounded sample
     if have_ref:
         O = Oracle()

@@ -79,3 +79,28 @@ def test_c3_poisson_100k_schedule_bit_exact(ctx, ref):
     assert (gpu["finish"].view(np.uint64) == cpu["finish"].view(np.uint64)).all()
     assert (gpu["ptl"].view(np.uint64) == cpu["ptl"].view(np.uint64)).all()
     assert gpu["iterations"] == cpu["iterations"]
+
+
+C3_B200 = ROOT / "oracle" / "_ref" / "c3_b200"
+
+
+@pytest.mark.gpu
+def test_c3_drop_in_simulator_bit_exact():
+    """BASELINE C3 through the drop-in: the reference's own program (tools/
+    c3_main.cpp, reference headers only) linked with libpars_b200 — GPU-trained
+    README model, GPU-scored priorities, the incremental-queue simulator —
+    reproduces the reference's FCFS and PARS runs."""
+    if not C3_B200.exists():
+        pytest.skip("c3_b200 not built")
+    import json
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    p = subprocess.run([str(C3_B200)], capture_output=True, text=True, env=env, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    assert r["fcfs"]["completion_fnv"] == "7be6c188801b08ca"
+    assert r["fcfs"]["iterations"] == 1723028
+    assert float(r["fcfs"]["simulated_s"]).hex() == (19947.193749500359).hex()
+    assert r["pars"]["completion_fnv"] == "322bc376a55e1141"
+    assert r["pars"]["iterations"] == 1723429
+    assert float(r["pars"]["mean_ms"]).hex() == (15.054321876707261).hex()
+    assert float(r["pars"]["p90_ms"]).hex() == (21.624751098502799).hex()
