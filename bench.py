@@ -328,16 +328,15 @@ def run_ours(args):
         for k in range(max(1, args.e2e_steps) + 1):
             barrier(world)
             t0 = time.perf_counter()
-            s = ctx.score_text(ex, txt, sub_offs, w, 0.0, P.MODE_EXACT)
-            order = ctx.priority_order(s, ids_rank)
+            s, order = ctx.score_order(ex, txt, sub_offs, w, ids_rank)
             t1 = time.perf_counter()
             if k > 0:
                 e2e_vals.append(barrier_max(world, t1 - t0))
     e2e_s = float(np.median(e2e_vals)) if e2e_vals else float("nan")
     e2e_vals_ok = bool(e2e_vals)
     e2e_value = (N_PROMPTS if world > 1 else n) / e2e_s
-    h2d = text_bytes + 8 * (n + 1) + 8 * DIM + 4 * n
-    d2h = 8 * n + 4 * n
+    h2d = text_bytes + 8 * (n + 1) + 8 * DIM + 4 * n  # text, offsets, weights, tie ranks
+    d2h = 8 * n + 4 * n  # scores, order
 
     # secondary: C5 all-pairs step (filtered pairs/s)
     configs = None
@@ -378,7 +377,7 @@ def run_ours(args):
                          "sort_ms": sort_ms},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "prompts/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "api": "pars_score_text + pars_priority_order (host buffers)"},
+                    "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "parity": {"scores_bitexact_sample": parity_ok, "sample": chk},

@@ -60,6 +60,7 @@ struct pars_ctx {
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
       gscratch, lists, plan_buf;
   HostBuf h_offs[2], h_scores;
+  std::vector<cudaEvent_t> ev_chunk;  // per-chunk score hand-off (grow-only)
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -375,6 +376,7 @@ void pars_ctx_destroy(pars_ctx* c) {
     if (b->p) cudaFree(b->p);
   for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores})
     if (b->p) cudaFreeHost(b->p);
+  for (cudaEvent_t e : c->ev_chunk) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(c->ev_copy[k]);
     cudaEventDestroy(c->ev_done[k]);
@@ -413,19 +415,28 @@ namespace {
 // either to pinned host staging (h_out) or stay on the device (d_out).
 int score_text_pipeline(pars_ctx* ctx, const FeatConfig& cfg, const char* text,
                         const int64_t* offsets, int64_t n, const double* weights, double bias,
-                        int mode, double* d_out, double* h_out) {
+                        int mode, double* d_out, double* h_out, std::vector<int64_t>* chunks) {
   cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
   PARS_TRY(upload_weights(ctx, cfg, weights, mode, st));
-  const int64_t kChunkBytes = 64ll << 20, kChunkPrompts = 1 << 18;
+  // chunk sizes ramp 4 MB -> 64 MB so the first kernel starts after a short
+  // first upload (the pipeline fills in ~0.1 ms instead of a full 64 MB copy)
+  const int64_t kChunkPrompts = 1 << 18;
+  int64_t chunk_bytes = 4ll << 20;
   std::vector<int64_t> starts;
   for (int64_t i = 0; i < n;) {
     starts.push_back(i);
     int64_t j = i + 1;
-    while (j < n && j - i < kChunkPrompts && offsets[j + 1] - offsets[i] <= kChunkBytes) ++j;
+    while (j < n && j - i < kChunkPrompts && offsets[j + 1] - offsets[i] <= chunk_bytes) ++j;
     i = j;
+    chunk_bytes = std::min<int64_t>(chunk_bytes * 2, 64ll << 20);
   }
   starts.push_back(n);
   const int nchunks = (int)starts.size() - 1;
+  while ((int)ctx->ev_chunk.size() < nchunks) {
+    cudaEvent_t e;
+    PARS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ev_chunk.push_back(e);
+  }
   int64_t max_bytes = 0, max_n = 0;
   for (int k = 0; k < nchunks; ++k) {
     max_bytes = std::max(max_bytes, offsets[starts[k + 1]] - offsets[starts[k]]);
@@ -457,9 +468,23 @@ int score_text_pipeline(pars_ctx* ctx, const FeatConfig& cfg, const char* text,
     const uint8_t* base = static_cast<const uint8_t*>(ctx->text[b].p) - t0;
     double* dst = d_out ? d_out + i0 : (double*)ctx->scores[b].p;
     PARS_TRY(score_chunk(ctx, cfg, mode, base, (const int64_t*)ctx->offs[b].p, m, bias, dst, st));
-    if (!d_out)
+    if (h_out) {
       PARS_CUDA_CHECK(cudaMemcpyAsync(h_out + i0, dst, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+      PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_chunk[k], st));
+    }
     PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_done[b], st));
+  }
+  *chunks = std::move(starts);
+  return PARS_OK;
+}
+
+// Hands each chunk's scores from pinned staging to the caller's buffer as
+// soon as its copy lands, while later chunks (and the sort) still run.
+int drain_scores(pars_ctx* ctx, const std::vector<int64_t>& chunks, const double* h_stage,
+                 double* out) {
+  for (size_t k = 0; k + 1 < chunks.size(); ++k) {
+    PARS_CUDA_CHECK(cudaEventSynchronize(ctx->ev_chunk[k]));
+    std::memcpy(out + chunks[k], h_stage + chunks[k], (size_t)(chunks[k + 1] - chunks[k]) * 8);
   }
   return PARS_OK;
 }
@@ -491,9 +516,10 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   Guard g(ctx);
   PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
   double* h_sc = static_cast<double*>(ctx->h_scores.p);
-  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, nullptr, h_sc));
+  std::vector<int64_t> chunks;
+  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, nullptr, h_sc, &chunks));
+  PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));
   PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-  std::memcpy(scores, h_sc, (size_t)n * 8);
   return PARS_OK;
 }
 
@@ -528,12 +554,12 @@ int pars_score_order(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   uint32_t* h_o = reinterpret_cast<uint32_t*>(h_sc + n);
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, tie_rank, (size_t)n * 4, cudaMemcpyHostToDevice, st));
   if (boosted) PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, boosted, (size_t)n, cudaMemcpyHostToDevice, st));
-  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, d_s, nullptr));
+  std::vector<int64_t> chunks;
+  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, d_s, h_sc, &chunks));
   PARS_TRY(launch_priority_sort(ctx, d_s, boosted ? d_b : nullptr, d_t, n, d_o, ctx->sort.p, st));
-  PARS_CUDA_CHECK(cudaMemcpyAsync(h_sc, d_s, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(h_o, d_o, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));  // overlaps the sort
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
-  std::memcpy(scores, h_sc, (size_t)n * 8);
   for (int64_t i = 0; i < n; ++i) order[i] = h_o[i];
   return PARS_OK;
 }
