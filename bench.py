@@ -437,7 +437,30 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
             "plan_sorted": plan.sorted,
             "workload": "C5: all 2,147,450,880 unordered pairs of 65,536 prompts (seed 25), "
                         "Eq.1 mask delta=0.2 + hinge + integer grad coefficients (fp64 scores)",
-            "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident"}
+            "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident",
+            "roofline": pairs_roofline(ms)}
+
+
+def pairs_roofline(ms):
+    """The all-pairs kernel is issue-bound (0.5 MB of inputs, DRAM ~0 %): its
+    roofline is the SM issue rate (one warp-instruction per cycle per SMSP).
+    achieved = the kernel's warp-instructions per launch (committed ncu
+    capture, profiles/allpairs_ncu.json) / the step time measured here."""
+    prof = ROOT / "profiles" / "allpairs_ncu.json"
+    if not prof.exists():
+        return None
+    pj = json.loads(prof.read_text())
+    instr = pj.get("warp_instructions")
+    if not instr:
+        return None
+    mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    clk = float(mp.get("sm_max_mhz", 1965.0)) * 1e6
+    peak = 148 * 4 * clk / 1e12  # T warp-instructions/s
+    ach = instr / (ms / 1e3) / 1e12
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "T warp-inst/s",
+            "frac": ach / peak, "source": "profiles/allpairs_ncu.json (executed instructions) "
+            "over this run's step time; peak = 148 SMs x 4 schedulers x max SM clock",
+            "ncu_issue_active_pct": pj.get("issue_active_pct")}
 
 
 def bench_embeddings(P, ctx, torch, dev, stream, args):

@@ -9,6 +9,7 @@ import subprocess
 import sys
 
 rep, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+note = sys.argv[4] if len(sys.argv) > 4 else "one launch over the first n prompts of the C4 workload"
 raw = list(csv.reader(io.StringIO(subprocess.run(
     ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)))
 h, units, v = raw[0], raw[1], raw[2]
@@ -35,8 +36,11 @@ j = {
     "fma_pipe_pct_active": float(d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]),
     "lsu_wavefronts_pct": float(d["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
     "issue_active_pct": float(d["sm__inst_issued.avg.pct_of_peak_sustained_active"]),
+    "ipc_active": float(d["sm__inst_executed.avg.per_cycle_active"]),
+    "warp_instructions": num("smsp__inst_executed.sum"),
+    "fp64_pipe_pct_active": float(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "nan")),
     "dram_throughput_pct": float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]),
-    "note": "ncu --set full --clock-control none, one launch over the first n prompts of the C4 workload",
+    "note": "ncu --set full --clock-control none, " + note,
 }
 json.dump(j, open(out, "w"), indent=1)
 print(json.dumps(j, indent=1))
