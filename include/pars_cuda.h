@@ -125,6 +125,13 @@ void pars_features_free(pars_features* f);
 /* LinearScorer::score(const FeatureVec&) for every row (scorer.cpp:40-42). */
 int pars_features_score(pars_ctx* ctx, const pars_features* f,
                         const double* weights, double bias, double* scores);
+/* Same on the device: rows [row_begin, row_end) of f scored with device
+ * weights into d_scores[row_begin, row_end), asynchronous on `stream` (NULL:
+ * the context's stream). The scoring step of a data-parallel training step. */
+int pars_dev_features_score(pars_ctx* ctx, const pars_features* f,
+                            int64_t row_begin, int64_t row_end,
+                            const double* d_weights, double bias,
+                            double* d_scores, void* stream);
 
 /* ---- pair construction / loss (pairs.hpp, pairs.cpp, train.cpp) ------
  * build_pairs (pairs.cpp:8-36): seeded sampler; host (the mt19937_64 stream

@@ -107,6 +107,7 @@ def _load() -> C.CDLL:
         "pars_train_pairwise": (C.c_int, [vp, vp, vp, vp, vp, i64, dbl, dbl, i32, i32, dbl, u64,
                                           u64, vp, vp, vp]),
         "pars_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+        "pars_dev_features_score": (C.c_int, [vp, vp, i64, i64, vp, dbl, vp, vp]),
         "pars_score_order": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp, vp, vp]),
         "pars_dev_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
         "pars_tie_ranks": (C.c_int, [vp, vp, vp, i64, vp]),

@@ -84,6 +84,14 @@ struct pars_features {
   uint32_t* d_cpk_off = nullptr;  // row offsets into d_cpk (entries)
   std::vector<uint32_t> h_cpk_off;
   int cpk_state = 0;  // 0 not built, 1 built, -1 not representable
+  // column-major copy for X^T c (built on first use)
+  int64_t* d_csc_ptr = nullptr;
+  uint32_t* d_csc_row = nullptr;
+  double* d_csc_val = nullptr;
+  void* d_csc_tasks = nullptr;       // column chunks (one warp each)
+  int64_t* d_csc_col_task = nullptr;  // [dim+1] first task of each column
+  double* d_csc_part = nullptr;       // per-task partial sums
+  int64_t csc_ntasks = 0;
 };
 
 namespace pars_b200 {
@@ -820,8 +828,10 @@ int pars_features_download(pars_ctx* ctx, const pars_features* f, int64_t* row_p
 
 void pars_features_free(pars_features* f) {
   if (!f) return;
-  void* ptrs[] = {f->d_rp, f->d_idx, f->d_val, f->d_cnt, f->d_inv, f->d_cpk, f->d_cpk_off};
-  pool_release(f->device, ptrs, 7);
+  void* ptrs[] = {f->d_rp,      f->d_idx,     f->d_val,     f->d_cnt,       f->d_inv,
+                  f->d_cpk,     f->d_cpk_off, f->d_csc_ptr, f->d_csc_row,   f->d_csc_val,
+                  f->d_csc_tasks, f->d_csc_col_task, f->d_csc_part};
+  pool_release(f->device, ptrs, 13);
   delete f;
 }
 
@@ -841,6 +851,26 @@ int pars_features_score(pars_ctx* ctx, const pars_features* f, const double* wei
   PARS_CUDA_CHECK(cudaGetLastError());
   PARS_CUDA_CHECK(cudaMemcpyAsync(scores, ctx->scores[0].p, (size_t)f->rows * 8, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+// Device-resident LinearScorer::score(FeatureVec) over rows [row_begin,
+// row_end) of a feature set (features.hpp:31-35 + scorer.cpp:40-42): scores
+// land at d_scores[row_begin, row_end). Asynchronous on `stream`.
+int pars_dev_features_score(pars_ctx* ctx, const pars_features* f, int64_t row_begin,
+                            int64_t row_end, const double* d_weights, double bias, double* d_scores,
+                            void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  row_begin = std::max<int64_t>(0, row_begin);
+  row_end = std::min<int64_t>(f->rows, row_end);
+  if (row_end <= row_begin) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  const int64_t m = row_end - row_begin;
+  csr_score_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(
+      f->d_rp + row_begin, f->d_idx, f->d_val, m, d_weights, bias, d_scores + row_begin);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
   return PARS_OK;
 }
 
@@ -1052,10 +1082,38 @@ int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
     PARS_CUDA_CHECK(cudaMemsetAsync(d_grad, 0, (size_t)f->dim * 8, st));
     return PARS_OK;
   }
-  const int parts = xtc_parts(row_end - row_begin);
-  PARS_TRY(ensure(ctx->misc2, (size_t)parts * f->dim * 8));
-  return launch_xtc(ctx, f->d_rp, f->d_idx, f->d_val, d_coeff, row_begin, row_end, f->dim,
-                    (double*)ctx->misc2.p, d_grad, st);
+  if (!f->d_csc_ptr) {  // the transpose, once per feature set
+    auto* fm = const_cast<pars_features*>(f);
+    if (!pool_alloc(ctx, (void**)&fm->d_csc_ptr, ((size_t)f->dim + 1) * 8) ||
+        !pool_alloc(ctx, (void**)&fm->d_csc_row, (size_t)std::max<int64_t>(f->nnz, 1) * 4) ||
+        !pool_alloc(ctx, (void**)&fm->d_csc_val, (size_t)std::max<int64_t>(f->nnz, 1) * 8)) {
+      set_error("device allocation failed (X^T c transpose)");
+      return PARS_ERR_OOM;
+    }
+    if (st != ctx->stream) PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // pool order
+    PARS_TRY(ensure(ctx->misc2, csc_scratch_bytes(f->rows, f->dim)));
+    PARS_TRY(build_csc(ctx, f->d_rp, f->d_idx, f->d_val, f->rows, f->dim, ctx->misc2.p,
+                       fm->d_csc_ptr, fm->d_csc_row, fm->d_csc_val, st));
+    // column chunks of <= 1,024 entries: the one-time host table
+    std::vector<int64_t> ptr((size_t)f->dim + 1), col_task;
+    std::vector<char> tasks;
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ptr.data(), fm->d_csc_ptr, ptr.size() * 8, cudaMemcpyDeviceToHost, st));
+    PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+    fm->csc_ntasks = make_csc_tasks(ptr.data(), f->dim, 1024, tasks, col_task);
+    if (!pool_alloc(ctx, &fm->d_csc_tasks, std::max<size_t>(tasks.size(), 16)) ||
+        !pool_alloc(ctx, (void**)&fm->d_csc_col_task, col_task.size() * 8) ||
+        !pool_alloc(ctx, (void**)&fm->d_csc_part, (size_t)std::max<int64_t>(fm->csc_ntasks, 1) * 8)) {
+      set_error("device allocation failed (X^T c tasks)");
+      return PARS_ERR_OOM;
+    }
+    PARS_CUDA_CHECK(cudaMemcpyAsync(fm->d_csc_tasks, tasks.data(), tasks.size(), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(fm->d_csc_col_task, col_task.data(), col_task.size() * 8,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  }
+  return launch_xtc_csc(ctx, f->d_csc_tasks, f->csc_ntasks, f->d_csc_col_task, f->d_csc_row,
+                        f->d_csc_val, d_coeff, row_begin, row_end, f->dim, f->d_csc_part, d_grad, st);
 }
 
 // ---- training ------------------------------------------------------------

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <vector>
 #include <cmath>
 
 #include "common.cuh"
@@ -169,48 +171,135 @@ __global__ void __launch_bounds__(kTile) tau_kernel(const double* __restrict__ x
   }
 }
 
-// X^T c over a CSR row range: each CTA walks its rows in order and
-// accumulates c_i * v into a shared dense vector (indices within one row are
-// unique, so no atomics); per-CTA partials are summed in CTA order by
-// xtc_reduce_kernel -> deterministic.
-__global__ void xtc_partial_kernel(const int64_t* __restrict__ rp, const uint32_t* __restrict__ idx,
-                                   const double* __restrict__ val, const int32_t* __restrict__ c,
-                                   int64_t r0, int64_t r1, uint32_t dim,
-                                   double* __restrict__ partial) {
-  extern __shared__ double g[];
-  for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) g[d] = 0.0;
-  __syncthreads();
-  const int64_t rows = r1 - r0;
-  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
-  const int64_t a = r0 + (int64_t)blockIdx.x * per;
-  const int64_t b = min(r1, a + per);
-  for (int64_t r = a; r < b; ++r) {
-    const int32_t ci = c[r];
-    if (ci != 0) {
-      const double cd = (double)ci;
-      for (int64_t k = rp[r] + threadIdx.x; k < rp[r + 1]; k += blockDim.x)
-        g[idx[k]] = __dadd_rn(g[idx[k]], __dmul_rn(cd, val[k]));
-    }
-    __syncthreads();
-  }
-  for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x)
-    partial[(int64_t)blockIdx.x * dim + d] = g[d];
-}
-
-__global__ void xtc_reduce_kernel(const double* __restrict__ partial, int nparts, uint32_t dim,
-                                  double* __restrict__ grad) {
-  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= dim) return;
-  double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s = __dadd_rn(s, partial[(int64_t)p * dim + d]);
-  grad[d] = s;
-}
-
 int sms_of_current() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sms;
+}
+
+// ---- X^T c through a column-major (CSC) copy of the features -------------
+// The feature matrix is fixed for a whole training run, so its transpose is
+// built once (stable: entries of a column in row order) and every step's
+// gradient becomes one warp per column: lane-strided partial sums of
+// c[row] * val in entry order, then a fixed xor-shuffle tree — deterministic
+// for a given row range, with no shared-memory accumulator or per-row
+// barrier. Rows [r0, r1) of a shard are found by binary search (each
+// column's rows are sorted).
+constexpr int kCscRows = 128;  // rows per placement block
+
+__global__ void csc_block_count(const int64_t* __restrict__ rp, const uint32_t* __restrict__ idx,
+                                int64_t rows, uint32_t dim, uint32_t* __restrict__ bcnt) {
+  extern __shared__ uint32_t h[];
+  for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) h[d] = 0;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kCscRows, r1 = min(rows, r0 + kCscRows);
+  for (int64_t k = rp[r0] + threadIdx.x; k < rp[r1]; k += blockDim.x) atomicAdd(&h[idx[k]], 1u);
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x) bcnt[(int64_t)blockIdx.x * dim + d] = h[d];
+}
+
+// per column: block offsets (exclusive over blocks) and the column total
+__global__ void csc_column_scan(uint32_t* __restrict__ bcnt, int nblocks, uint32_t dim,
+                                uint32_t* __restrict__ colcnt) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= dim) return;
+  uint32_t run = 0;
+  for (int b = 0; b < nblocks; ++b) {
+    const uint32_t c = bcnt[(int64_t)b * dim + d];
+    bcnt[(int64_t)b * dim + d] = run;
+    run += c;
+  }
+  colcnt[d] = run;
+}
+
+__global__ void csc_ptr_scan(const uint32_t* __restrict__ colcnt, uint32_t dim,
+                             int64_t* __restrict__ ptr) {
+  if (threadIdx.x != 0) return;
+  int64_t run = 0;
+  for (uint32_t d = 0; d < dim; ++d) {
+    ptr[d] = run;
+    run += colcnt[d];
+  }
+  ptr[dim] = run;
+}
+
+__global__ void csc_place(const int64_t* __restrict__ rp, const uint32_t* __restrict__ idx,
+                          const double* __restrict__ val, int64_t rows, uint32_t dim,
+                          const uint32_t* __restrict__ boff, const int64_t* __restrict__ ptr,
+                          uint32_t* __restrict__ crow, double* __restrict__ cval) {
+  extern __shared__ uint32_t cur[];
+  for (uint32_t d = threadIdx.x; d < dim; d += blockDim.x)
+    cur[d] = boff[(int64_t)blockIdx.x * dim + d];
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kCscRows, r1 = min(rows, r0 + kCscRows);
+  for (int64_t r = r0; r < r1; ++r) {
+    // a row's columns are unique: its entries take distinct cursors
+    for (int64_t k = rp[r] + threadIdx.x; k < rp[r + 1]; k += blockDim.x) {
+      const uint32_t d = idx[k];
+      const int64_t pos = ptr[d] + cur[d];
+      cur[d] += 1;
+      crow[pos] = (uint32_t)r;
+      cval[pos] = val[k];
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int64_t lower_row(const uint32_t* __restrict__ rows, int64_t lo,
+                                             int64_t hi, int64_t r) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)rows[mid] < r)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One warp per task = a fixed chunk of one column's entries (long columns —
+// hot buckets present in most prompts — are split so no warp walks tens of
+// thousands of dependent gathers): lane-strided partial sums in entry order,
+// then a fixed xor-shuffle tree. The row range [r0, r1) clamps the chunk.
+struct CscTask {
+  int64_t beg, end;
+  int32_t col, pad;
+};
+
+__global__ void xtc_csc_kernel(const CscTask* __restrict__ tasks, int64_t ntasks,
+                               const uint32_t* __restrict__ crow, const double* __restrict__ cval,
+                               const int32_t* __restrict__ c, int64_t r0, int64_t r1,
+                               double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= ntasks) return;
+  const CscTask tk = tasks[t];
+  const int64_t b = lower_row(crow, tk.beg, tk.end, r0);
+  const int64_t e = lower_row(crow, b, tk.end, r1);
+  double s = 0.0;
+  int64_t k = b + lane;
+  for (; k + 96 < e; k += 128) {  // four independent gathers in flight
+    const uint32_t q0 = crow[k], q1 = crow[k + 32], q2 = crow[k + 64], q3 = crow[k + 96];
+    const double v0 = cval[k], v1 = cval[k + 32], v2 = cval[k + 64], v3 = cval[k + 96];
+    const double p0 = __dmul_rn((double)c[q0], v0), p1 = __dmul_rn((double)c[q1], v1);
+    const double p2 = __dmul_rn((double)c[q2], v2), p3 = __dmul_rn((double)c[q3], v3);
+    s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+  }
+  for (; k < e; k += 32) s = __dadd_rn(s, __dmul_rn((double)c[crow[k]], cval[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if (lane == 0) part[t] = s;
+}
+
+// column d = the sum of its tasks' partials, in task order
+__global__ void xtc_task_reduce(const int64_t* __restrict__ col_task, const double* __restrict__ part,
+                                uint32_t dim, double* __restrict__ grad) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= dim) return;
+  double s = 0.0;
+  for (int64_t t = col_task[d]; t < col_task[d + 1]; ++t) s = __dadd_rn(s, part[t]);
+  grad[d] = s;
 }
 
 }  // namespace
@@ -252,26 +341,57 @@ int launch_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
   return PARS_OK;
 }
 
-int xtc_parts(int64_t rows) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(sms_of_current(), ceil_div(rows, 64)));
+size_t csc_scratch_bytes(int64_t rows, uint32_t dim) {
+  return (size_t)ceil_div(std::max<int64_t>(rows, 1), kCscRows) * dim * 4 + (size_t)dim * 4 + 256;
 }
 
-int launch_xtc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
-               const int32_t* c, int64_t r0, int64_t r1, uint32_t dim, double* partial,
-               double* grad, cudaStream_t st) {
-  const int parts = xtc_parts(r1 - r0);
-  const size_t smem = (size_t)dim * sizeof(double);
-  if (smem > 227 * 1024) {
-    set_error("X^T c: dimension %u exceeds the shared-memory accumulator", dim);
-    return PARS_ERR_UNSUPPORTED;
-  }
-  PARS_CUDA_CHECK(cudaFuncSetAttribute(xtc_partial_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  xtc_partial_kernel<<<parts, 256, smem, st>>>(rp, idx, val, c, r0, r1, dim, partial);
-  xtc_reduce_kernel<<<(unsigned)ceil_div(dim, 256), 256, 0, st>>>(partial, parts, dim, grad);
+int build_csc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
+              int64_t rows, uint32_t dim, void* scratch, int64_t* ptr, uint32_t* crow,
+              double* cval, cudaStream_t st) {
+  if (rows <= 0) return PARS_OK;
+  const int nb = (int)ceil_div(rows, kCscRows);
+  uint32_t* bcnt = static_cast<uint32_t*>(scratch);
+  uint32_t* colcnt = bcnt + (size_t)nb * dim;
+  const size_t sm = (size_t)dim * 4;
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(csc_block_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(csc_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  csc_block_count<<<nb, 256, sm, st>>>(rp, idx, rows, dim, bcnt);
+  csc_column_scan<<<(unsigned)ceil_div(dim, 256), 256, 0, st>>>(bcnt, nb, dim, colcnt);
+  csc_ptr_scan<<<1, 32, 0, st>>>(colcnt, dim, ptr);
+  csc_place<<<nb, 256, sm, st>>>(rp, idx, val, rows, dim, bcnt, ptr, crow, cval);
+  count_launch(ctx, 4);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  return PARS_OK;
+}
+
+int launch_xtc_csc(pars_ctx* ctx, const void* tasks, int64_t ntasks, const int64_t* col_task,
+                   const uint32_t* crow, const double* cval, const int32_t* c, int64_t r0,
+                   int64_t r1, uint32_t dim, double* part, double* grad, cudaStream_t st) {
+  xtc_csc_kernel<<<(unsigned)ceil_div(ntasks * 32, 256), 256, 0, st>>>(
+      static_cast<const CscTask*>(tasks), ntasks, crow, cval, c, r0, r1, part);
+  xtc_task_reduce<<<(unsigned)ceil_div(dim, 256), 256, 0, st>>>(col_task, part, dim, grad);
   count_launch(ctx, 2);
   PARS_CUDA_CHECK(cudaGetLastError());
   return PARS_OK;
+}
+
+size_t csc_task_bytes() { return sizeof(CscTask); }
+
+// Host: split every column [ptr[d], ptr[d+1]) into chunks of at most `chunk`
+// entries. Fills task records (packed CscTask) and col_task[dim+1].
+int64_t make_csc_tasks(const int64_t* ptr, uint32_t dim, int64_t chunk, std::vector<char>& tasks,
+                       std::vector<int64_t>& col_task) {
+  std::vector<CscTask> t;
+  col_task.assign((size_t)dim + 1, 0);
+  for (uint32_t d = 0; d < dim; ++d) {
+    col_task[d] = (int64_t)t.size();
+    for (int64_t b = ptr[d]; b < ptr[d + 1]; b += chunk)
+      t.push_back(CscTask{b, std::min(ptr[d + 1], b + chunk), (int32_t)d, 0});
+  }
+  col_task[dim] = (int64_t)t.size();
+  tasks.resize(t.size() * sizeof(CscTask));
+  if (!t.empty()) std::memcpy(tasks.data(), t.data(), tasks.size());
+  return (int64_t)t.size();
 }
 
 }  // namespace pars_b200

@@ -2,6 +2,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace pars_b200 {
@@ -13,11 +15,18 @@ int launch_allpairs(pars_ctx* ctx, const double* s, const int32_t* L, const int3
 int launch_sum_partials(pars_ctx* ctx, const double* p, int64_t n, double* out, cudaStream_t st);
 int launch_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
                unsigned long long* out, cudaStream_t st);
-int xtc_parts(int64_t rows);
-int launch_xtc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
-               const int32_t* c, int64_t r0, int64_t r1, uint32_t dim, double* partial,
-               double* grad, cudaStream_t st);
-
+// Column-major copy of a CSR feature set (stable: rows ascending within a
+// column) and the per-step gradient X[r0:r1]^T c over it.
+size_t csc_scratch_bytes(int64_t rows, uint32_t dim);
+int build_csc(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, const double* val,
+              int64_t rows, uint32_t dim, void* scratch, int64_t* ptr, uint32_t* crow,
+              double* cval, cudaStream_t st);
+int launch_xtc_csc(pars_ctx* ctx, const void* tasks, int64_t ntasks, const int64_t* col_task,
+                   const uint32_t* crow, const double* cval, const int32_t* c, int64_t r0,
+                   int64_t r1, uint32_t dim, double* part, double* grad, cudaStream_t st);
+size_t csc_task_bytes();
+int64_t make_csc_tasks(const int64_t* ptr, uint32_t dim, int64_t chunk, std::vector<char>& tasks,
+                       std::vector<int64_t>& col_task);
 // length-sorted all-pairs plan (pairs_sorted.cu)
 struct PairPlanDev {
   int64_t n = 0;

@@ -14,6 +14,12 @@ Only the paths that shard naturally are partitioned:
 * full-batch step: grad = X^T c over each rank's row shard, all-reduced
   (D doubles), then the update.
 
+`train_step` is the whole C5 data-parallel step — score this rank's prompt
+shard with the current weights, all-gather the scores, the rank's all-pairs
+tiles, the coefficient all-reduce, X^T c on the row shard, the gradient
+all-reduce and w -= (lr / kept) * grad — with every collective on device
+tensors and no host synchronisation inside the step.
+
 The per-rank compute is the CUDA kernel (`pars_dev_allpairs`); the CPU tests
 substitute a reference implementation of the same per-tile contract to check
 the partition and the collectives with the gloo backend.
@@ -65,16 +71,17 @@ def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream, plan
     import torch
     from ._lib import ParsError, lib
 
-    def run(t0: int, t1: int):
-        dev = d_scores.device
+    def run(t0: int, t1: int, scores=None):
+        d_s = d_scores if scores is None else scores
+        dev = d_s.device
         c = torch.zeros(n, dtype=torch.int32, device=dev)
         cnt = torch.zeros(4, dtype=torch.int64, device=dev)
         part = torch.zeros(max(1, t1 - t0), dtype=torch.float64, device=dev)
         if plan is not None:
-            plan.run(d_scores.data_ptr(), margin, t0, t1, c.data_ptr(), cnt.data_ptr(),
+            plan.run(d_s.data_ptr(), margin, t0, t1, c.data_ptr(), cnt.data_ptr(),
                      part.data_ptr(), stream or 0)
         else:
-            rc = lib().pars_dev_allpairs(ctx.h, d_scores.data_ptr(), d_lengths.data_ptr(), n, delta,
+            rc = lib().pars_dev_allpairs(ctx.h, d_s.data_ptr(), d_lengths.data_ptr(), n, delta,
                                          margin, max_len, t0, t1, c.data_ptr(), cnt.data_ptr(),
                                          part.data_ptr(), stream)
             if rc != 0:
@@ -136,3 +143,70 @@ def grad_step_gpu(ctx, feats, d_coeff, scale: float, group=None, stream: int = 0
     if world > 1:
         dist.all_reduce(g, group=group)
     return g * scale
+
+
+def train_step(n: int, w, scores_pad, score_rows: Callable, tiles: Callable, xt_c: Callable,
+               lr_over_kept: float, group=None):
+    """One full-batch data-parallel step of all-pairs margin-ranking training.
+
+    w             device float64[D], updated in place
+    scores_pad    device float64[per * world] (per = ceil(n / world)); rank r
+                  owns [r*per, r*per + shard); the first n entries end up as
+                  the full score vector on every rank
+    score_rows(r0, r1, out)  writes scores of prompts [r0, r1) into out[0:r1-r0]
+    tiles(scores, t0, t1)    -> (coeff int32[n], counts int64[2], loss partials)
+    xt_c(coeff, r0, r1)      -> float64[D] = X[r0:r1]^T coeff[r0:r1]
+    Returns device tensors (counts = kept, active; loss partials of this
+    rank's tiles, in tile order)."""
+    dist = _dist()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    per = (n + world - 1) // world
+    r0, r1 = shard_range(n, world, rank)
+    mine = scores_pad[rank * per:(rank + 1) * per]
+    if r1 > r0:
+        score_rows(r0, r1, mine)
+    if world > 1:
+        dist.all_gather_into_tensor(scores_pad, mine, group=group)
+    t0, t1 = tile_range(n, world, rank)
+    c, cnt, part = tiles(scores_pad[:n], t0, t1)
+    if world > 1:
+        dist.all_reduce(c, group=group)
+        dist.all_reduce(cnt, group=group)
+    g = xt_c(c, r0, r1)
+    if world > 1:
+        dist.all_reduce(g, group=group)
+    w.sub_(g * lr_over_kept)
+    return cnt, part
+
+
+def train_step_gpu(ctx, feats, d_w, scores_pad, d_lengths, n: int, delta: float, margin: float,
+                   max_len: int, lr_over_kept: float, stream: int = 0, group=None, plan=None):
+    """train_step with the CUDA kernels: pars_dev_features_score (exact CSR
+    dot), the all-pairs tiles (length-sorted plan kernel when `plan` is
+    given) and pars_dev_xt_c."""
+    import torch
+    from ._lib import ParsError, lib
+
+    def check(rc):
+        if rc != 0:
+            raise ParsError(rc, lib().pars_last_error().decode())
+
+    def score_rows(r0, r1, out):
+        # the kernel writes d_scores[r0:r1]; point it so that lands in out
+        base = out.data_ptr() - r0 * 8
+        check(lib().pars_dev_features_score(ctx.h, C.c_void_p(feats.h), r0, r1, d_w.data_ptr(),
+                                            0.0, base, stream or None))
+
+    gpu_tiles = _gpu_tiles(ctx, None, d_lengths, n, delta, margin, max_len, stream or None, plan)
+
+    def tiles(scores, t0, t1):
+        return gpu_tiles(t0, t1, scores)
+
+    def xt_c(c, r0, r1):
+        g = torch.empty(feats.dim, dtype=torch.float64, device=d_w.device)
+        check(lib().pars_dev_xt_c(ctx.h, C.c_void_p(feats.h), c.data_ptr(), r0, r1, g.data_ptr(),
+                                  stream or None))
+        return g
+
+    return train_step(n, d_w, scores_pad, score_rows, tiles, xt_c, lr_over_kept, group)

@@ -113,3 +113,61 @@ def test_allpairs_dp_gloo_matches_single_process_and_oracle(world, oracle):
         # per-tile partials summed in tile order: bit-identical for any world size
         assert loss == single[3]
         assert abs(loss - oloss) <= 1e-12 * max(1.0, oloss)
+
+
+def _step_fns(X, lens, delta, margin):
+    """CPU stand-ins for the three per-rank kernels of train_step."""
+    def score_rows(r0, r1, out):
+        out[: r1 - r0] = torch.from_numpy(X[r0:r1]) @ W["w"]
+
+    def tiles(scores, t0, t1):
+        return tile_compute_numpy(scores.numpy(), lens, delta, margin)(t0, t1)
+
+    def xt_c(c, r0, r1):
+        return torch.from_numpy(X[r0:r1].T) @ c[r0:r1].to(torch.float64)
+
+    return score_rows, tiles, xt_c
+
+
+W = {}
+
+
+def _step_worker(rank, world, port, X, lens, w0, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = X.shape[0]
+        w = torch.tensor(w0)
+        W["w"] = w
+        per = (n + world - 1) // world
+        pad = torch.zeros(per * world, dtype=torch.float64)
+        fns = _step_fns(X, lens, 0.2, 1.0)
+        cnt, _ = D.train_step(n, w, pad, *fns, lr_over_kept=0.1 / 1000)
+        out[rank] = (w.numpy().tolist(), cnt.numpy().tolist(), pad[:n].numpy().tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_train_step_gloo_matches_single_process():
+    """The full DP step (shard scoring + score all-gather, tile slice +
+    coefficient all-reduce, X^T c + gradient all-reduce, update) on 2 ranks
+    equals the single-process step: scores and integer counts exactly, the
+    weights to fp64 summation-order rounding."""
+    rng = np.random.default_rng(9)
+    n, dim = 300, 16
+    X = rng.normal(size=(n, dim))
+    lens = rng.integers(1, 200, size=n)
+    w0 = rng.normal(size=dim) * 0.1
+    w1 = torch.tensor(w0)
+    W["w"] = w1
+    pad = torch.zeros(n, dtype=torch.float64)
+    cnt1, _ = D.train_step(n, w1, pad, *_step_fns(X, lens, 0.2, 1.0), lr_over_kept=0.1 / 1000)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_step_worker, args=(2, _free_port(), X, lens, w0, out), nprocs=2, join=True,
+                       start_method="fork")
+    for r in range(2):
+        w, cnt, sc = out[r]
+        assert cnt == cnt1.numpy().tolist()
+        np.testing.assert_allclose(sc, X @ w0, rtol=1e-13, atol=1e-14)
+        np.testing.assert_allclose(w, w1.numpy(), rtol=1e-12, atol=1e-15)
