@@ -199,6 +199,33 @@ __global__ void csr_score_kernel(const int64_t* __restrict__ rp, const uint32_t*
   out[r] = __dadd_rn(s, bias);
 }
 
+// Same dot over the compact rows (idx << 16 | count16, 4-entry aligned):
+// v = count * inv_row is recomputed with the very __dmul_rn that produced the
+// CSR value, so the products and the sequential sum are identical; 4 bytes
+// per entry instead of 12, read 16 bytes at a time.
+__global__ void cpk_score_kernel(const int64_t* __restrict__ rp, const uint32_t* __restrict__ cpk,
+                                 const uint32_t* __restrict__ off, const double* __restrict__ inv_row,
+                                 int64_t rows, const double* __restrict__ w, double bias,
+                                 double* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t len = rp[r + 1] - rp[r];
+  const uint32_t* row = cpk + off[r];
+  const double inv = inv_row[r];
+  double s = 0.0;
+  int64_t k = 0;
+  for (; k + 4 <= len; k += 4) {
+    const uint4 q = *reinterpret_cast<const uint4*>(row + k);
+    const uint32_t e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      s = __dadd_rn(s, __dmul_rn(w[e[j] >> 16], __dmul_rn((double)(int16_t)(e[j] & 0xffffu), inv)));
+  }
+  for (; k < len; ++k)
+    s = __dadd_rn(s, __dmul_rn(w[row[k] >> 16], __dmul_rn((double)(int16_t)(row[k] & 0xffffu), inv)));
+  out[r] = __dadd_rn(s, bias);
+}
+
 // Compact per-prompt slots into a CSR.
 __global__ void compact_kernel(const int64_t* __restrict__ slot, const int64_t* __restrict__ rp,
                                int64_t n, const uint32_t* __restrict__ sidx,
@@ -854,26 +881,6 @@ int pars_features_score(pars_ctx* ctx, const pars_features* f, const double* wei
   return PARS_OK;
 }
 
-// Device-resident LinearScorer::score(FeatureVec) over rows [row_begin,
-// row_end) of a feature set (features.hpp:31-35 + scorer.cpp:40-42): scores
-// land at d_scores[row_begin, row_end). Asynchronous on `stream`.
-int pars_dev_features_score(pars_ctx* ctx, const pars_features* f, int64_t row_begin,
-                            int64_t row_end, const double* d_weights, double bias, double* d_scores,
-                            void* stream) {
-  PARS_TRY(check_ctx(ctx));
-  row_begin = std::max<int64_t>(0, row_begin);
-  row_end = std::min<int64_t>(f->rows, row_end);
-  if (row_end <= row_begin) return PARS_OK;
-  Guard g(ctx);
-  cudaStream_t st = pick(ctx, stream);
-  const int64_t m = row_end - row_begin;
-  csr_score_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(
-      f->d_rp + row_begin, f->d_idx, f->d_val, m, d_weights, bias, d_scores + row_begin);
-  count_launch(ctx);
-  PARS_CUDA_CHECK(cudaGetLastError());
-  return PARS_OK;
-}
-
 // ---- all-pairs -----------------------------------------------------------
 
 int64_t pars_allpairs_tiles(int64_t n) { return allpairs_tile_count(n); }
@@ -1228,6 +1235,34 @@ int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uin
 
 }  // namespace capi_detail
 }  // namespace pars_b200
+
+// Device-resident LinearScorer::score(FeatureVec) over rows [row_begin,
+// row_end) of a feature set (features.hpp:31-35 + scorer.cpp:40-42): scores
+// land at d_scores[row_begin, row_end). Asynchronous on `stream`.
+int pars_dev_features_score(pars_ctx* ctx, const pars_features* f, int64_t row_begin,
+                            int64_t row_end, const double* d_weights, double bias, double* d_scores,
+                            void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  row_begin = std::max<int64_t>(0, row_begin);
+  row_end = std::min<int64_t>(f->rows, row_end);
+  if (row_end <= row_begin) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  const int64_t m = row_end - row_begin;
+  auto* fm = const_cast<pars_features*>(f);
+  PARS_TRY(ensure_compact(ctx, fm, st));
+  if (f->cpk_state == 1)
+    cpk_score_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(
+        f->d_rp + row_begin, f->d_cpk, f->d_cpk_off + row_begin, f->d_inv + row_begin, m, d_weights,
+        bias, d_scores + row_begin);
+  else
+    csr_score_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(
+        f->d_rp + row_begin, f->d_idx, f->d_val, m, d_weights, bias, d_scores + row_begin);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  return PARS_OK;
+}
+
 
 int pars_sgd_epoch(pars_ctx* ctx, const pars_features* f, const uint32_t* a, const uint32_t* b,
                    const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,

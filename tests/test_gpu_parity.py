@@ -425,3 +425,25 @@ def test_score_order_fused_matches_two_calls_and_oracle(ctx, oracle):
     assert (s.view(np.uint64) == s2.view(np.uint64)).all()
     assert (order == ctx.priority_order(s2, tie, boosted)).all()
     assert (order == oracle.select_order(arrival, ids, s2, boosted, 0.0)).all()
+
+
+def test_dev_features_score_compact_rows_bit_identical(ctx, oracle):
+    """pars_dev_features_score (the scoring step of the DP training step)
+    over the compact (idx, count16) rows, row shards included, equals the
+    reference's score_batch bit for bit."""
+    import ctypes
+    import torch
+    from paper_2510_03243_b200 import Extractor, Workload, lib
+    wl = Workload.synthesize(2500, 12)
+    e = Extractor.make()
+    f = ctx.extract(e, wl.text, wl.offsets)
+    w = np.random.default_rng(13).normal(size=4096)
+    d_w = torch.from_numpy(w).cuda()
+    out = torch.full((len(wl),), float("nan"), dtype=torch.float64, device="cuda")
+    for r0, r1 in ((0, 1000), (1000, 1001), (1001, len(wl))):
+        assert lib().pars_dev_features_score(ctx.h, ctypes.c_void_p(f.h), r0, r1, d_w.data_ptr(), 0.5,
+                                             out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    want = oracle.score_batch(oex(e), wl.text, wl.offsets, w, 0.5)
+    assert (out.cpu().numpy().view(np.uint64) == want.view(np.uint64)).all()
+    f.free()
