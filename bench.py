@@ -261,13 +261,13 @@ def run_ours(args):
                                    d_offs.data_ptr(), n, d_w.data_ptr(), 0.0, P.MODE_EXACT,
                                    d_scores.data_ptr(), sh)
         if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode())
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
         if ev is not None:
             ev[1].record(stream)
         rc = L.pars_dev_priority_order(ctx.h, d_scores.data_ptr(), None, d_tie.data_ptr(), n,
                                        d_order.data_ptr(), sh)
         if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode())
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
         if ev is not None:
             ev[2].record(stream)
 
@@ -507,7 +507,7 @@ def bench_embeddings(P, ctx, torch, dev, stream, args):
         rc = L.pars_dev_score_embeddings(ctx.h, C.byref(ex), X.data_ptr(), n, w.data_ptr(), 0.0,
                                          P.MODE_EXACT, out.data_ptr(), sh)
         if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode())
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
 
     for _ in range(3):
         step()

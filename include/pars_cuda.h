@@ -108,6 +108,35 @@ int pars_dev_score_embeddings(pars_ctx* ctx, const pars_extractor* ex,
                               const double* d_weights, double bias, int mode,
                               double* d_scores, void* stream);
 
+/* ---- dataset ingestion (load_dataset, dataset.cpp:73-173) ------------ */
+/* The records of a JSONL dataset file parsed and validated ON THE GPU into a
+ * device-resident prompt arena + int64 offsets (what pars_dev_score_text
+ * reads), ids, output_len and prompt_len (given, or the whitespace token
+ * count). Same acceptance and the reference's error text ("<path>: line N:
+ * ..."), limit < 0 = no limit. Records carrying an 'embedding' array are
+ * rejected with PARS_ERR_UNSUPPORTED (the GPU loader does not parse them). */
+typedef struct pars_dataset pars_dataset;
+int pars_load_dataset(pars_ctx* ctx, const char* path, int64_t limit,
+                      pars_dataset** out);
+int pars_load_dataset_bytes(pars_ctx* ctx, const char* path_for_messages,
+                            const char* bytes, int64_t nbytes, int64_t limit,
+                            pars_dataset** out);
+int64_t pars_dataset_size(const pars_dataset* d);
+int64_t pars_dataset_text_bytes(const pars_dataset* d);
+int64_t pars_dataset_id_bytes(const pars_dataset* d);
+int64_t pars_dataset_embedding_dim(const pars_dataset* d);
+const char* pars_dataset_dev_text(const pars_dataset* d);        /* device */
+const int64_t* pars_dataset_dev_offsets(const pars_dataset* d);  /* device, [n+1] */
+const int64_t* pars_dataset_dev_output_len(const pars_dataset* d);
+/* host copies (any pointer may be NULL) */
+int pars_dataset_export(const pars_dataset* d, char* text, int64_t* offsets,
+                        int64_t* output_len, int64_t* prompt_len, char* ids,
+                        int64_t* id_offsets);
+/* output_len_samples of record i; returns the count (-1 if > cap) */
+int64_t pars_dataset_samples(const pars_dataset* d, int64_t i, int64_t* out,
+                             int64_t cap);
+void pars_dataset_free(pars_dataset* d);
+
 /* ---- features (extract_all, features.cpp:124-150) -------------------- */
 int pars_extract(pars_ctx* ctx, const pars_extractor* ex, const char* text,
                  const int64_t* offsets, int64_t n, const double* embeddings,

@@ -241,7 +241,7 @@ class Dataset:
 
     def __init__(self, ref: "Ref", handle):
         if not handle:
-            raise OracleError(ref.L.ref_last_error().decode())
+            raise OracleError(ref.L.ref_last_error().decode("utf-8", "replace"))
         self.ref, self.h = ref, handle
         L = ref.L
         n = L.ref_dataset_size(handle)
@@ -286,8 +286,12 @@ class Ref:
         L = self.L = C.CDLL(str(path))
         L.ref_last_error.restype = C.c_char_p
         for name in ("ref_synthesize", "ref_dataset_from_arrays", "ref_split", "ref_subset",
-                     "ref_simulate"):
+                     "ref_simulate", "ref_load_dataset"):
             getattr(L, name).restype = C.c_void_p
+        L.ref_load_dataset.argtypes = [C.c_char_p, C.c_int64]
+        L.ref_save_dataset.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_dataset_samples.restype = C.c_int64
+        L.ref_dataset_samples.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_int64]
         L.ref_synthesize.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64,
                                      C.c_int64, C.c_int64]
         L.ref_split.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int]
@@ -329,7 +333,7 @@ class Ref:
         L.ref_set_threads.argtypes = [C.c_int]
 
     def _err(self):
-        return OracleError(self.L.ref_last_error().decode())
+        return OracleError(self.L.ref_last_error().decode("utf-8", "replace"))
 
     def set_threads(self, n):
         self.L.ref_set_threads(n)
@@ -337,6 +341,19 @@ class Ref:
     # datasets
     def synthesize(self, n, seed, mu=5.0, sigma=1.2, embed_dim=0, max_len=0):
         return Dataset(self, self.L.ref_synthesize(n, mu, sigma, seed, embed_dim, max_len))
+
+    def load_dataset(self, path, limit=-1):
+        """load_dataset (dataset.cpp:73-173); raises OracleError with its message."""
+        return Dataset(self, self.L.ref_load_dataset(str(path).encode(), limit))
+
+    def save_dataset(self, ds, path):
+        if self.L.ref_save_dataset(ds.h, str(path).encode()) != 0:
+            raise self._err()
+
+    def samples(self, ds, i):
+        out = np.zeros(4096, np.int64)
+        k = self.L.ref_dataset_samples(ds.h, C.c_uint64(i), _ptr(out), C.c_int64(4096))
+        return out[:k].tolist()
 
     def from_arrays(self, text, offs, output_len, prompt_len=None, emb=None):
         text = np.ascontiguousarray(text, np.uint8)

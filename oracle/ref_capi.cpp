@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <optional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -126,6 +127,26 @@ void* ref_dataset_from_arrays(const char* text, const int64_t* offs,
   return ds;
 }
 
+// load_dataset / save_dataset (dataset.cpp:73-195), for the ingestion parity
+// tests; limit < 0 means no limit.
+void* ref_load_dataset(const char* path, int64_t limit) {
+  Dataset* ds = nullptr;
+  int rc = guard([&] {
+    std::optional<size_t> lim;
+    if (limit >= 0) lim = static_cast<size_t>(limit);
+    ds = new Dataset(load_dataset(path, lim));
+  });
+  return rc == 0 ? ds : nullptr;
+}
+int ref_save_dataset(void* h, const char* path) {
+  return guard([&] { save_dataset(path, *static_cast<Dataset*>(h)); });
+}
+int64_t ref_dataset_samples(void* h, uint64_t i, int64_t* out, int64_t cap) {
+  const auto& s = static_cast<Dataset*>(h)->records[i].output_len_samples;
+  if (static_cast<int64_t>(s.size()) > cap) return -1;
+  for (size_t k = 0; k < s.size(); ++k) out[k] = s[k];
+  return static_cast<int64_t>(s.size());
+}
 void ref_dataset_free(void* ds) { delete static_cast<Dataset*>(ds); }
 uint64_t ref_dataset_size(void* ds) { return static_cast<Dataset*>(ds)->size(); }
 int64_t ref_dataset_text_bytes(void* h) {

@@ -82,6 +82,18 @@ def _load() -> C.CDLL:
         "pars_dev_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
         "pars_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
         "pars_dev_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
+        "pars_load_dataset": (C.c_int, [vp, C.c_char_p, i64, vp]),
+        "pars_load_dataset_bytes": (C.c_int, [vp, C.c_char_p, C.c_char_p, i64, i64, vp]),
+        "pars_dataset_size": (i64, [vp]),
+        "pars_dataset_text_bytes": (i64, [vp]),
+        "pars_dataset_id_bytes": (i64, [vp]),
+        "pars_dataset_embedding_dim": (i64, [vp]),
+        "pars_dataset_dev_text": (vp, [vp]),
+        "pars_dataset_dev_offsets": (vp, [vp]),
+        "pars_dataset_dev_output_len": (vp, [vp]),
+        "pars_dataset_export": (C.c_int, [vp] * 7),
+        "pars_dataset_samples": (i64, [vp, i64, vp, i64]),
+        "pars_dataset_free": (None, [vp]),
         "pars_extract": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
         "pars_features_upload": (C.c_int, [vp, u32, i64, vp, vp, vp, vp]),
         "pars_features_rows": (i64, [vp]),
@@ -295,6 +307,58 @@ class Features:
             pass
 
 
+class GpuDataset:
+    """A dataset loaded by the GPU loader (pars_dataset*): device arena +
+    offsets (dev_text / dev_offsets for pars_dev_score_text), host exports."""
+
+    def __init__(self, handle: int):
+        L = lib()
+        self.h = handle
+        self.n = L.pars_dataset_size(C.c_void_p(handle))
+        self.embedding_dim = L.pars_dataset_embedding_dim(C.c_void_p(handle))
+
+    def __len__(self):
+        return self.n
+
+    @property
+    def dev_text(self) -> int:
+        return lib().pars_dataset_dev_text(C.c_void_p(self.h)) or 0
+
+    @property
+    def dev_offsets(self) -> int:
+        return lib().pars_dataset_dev_offsets(C.c_void_p(self.h)) or 0
+
+    def export(self):
+        """(text uint8, offsets int64[n+1], output_len, prompt_len, ids list)"""
+        L, hv = lib(), C.c_void_p(self.h)
+        text = np.zeros(max(1, L.pars_dataset_text_bytes(hv)), np.uint8)
+        idb = np.zeros(max(1, L.pars_dataset_id_bytes(hv)), np.uint8)
+        offs = np.zeros(self.n + 1, np.int64)
+        ido = np.zeros(self.n + 1, np.int64)
+        ol = np.zeros(max(1, self.n), np.int64)
+        pl = np.zeros(max(1, self.n), np.int64)
+        _check(L.pars_dataset_export(hv, _p(text), _p(offs), _p(ol), _p(pl), _p(idb), _p(ido)))
+        ids = [idb[ido[i]:ido[i + 1]].tobytes().decode("utf-8", "surrogateescape")
+               for i in range(self.n)]
+        return text[:offs[-1]], offs, ol[:self.n], pl[:self.n], ids
+
+    def samples(self, i: int):
+        out = np.zeros(4096, np.int64)
+        k = lib().pars_dataset_samples(C.c_void_p(self.h), i, _p(out), 4096)
+        return out[:k].tolist()
+
+    def free(self):
+        if self.h:
+            lib().pars_dataset_free(C.c_void_p(self.h))
+            self.h = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class PairPlan:
     """Per-dataset plan of the length-sorted all-pairs kernel (pars_pair_plan*)."""
 
@@ -436,6 +500,18 @@ class Context:
                                         0 if algo == "sorted" else 1, _p(c), C.byref(kept),
                                         C.byref(act), C.byref(loss)))
         return c, kept.value, act.value, loss.value
+
+    def load_dataset(self, path, limit: int = -1) -> "GpuDataset":
+        """load_dataset (dataset.cpp:73-173) with the records parsed on the GPU."""
+        h = C.c_void_p()
+        _check(lib().pars_load_dataset(self.h, str(path).encode(), limit, C.byref(h)))
+        return GpuDataset(h.value)
+
+    def load_dataset_bytes(self, data: bytes, path: str = "<bytes>", limit: int = -1) -> "GpuDataset":
+        h = C.c_void_p()
+        _check(lib().pars_load_dataset_bytes(self.h, path.encode(), data, len(data), limit,
+                                             C.byref(h)))
+        return GpuDataset(h.value)
 
     def pair_plan(self, lengths, delta: float = 0.2) -> "PairPlan":
         return PairPlan(self, lengths, delta)

@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "featurize.cuh"
 #include "pairs.cuh"
+#include "ingest.cuh"
+#include "ingest_host.hpp"
 #include "sgd_cluster.cuh"
 
 namespace pars_b200 {
@@ -1432,6 +1434,296 @@ int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
   const double tau = (static_cast<double>(c[0]) - static_cast<double>(c[1])) / denom;
   *tau_b = std::clamp(tau, -1.0, 1.0);
   return PARS_OK;
+}
+
+}  // extern "C"
+
+// ---- dataset ingestion (load_dataset, dataset.cpp:73-173) -----------------
+
+struct pars_dataset {
+  pars_ctx* ctx = nullptr;
+  int device = 0;
+  int64_t n = 0, text_bytes = 0, id_bytes = 0, embedding_dim = 0;
+  uint8_t* d_text = nullptr;     // decoded prompts, concatenated
+  int64_t* d_offsets = nullptr;  // [n+1]
+  uint8_t* d_ids = nullptr;
+  int64_t* d_id_offsets = nullptr;
+  int64_t* d_output_len = nullptr;
+  int64_t* d_prompt_len = nullptr;
+  std::vector<int64_t> samples_rp, samples;  // host CSR of output_len_samples
+};
+
+namespace {
+using namespace pars_b200;
+
+int ds_fail(const char* path, int64_t line, const std::string& msg) {
+  set_error("%s: line %lld: %s", path, (long long)line, msg.c_str());
+  return PARS_ERR_INVALID;
+}
+}  // namespace
+
+extern "C" {
+
+int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, int64_t nbytes,
+                            int64_t limit, pars_dataset** out) {
+  *out = nullptr;
+  PARS_TRY(check_ctx(ctx));
+  if (!path) path = "<bytes>";
+  if (nbytes <= 0) {
+    set_error("%s: empty file, missing header", path);
+    return PARS_ERR_INVALID;
+  }
+  // header line (host): the reference's checks with the same JSON library
+  const char* nlp = static_cast<const char*>(std::memchr(bytes, '\n', (size_t)nbytes));
+  const int64_t hlen = nlp ? (int64_t)(nlp - bytes) : nbytes;
+  int64_t emb_dim = 0;
+  const std::string herr = ingest_header_error(std::string(bytes, (size_t)hlen), &emb_dim);
+  if (!herr.empty()) return ds_fail(path, 1, herr);
+  const char* body = nlp ? nlp + 1 : bytes + nbytes;
+  const int64_t nb = nbytes - (int64_t)(body - bytes);
+  if (limit < 0) limit = INT64_MAX;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  auto* d = new pars_dataset();
+  d->ctx = ctx;
+  d->device = ctx->device;
+  d->embedding_dim = emb_dim;
+  std::vector<void*> tmp;  // per-call device scratch, released at the end
+  auto talloc = [&](size_t sz) -> void* {
+    void* p = nullptr;
+    if (!pool_alloc(ctx, &p, std::max<size_t>(sz, 16))) return nullptr;
+    tmp.push_back(p);
+    return p;
+  };
+  auto done = [&](int rc) {
+    for (void* p : tmp) pool_free(ctx, p);
+    if (rc != PARS_OK) {
+      pars_dataset_free(d);
+    } else {
+      *out = d;
+    }
+    return rc;
+  };
+  auto oom = [&]() {
+    set_error("device allocation failed (dataset loader)");
+    return done(PARS_ERR_OOM);
+  };
+#define DS_CUDA(x)                                                            \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) {                                                  \
+      set_error("CUDA error in the dataset loader: %s", cudaGetErrorString(e_)); \
+      return done(PARS_ERR_CUDA);                                             \
+    }                                                                         \
+  } while (0)
+  // 1. lines of the body
+  int64_t nrec = 0, nlines = 0;
+  uint8_t* d_body = nullptr;
+  int64_t* d_nl = nullptr;
+  if (nb > 0) {
+    d_body = (uint8_t*)talloc((size_t)nb);
+    const int64_t nblk = ingest_block_count(nb);
+    uint32_t* d_blk = (uint32_t*)talloc((size_t)(nblk + 1) * 4);
+    if (!d_body || !d_blk) return oom();
+    DS_CUDA(cudaMemcpyAsync(d_body, body, (size_t)nb, cudaMemcpyHostToDevice, st));
+    int64_t nlc = 0;
+    if (ingest_count_newlines(d_body, nb, d_blk, &nlc, st) != PARS_OK) return done(PARS_ERR_CUDA);
+    nlines = nlc + 1;  // the segment after the last '\n' (empty when the file ends with one)
+    d_nl = (int64_t*)talloc((size_t)nlines * 8);
+    if (!d_nl) return oom();
+    ingest_write_newlines(d_body, nb, d_blk, d_nl, st);
+    DS_CUDA(cudaMemcpyAsync(d_nl + nlc, &nb, 8, cudaMemcpyHostToDevice, st));
+    // 2. non-empty lines, ranked, truncated to `limit`
+    uint32_t* d_rank = (uint32_t*)talloc((size_t)(nlines + 1) * 4);
+    if (!d_rank) return oom();
+    ingest_launch_line_flags(d_nl, nlines, nb, d_rank, st);
+    ingest_launch_scan(d_rank, nlines, st);
+    uint32_t total = 0;
+    DS_CUDA(cudaMemcpyAsync(&total, d_rank + nlines, 4, cudaMemcpyDeviceToHost, st));
+    DS_CUDA(cudaStreamSynchronize(st));
+    nrec = std::min<int64_t>(total, limit);
+    if (nrec > 0) {
+      int64_t* d_rb = (int64_t*)talloc((size_t)nrec * 8);
+      int64_t* d_re = (int64_t*)talloc((size_t)nrec * 8);
+      int64_t* d_rl = (int64_t*)talloc((size_t)nrec * 8);
+      if (!d_rb || !d_re || !d_rl) return oom();
+      ingest_launch_record_lines(d_nl, nlines, nb, d_rank, nrec, d_rb, d_re, d_rl, st);
+      // 3. parse + validate every record line
+      RecordOut R;
+      R.err = (uint32_t*)talloc((size_t)nrec * 4);
+      R.flags = (uint32_t*)talloc((size_t)nrec * 4);
+      int64_t** i64s[] = {&R.id_b, &R.id_e, &R.id_len, &R.pr_b, &R.pr_e, &R.pr_len,
+                          &R.out_len, &R.prompt_len, &R.sm_b, &R.sm_e};
+      for (int64_t** q : i64s) {
+        *q = (int64_t*)talloc((size_t)nrec * 8);
+        if (!*q) return oom();
+      }
+      if (!R.err || !R.flags) return oom();
+      ingest_launch_parse(d_body, d_rb, d_re, nrec, R, st);
+      // 4. arenas: decoded lengths -> offsets
+      int64_t* d_pro = nullptr;
+      int64_t* d_ido = nullptr;
+      if (!pool_alloc(ctx, (void**)&d->d_offsets, (size_t)(nrec + 1) * 8) ||
+          !pool_alloc(ctx, (void**)&d->d_id_offsets, (size_t)(nrec + 1) * 8) ||
+          !pool_alloc(ctx, (void**)&d->d_output_len, (size_t)nrec * 8) ||
+          !pool_alloc(ctx, (void**)&d->d_prompt_len, (size_t)nrec * 8))
+        return oom();
+      d_pro = d->d_offsets;
+      d_ido = d->d_id_offsets;
+      ingest_launch_lengths(nrec, R, d_pro, d_ido, st);
+      ingest_launch_scan_i64(d_pro, nrec, st);
+      ingest_launch_scan_i64(d_ido, nrec, st);
+      int64_t tot[2] = {0, 0};
+      DS_CUDA(cudaMemcpyAsync(&tot[0], d_pro + nrec, 8, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaMemcpyAsync(&tot[1], d_ido + nrec, 8, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      d->text_bytes = tot[0];
+      d->id_bytes = tot[1];
+      if (!pool_alloc(ctx, (void**)&d->d_text, (size_t)tot[0] + 16) ||
+          !pool_alloc(ctx, (void**)&d->d_ids, (size_t)tot[1] + 16))
+        return oom();
+      ingest_launch_emit(d_body, nrec, R, d_pro, d->d_text, d_ido, d->d_ids, d->d_prompt_len, st);
+      // 5. duplicates, medians, and the first failing record
+      uint64_t cap = 1024;
+      while (cap < (uint64_t)nrec * 2) cap <<= 1;
+      uint64_t* d_hash = (uint64_t*)talloc((size_t)nrec * 8);
+      unsigned long long* d_tkey = (unsigned long long*)talloc((size_t)cap * 8);
+      unsigned long long* d_tmin = (unsigned long long*)talloc((size_t)cap * 8);
+      uint32_t* d_dup = (uint32_t*)talloc((size_t)nrec * 4);
+      uint32_t* d_mis = (uint32_t*)talloc((size_t)nrec * 4);
+      uint32_t* d_uns = (uint32_t*)talloc((size_t)nrec * 4);
+      unsigned long long* d_first = (unsigned long long*)talloc(8);
+      if (!d_hash || !d_tkey || !d_tmin || !d_dup || !d_mis || !d_uns || !d_first) return oom();
+      DS_CUDA(cudaMemsetAsync(d_tkey, 0, (size_t)cap * 8, st));
+      DS_CUDA(cudaMemsetAsync(d_tmin, 0xff, (size_t)cap * 8, st));
+      DS_CUDA(cudaMemsetAsync(d_dup, 0, (size_t)nrec * 4, st));
+      DS_CUDA(cudaMemsetAsync(d_mis, 0, (size_t)nrec * 4, st));
+      DS_CUDA(cudaMemsetAsync(d_uns, 0, (size_t)nrec * 4, st));
+      DS_CUDA(cudaMemsetAsync(d_first, 0xff, 8, st));
+      ingest_launch_dups(d->d_ids, d_ido, nrec, d_hash, cap, d_tkey, d_tmin, d_dup, st);
+      ingest_launch_samples(d_body, nrec, R, d_mis, d_uns, st);
+      ingest_launch_first_fail(nrec, R, d_dup, d_mis, d_uns, d->d_prompt_len, d_first, st);
+      DS_CUDA(cudaMemcpyAsync(d->d_output_len, R.out_len, (size_t)nrec * 8, cudaMemcpyDeviceToDevice, st));
+      unsigned long long first = 0;
+      DS_CUDA(cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      count_launch(ctx, 14);
+      if (first != ~0ull) {
+        // the reference stops at this line: its message, re-derived on the host
+        int64_t b = 0, e = 0, ln = 0;
+        uint32_t dup = 0;
+        DS_CUDA(cudaMemcpy(&b, d_rb + first, 8, cudaMemcpyDeviceToHost));
+        DS_CUDA(cudaMemcpy(&e, d_re + first, 8, cudaMemcpyDeviceToHost));
+        DS_CUDA(cudaMemcpy(&ln, d_rl + first, 8, cudaMemcpyDeviceToHost));
+        DS_CUDA(cudaMemcpy(&dup, d_dup + first, 4, cudaMemcpyDeviceToHost));
+        bool has_emb = false;
+        const std::string msg =
+            ingest_record_error(std::string(body + b, (size_t)(e - b)), dup != 0, emb_dim, &has_emb);
+        if (!msg.empty()) {
+          ds_fail(path, ln + 2, msg);
+          return done(PARS_ERR_INVALID);
+        }
+        set_error("%s: line %lld: the GPU dataset loader does not parse %s", path,
+                  (long long)(ln + 2),
+                  has_emb ? "'embedding' arrays" : "more than 256 output_len_samples");
+        return done(PARS_ERR_UNSUPPORTED);
+      }
+      // output_len_samples (host CSR, for export)
+      d->samples_rp.assign((size_t)nrec + 1, 0);
+      std::vector<uint32_t> fl((size_t)nrec);
+      DS_CUDA(cudaMemcpy(fl.data(), R.flags, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+      bool any = false;
+      for (uint32_t f : fl) any = any || (f & kIngHasSamples);
+      if (any) {
+        std::vector<int64_t> sb((size_t)nrec), se((size_t)nrec);
+        DS_CUDA(cudaMemcpy(sb.data(), R.sm_b, (size_t)nrec * 8, cudaMemcpyDeviceToHost));
+        DS_CUDA(cudaMemcpy(se.data(), R.sm_e, (size_t)nrec * 8, cudaMemcpyDeviceToHost));
+        for (int64_t r = 0; r < nrec; ++r) {
+          if (fl[r] & kIngHasSamples) {
+            const std::vector<int64_t> v =
+                ingest_parse_samples(std::string(body + sb[r], (size_t)(se[r] - sb[r])));
+            d->samples.insert(d->samples.end(), v.begin(), v.end());
+          }
+          d->samples_rp[r + 1] = (int64_t)d->samples.size();
+        }
+      }
+    }
+  }
+#undef DS_CUDA
+  d->n = nrec;
+  if (nrec == 0) {
+    if (!pool_alloc(ctx, (void**)&d->d_offsets, 8) || !pool_alloc(ctx, (void**)&d->d_id_offsets, 8))
+      return oom();
+    cudaMemsetAsync(d->d_offsets, 0, 8, st);
+    cudaMemsetAsync(d->d_id_offsets, 0, 8, st);
+    d->samples_rp.assign(1, 0);
+  }
+  cudaStreamSynchronize(st);
+  return done(PARS_OK);
+}
+
+int pars_load_dataset(pars_ctx* ctx, const char* path, int64_t limit, pars_dataset** out) {
+  *out = nullptr;
+  FILE* f = std::fopen(path, "rb");
+  if (!f) {
+    set_error("cannot open dataset file '%s'", path);
+    return PARS_ERR_INVALID;
+  }
+  std::fseek(f, 0, SEEK_END);
+  const long sz = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  void* buf = nullptr;
+  if (cudaHostAlloc(&buf, (size_t)std::max<long>(sz, 1), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    std::fclose(f);
+    set_error("pinned host allocation of %ld bytes failed", sz);
+    return PARS_ERR_OOM;
+  }
+  const size_t got = std::fread(buf, 1, (size_t)std::max<long>(sz, 0), f);
+  std::fclose(f);
+  const int rc = pars_load_dataset_bytes(ctx, path, static_cast<const char*>(buf), (int64_t)got, limit, out);
+  cudaFreeHost(buf);
+  return rc;
+}
+
+int64_t pars_dataset_size(const pars_dataset* d) { return d ? d->n : 0; }
+int64_t pars_dataset_text_bytes(const pars_dataset* d) { return d ? d->text_bytes : 0; }
+int64_t pars_dataset_embedding_dim(const pars_dataset* d) { return d ? d->embedding_dim : 0; }
+const char* pars_dataset_dev_text(const pars_dataset* d) { return (const char*)d->d_text; }
+const int64_t* pars_dataset_dev_offsets(const pars_dataset* d) { return d->d_offsets; }
+const int64_t* pars_dataset_dev_output_len(const pars_dataset* d) { return d->d_output_len; }
+
+int pars_dataset_export(const pars_dataset* d, char* text, int64_t* offsets, int64_t* output_len,
+                        int64_t* prompt_len, char* ids, int64_t* id_offsets) {
+  cudaSetDevice(d->device);
+  const int64_t n = d->n;
+  if (text && d->text_bytes)
+    PARS_CUDA_CHECK(cudaMemcpy(text, d->d_text, (size_t)d->text_bytes, cudaMemcpyDeviceToHost));
+  if (offsets) PARS_CUDA_CHECK(cudaMemcpy(offsets, d->d_offsets, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost));
+  if (output_len && n)
+    PARS_CUDA_CHECK(cudaMemcpy(output_len, d->d_output_len, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  if (prompt_len && n)
+    PARS_CUDA_CHECK(cudaMemcpy(prompt_len, d->d_prompt_len, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  if (ids && d->id_bytes) PARS_CUDA_CHECK(cudaMemcpy(ids, d->d_ids, (size_t)d->id_bytes, cudaMemcpyDeviceToHost));
+  if (id_offsets)
+    PARS_CUDA_CHECK(cudaMemcpy(id_offsets, d->d_id_offsets, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost));
+  return PARS_OK;
+}
+
+int64_t pars_dataset_id_bytes(const pars_dataset* d) { return d ? d->id_bytes : 0; }
+
+int64_t pars_dataset_samples(const pars_dataset* d, int64_t i, int64_t* out, int64_t cap) {
+  const int64_t b = d->samples_rp[i], e = d->samples_rp[i + 1];
+  if (e - b > cap) return -1;
+  for (int64_t k = b; k < e; ++k) out[k - b] = d->samples[k];
+  return e - b;
+}
+
+void pars_dataset_free(pars_dataset* d) {
+  if (!d) return;
+  void* ptrs[] = {d->d_text, d->d_offsets, d->d_ids, d->d_id_offsets, d->d_output_len, d->d_prompt_len};
+  pool_release(d->device, ptrs, 6);
+  delete d;
 }
 
 }  // extern "C"

@@ -85,7 +85,7 @@ def _gpu_tiles(ctx, d_scores, d_lengths, n, delta, margin, max_len, stream, plan
                                          margin, max_len, t0, t1, c.data_ptr(), cnt.data_ptr(),
                                          part.data_ptr(), stream)
             if rc != 0:
-                raise ParsError(rc, lib().pars_last_error().decode())
+                raise ParsError(rc, lib().pars_last_error().decode("utf-8", "replace"))
         return c, cnt[:2], part[: max(0, t1 - t0)]
 
     return run
@@ -139,7 +139,7 @@ def grad_step_gpu(ctx, feats, d_coeff, scale: float, group=None, stream: int = 0
     rc = lib().pars_dev_xt_c(ctx.h, C.c_void_p(feats.h), d_coeff.data_ptr(), r0, r1, g.data_ptr(),
                              stream or None)
     if rc != 0:
-        raise ParsError(rc, lib().pars_last_error().decode())
+        raise ParsError(rc, lib().pars_last_error().decode("utf-8", "replace"))
     if world > 1:
         dist.all_reduce(g, group=group)
     return g * scale
@@ -190,7 +190,7 @@ def train_step_gpu(ctx, feats, d_w, scores_pad, d_lengths, n: int, delta: float,
 
     def check(rc):
         if rc != 0:
-            raise ParsError(rc, lib().pars_last_error().decode())
+            raise ParsError(rc, lib().pars_last_error().decode("utf-8", "replace"))
 
     def score_rows(r0, r1, out):
         # the kernel writes d_scores[r0:r1]; point it so that lands in out

@@ -14,6 +14,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:feat
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:allpairs -s 1 -c 1 \
   -o $OUT/pairs_full -f python bench.py --prompts 20000 --steps 1 --warmup 3 --no-cpu --no-e2e \
   --no-configs > $OUT/ncu_pairs.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dense_exact -s 1 -c 1 \
+  -o $OUT/dense_full -f python bench.py --prompts 20000 --steps 1 --warmup 3 --no-cpu --no-pairs \
+  --no-e2e > $OUT/ncu_dense.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 \
   > $OUT/ncu_launches.log 2>&1
