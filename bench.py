@@ -355,6 +355,8 @@ def run_ours(args):
     embed = None
     if world == 1 and not args.no_configs:
         embed = bench_embeddings(P, ctx, torch, dev, stream, args)
+        if configs is not None:
+            configs["ingest_c4"] = bench_ingest(P, ctx, torch, dev, stream, wl, w, args)
 
     line = None
     if rank == 0:
@@ -536,6 +538,87 @@ def bench_embeddings(P, ctx, torch, dev, stream, args):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "algorithmic_bytes_per_launch": alg,
                          "note": "exact mode reads the rows twice (norm chain, then dot chain)"}}
+
+
+def bench_ingest(P, ctx, torch, dev, stream, wl, w, args):
+    """From JSONL bytes to the SJF order: the C4 workload written as a
+    pars.dataset file (1M records, ~2.2 GB), loaded by the GPU loader
+    (pars_load_dataset_bytes: H2D of the bytes, line split, JSON validation,
+    decoded prompt arena), scored and ordered on the device. Beside it the
+    reference's load_dataset + score_batch + select_batch on the first 100k
+    records of the same file (bounded sample)."""
+    import ctypes as C
+    import tempfile
+    n = len(wl)
+    head = b'{"embedding_dim":0,"format":"pars.dataset","version":1}\n'
+    parts = [head]
+    for i in range(n):
+        parts.append(b'{"id":"p%07d","output_len":%d,"prompt":"' % (i, int(wl.output_len[i])))
+        parts.append(wl.text[wl.offsets[i]:wl.offsets[i + 1]].tobytes())
+        parts.append(b'"}\n')
+    blob = b"".join(parts)
+    nbytes = len(blob)
+    hb = C.c_void_p()
+    if P.lib().pars_host_alloc(nbytes, C.byref(hb)) != 0:
+        raise MemoryError("pinned host allocation failed")
+    host = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(hb.value))
+    host[:] = np.frombuffer(blob, np.uint8)
+    del blob, parts
+    L = P.lib()
+    ex = P.Extractor.make()
+    d_w = torch.from_numpy(w).to(dev)
+    d_s = torch.empty(n, dtype=torch.float64, device=dev)
+    d_tie = torch.arange(n, dtype=torch.int32, device=dev)
+    d_o = torch.empty(n, dtype=torch.int32, device=dev)
+    sh = stream.cuda_stream
+
+    def step():
+        h = C.c_void_p()
+        rc = L.pars_load_dataset_bytes(ctx.h, b"c4.jsonl", C.c_char_p(hb.value), nbytes, -1, C.byref(h))
+        if rc != 0:
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+        g = P._lib.GpuDataset(h.value)
+        L.pars_dev_score_text(ctx.h, C.byref(ex), g.dev_text, g.dev_offsets, len(g), d_w.data_ptr(),
+                              0.0, P.MODE_EXACT, d_s.data_ptr(), sh)
+        L.pars_dev_priority_order(ctx.h, d_s.data_ptr(), None, d_tie.data_ptr(), len(g),
+                                  d_o.data_ptr(), sh)
+        torch.cuda.synchronize()
+        g.free()
+
+    step()
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    out = {"workload": "C4 as a pars.dataset JSONL (%d records, %.2f GB): GPU load "
+                       "(pars_load_dataset_bytes, bytes in pinned host memory) + score + SJF order"
+                       % (n, nbytes / 1e9),
+           "gpu_s": t, "gpu_records_per_s": n / t}
+    if not args.no_cpu:
+        from oracle.bind import Extractor as OEx
+        from oracle.bind import Ref
+        R = Ref()
+        R.set_threads(host_threads())
+        path = tempfile.mktemp(suffix=".jsonl")
+        sample = 100_000
+        with open(path, "wb") as f:
+            f.write(host.tobytes())
+        t0 = time.perf_counter()
+        ds = R.load_dataset(path, sample)
+        t_load = time.perf_counter() - t0
+        rs = R.score_batch(OEx.make(), ds, w)
+        R.select_batch(np.zeros(len(ds)), ["p%07d" % i for i in range(len(ds))], rs,
+                       np.zeros(len(ds), np.uint8), 0.0, len(ds))
+        t_all = time.perf_counter() - t0
+        os.unlink(path)
+        out.update({"cpu_records_per_s": sample / t_all, "cpu_load_s": t_load, "cpu_total_s": t_all,
+                    "cpu_sample": "first %d records: load_dataset (1 thread, as the reference) + "
+                                  "score_batch (OpenMP %d threads) + select_batch"
+                                  % (sample, host_threads())})
+    P.lib().pars_host_free(hb)
+    return out
 
 
 def fnv64(a: np.ndarray) -> str:
