@@ -352,6 +352,9 @@ def run_ours(args):
     pairs = None
     if not args.no_pairs:
         pairs = bench_pairs(P, ctx, torch, dev, stream, world, rank, args)
+    tau = None
+    if not args.no_pairs:
+        tau = bench_tau(P, ctx, torch, dev, stream, world, rank, args)
     embed = None
     if world == 1 and not args.no_configs:
         embed = bench_embeddings(P, ctx, torch, dev, stream, args)
@@ -391,6 +394,7 @@ def run_ours(args):
             "clocks": clk,
             "parity": {"scores_bitexact_sample": parity_ok, "sample": chk},
             "pairs": pairs,
+            "kendall_tau": tau,
             "embeddings": embed,
             "configs": configs,
             "workload_gen_s": t_gen,
@@ -464,6 +468,47 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
                         "rank's tiles + all-reduce, X^T c + gradient all-reduce, SGD update",
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident",
             "roofline": pairs_roofline(ms)}
+
+
+def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
+    """Kendall tau-b counts (metrics.cpp:42-64) at compare_policies scale: the
+    PARS scores vs output lengths of 100,000 requests (C3-sized trace), all
+    4,999,950,000 pairs, tiles split over ranks + one exact all-reduce."""
+    from paper_2510_03243_b200 import distributed as D
+    n = 100_000
+    wl = P.Workload.synthesize(n, 23)
+    w = np.random.default_rng(5).normal(size=DIM) * 0.05
+    s = ctx.score_text(P.Extractor.make(), wl.text, wl.offsets, w)
+    y = wl.output_len.astype(np.float64)
+    dx, dy = torch.from_numpy(s).to(dev), torch.from_numpy(y).to(dev)
+    sh = stream.cuda_stream
+    for _ in range(2):
+        tau, c = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
+    torch.cuda.synchronize()
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(3, args.steps)
+    a.record(stream)
+    for _ in range(k):
+        tau, c = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = barrier_max(world, a.elapsed_time(b)) / k
+    pairs = n * (n - 1) // 2
+    out = {"metric": "pairs/s", "value": pairs / (ms / 1e3), "ms_per_call": ms, "tau_b": tau,
+           "workload": "kendall_tau_b(scores, output_len) over 100,000 requests "
+                       "(4,999,950,000 pairs), exact integer counts"}
+    if world == 1 and not args.no_cpu:
+        from oracle.bind import Oracle
+        m = 30_000
+        t0 = time.perf_counter()
+        otau, oc = Oracle().kendall(s[:m], y[:m], threads=host_threads())
+        dt = time.perf_counter() - t0
+        gt, gc = D.kendall_tau_gpu(ctx, dx[:m].contiguous(), dy[:m].contiguous(), m, stream=sh)
+        out.update({"cpu_pairs_per_s": (m * (m - 1) // 2) / dt, "cpu_threads": host_threads(),
+                    "cpu_sample": "first %d requests (port of metrics.cpp, OpenMP)" % m,
+                    "sample_counts_match": bool((gc == oc).all()) and gt == otau})
+    return out
 
 
 def pairs_roofline(ms):

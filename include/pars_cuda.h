@@ -275,6 +275,17 @@ int pars_tie_ranks(const double* arrival, const char* ids,
  * with the reference's message. */
 int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y,
                      int64_t n, uint64_t* counts, double* tau_b);
+/* The same counts split over upper-triangle tiles (the all-pairs tiling):
+ * {n_c, n_d, n1, n2} of tiles [tile_begin, tile_end) ACCUMULATED into
+ * d_counts[4] on the device (for data-parallel ranks: sum the counts, an
+ * exact integer all-reduce), then pars_kendall_finish on the totals. */
+int64_t pars_kendall_tiles(int64_t n);
+int pars_dev_kendall_counts(pars_ctx* ctx, const double* d_x, const double* d_y,
+                            int64_t n, int64_t tile_begin, int64_t tile_end,
+                            unsigned long long* d_counts, void* stream);
+/* finish_tau (metrics.cpp:13-32): counts5 = {n_c, n_d, n0, n1, n2}. */
+int pars_kendall_finish(const uint64_t* counts4, int64_t n, uint64_t* counts5,
+                        double* tau_b);
 
 /* ---- synthetic workloads (host; dataset.cpp:204-297 restated) ----------
  * synthesize_dataset(n, lognormal(mu, sigma), seed) with the reference's

@@ -82,6 +82,9 @@ def _load() -> C.CDLL:
         "pars_dev_score_text": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
         "pars_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
         "pars_dev_score_embeddings": (C.c_int, [vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp]),
+        "pars_kendall_tiles": (i64, [i64]),
+        "pars_dev_kendall_counts": (C.c_int, [vp, vp, vp, i64, i64, i64, vp, vp]),
+        "pars_kendall_finish": (C.c_int, [vp, i64, vp, vp]),
         "pars_load_dataset": (C.c_int, [vp, C.c_char_p, i64, vp]),
         "pars_load_dataset_bytes": (C.c_int, [vp, C.c_char_p, C.c_char_p, i64, i64, vp]),
         "pars_dataset_size": (i64, [vp]),

@@ -1415,13 +1415,18 @@ int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
   unsigned long long c[4];
   PARS_CUDA_CHECK(cudaMemcpyAsync(c, d_c, 32, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  const uint64_t c4[4] = {c[0], c[1], c[2], c[3]};
+  return pars_kendall_finish(c4, n, counts, tau_b);
+}
+
+// finish_tau (metrics.cpp:13-32) on counts {n_c, n_d, n1, n2} of all pairs
+int pars_kendall_finish(const uint64_t* c, int64_t n, uint64_t* counts, double* tau_b) {
   const uint64_t n0 = (uint64_t)n * (uint64_t)(n - 1) / 2;
   counts[0] = c[0];
   counts[1] = c[1];
   counts[2] = n0;
   counts[3] = c[2];
   counts[4] = c[3];
-  // finish_tau (metrics.cpp:13-32)
   if (c[2] == n0) {
     set_error("degenerate ranking: all values tied in first argument");
     return PARS_ERR_INVALID;
@@ -1434,6 +1439,17 @@ int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
   const double tau = (static_cast<double>(c[0]) - static_cast<double>(c[1])) / denom;
   *tau_b = std::clamp(tau, -1.0, 1.0);
   return PARS_OK;
+}
+
+int64_t pars_kendall_tiles(int64_t n) { return allpairs_tile_count(n); }
+
+int pars_dev_kendall_counts(pars_ctx* ctx, const double* d_x, const double* d_y, int64_t n,
+                            int64_t tile_begin, int64_t tile_end, unsigned long long* d_counts,
+                            void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  if (n < 2) return PARS_OK;
+  Guard g(ctx);
+  return launch_tau(ctx, d_x, d_y, n, d_counts, pick(ctx, stream), tile_begin, tile_end);
 }
 
 }  // extern "C"

@@ -126,13 +126,13 @@ __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, dou
 // Kendall tau-b counts (metrics.cpp:47-62): n_c, n_d, n1 (ties in x), n2.
 __global__ void __launch_bounds__(kTile) tau_kernel(const double* __restrict__ x,
                                                     const double* __restrict__ y, int64_t n,
-                                                    int64_t nt, int64_t ntiles,
+                                                    int64_t nt, int64_t t0, int64_t t1,
                                                     unsigned long long* __restrict__ out) {
   __shared__ double sx[kTile], sy[kTile];
   __shared__ unsigned long long red[kTile / 32];
   const int tid = threadIdx.x;
   unsigned long long nc = 0, nd = 0, n1 = 0, n2 = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (int64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
     int64_t I, J;
     tile_of(t, nt, &I, &J);
     const int64_t gi = I * kTile + tid;
@@ -331,11 +331,14 @@ int launch_sum_partials(pars_ctx* ctx, const double* p, int64_t n, double* out, 
 }
 
 int launch_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
-               unsigned long long* out, cudaStream_t st) {
+               unsigned long long* out, cudaStream_t st, int64_t t0, int64_t t1) {
   const int64_t nt = ceil_div(n, kTile);
   const int64_t tiles = nt * (nt + 1) / 2;
-  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sms_of_current() * 8);
-  tau_kernel<<<(unsigned)grid, kTile, 0, st>>>(x, y, n, nt, tiles, out);
+  if (t1 < 0 || t1 > tiles) t1 = tiles;
+  t0 = std::max<int64_t>(0, t0);
+  if (t1 <= t0) return PARS_OK;
+  const int64_t grid = std::min<int64_t>(t1 - t0, (int64_t)sms_of_current() * 8);
+  tau_kernel<<<(unsigned)grid, kTile, 0, st>>>(x, y, n, nt, t0, t1, out);
   count_launch(ctx);
   PARS_CUDA_CHECK(cudaGetLastError());
   return PARS_OK;

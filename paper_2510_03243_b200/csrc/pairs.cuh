@@ -13,8 +13,10 @@ int launch_allpairs(pars_ctx* ctx, const double* s, const int32_t* L, const int3
                     int64_t n, double margin, int64_t t0, int64_t t1, int32_t* coeff,
                     unsigned long long* counters, double* loss_part, cudaStream_t st);
 int launch_sum_partials(pars_ctx* ctx, const double* p, int64_t n, double* out, cudaStream_t st);
+// Kendall counts {n_c, n_d, n1, n2} of the upper-triangle tiles [t0, t1)
+// (t1 < 0: all), accumulated into out[4]
 int launch_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
-               unsigned long long* out, cudaStream_t st);
+               unsigned long long* out, cudaStream_t st, int64_t t0 = 0, int64_t t1 = -1);
 // Column-major copy of a CSR feature set (stable: rows ascending within a
 // column) and the per-step gradient X[r0:r1]^T c over it.
 size_t csc_scratch_bytes(int64_t rows, uint32_t dim);

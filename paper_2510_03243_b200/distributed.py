@@ -14,6 +14,9 @@ Only the paths that shard naturally are partitioned:
 * full-batch step: grad = X^T c over each rank's row shard, all-reduced
   (D doubles), then the update.
 
+`kendall_tau_dp` splits kendall_tau_b's O(n^2) pair counts over the same
+upper-triangle tiles; the exchange is one all-reduce of 4 integer counts.
+
 `train_step` is the whole C5 data-parallel step — score this rank's prompt
 shard with the current weights, all-gather the scores, the rank's all-pairs
 tiles, the coefficient all-reduce, X^T c on the row shard, the gradient
@@ -210,3 +213,44 @@ def train_step_gpu(ctx, feats, d_w, scores_pad, d_lengths, n: int, delta: float,
         return g
 
     return train_step(n, d_w, scores_pad, score_rows, tiles, xt_c, lr_over_kept, group)
+
+
+def kendall_tau_dp(n: int, counts: Callable, finish: Callable, group=None):
+    """kendall_tau_b (metrics.cpp:42-64) over n items with the pair tiles split
+    across ranks: counts(t0, t1) -> int64[4] {n_c, n_d, n1, n2} of this rank's
+    tiles; one exact all-reduce; finish(totals) -> (tau_b, counts5)."""
+    dist = _dist()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    t0, t1 = tile_range(n, world, rank)
+    c = counts(t0, t1)
+    if world > 1:
+        dist.all_reduce(c, group=group)
+    return finish(c)
+
+
+def kendall_tau_gpu(ctx, d_x, d_y, n: int, stream: int = 0, group=None):
+    """kendall_tau_dp with the CUDA tile kernel (pars_dev_kendall_counts) and
+    the reference's finish_tau (pars_kendall_finish)."""
+    import numpy as np
+    import torch
+    from ._lib import ParsError, lib
+
+    def counts(t0, t1):
+        c = torch.zeros(4, dtype=torch.int64, device=d_x.device)
+        rc = lib().pars_dev_kendall_counts(ctx.h, d_x.data_ptr(), d_y.data_ptr(), n, t0, t1,
+                                           c.data_ptr(), stream or None)
+        if rc != 0:
+            raise ParsError(rc, lib().pars_last_error().decode("utf-8", "replace"))
+        return c
+
+    def finish(c):
+        c4 = np.ascontiguousarray(c.cpu().numpy().astype(np.uint64))
+        c5 = np.zeros(5, np.uint64)
+        tau = C.c_double()
+        rc = lib().pars_kendall_finish(c4.ctypes.data, n, c5.ctypes.data, C.byref(tau))
+        if rc != 0:
+            raise ParsError(rc, lib().pars_last_error().decode("utf-8", "replace"))
+        return tau.value, c5
+
+    return kendall_tau_dp(n, counts, finish, group)

@@ -171,3 +171,55 @@ def test_train_step_gloo_matches_single_process():
         assert cnt == cnt1.numpy().tolist()
         np.testing.assert_allclose(sc, X @ w0, rtol=1e-13, atol=1e-14)
         np.testing.assert_allclose(w, w1.numpy(), rtol=1e-12, atol=1e-15)
+
+
+def _tau_counts_numpy(x, y):
+    """Per-tile Kendall counts with the kernel's contract (pairs.cu tau_kernel)."""
+    n = len(x)
+
+    def run(t0, t1):
+        nc = nd = n1 = n2 = 0
+        for t in range(t0, t1):
+            I, J = D.tile_coords(t, n)
+            for i in range(I * D.TILE, min(n, (I + 1) * D.TILE)):
+                for j in range(J * D.TILE, min(n, (J + 1) * D.TILE)):
+                    if I == J and j <= i:
+                        continue
+                    dx, dy = x[i] - x[j], y[i] - y[j]
+                    n1 += dx == 0
+                    n2 += dy == 0
+                    if dx != 0 and dy != 0:
+                        if (dx > 0) == (dy > 0):
+                            nc += 1
+                        else:
+                            nd += 1
+        return torch.tensor([nc, nd, n1, n2], dtype=torch.int64)
+
+    return run
+
+
+def _tau_worker(rank, world, port, x, y, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = D.kendall_tau_dp(len(x), _tau_counts_numpy(x, y), lambda t: t.numpy().tolist())
+        out[rank] = c
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kendall_tau_dp_gloo_matches_oracle(oracle):
+    """Tiles split over 2 ranks + one integer all-reduce = the reference's
+    counts (oracle kendall)."""
+    rng = np.random.default_rng(4)
+    n = 520
+    x = rng.integers(0, 40, n).astype(np.float64)
+    y = rng.integers(0, 30, n).astype(np.float64)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_tau_worker, args=(2, _free_port(), x, y, out), nprocs=2, join=True,
+                       start_method="fork")
+    single = D.kendall_tau_dp(n, _tau_counts_numpy(x, y), lambda t: t.numpy().tolist())
+    assert out[0] == out[1] == single
+    tau, counts = oracle.kendall(x, y)
+    assert single == [int(counts[0]), int(counts[1]), int(counts[3]), int(counts[4])]

@@ -447,3 +447,20 @@ def test_dev_features_score_compact_rows_bit_identical(ctx, oracle):
     want = oracle.score_batch(oex(e), wl.text, wl.offsets, w, 0.5)
     assert (out.cpu().numpy().view(np.uint64) == want.view(np.uint64)).all()
     f.free()
+
+
+def test_kendall_tau_tile_split_matches_single_call(ctx, oracle):
+    """pars_dev_kendall_counts over tile slices (as data-parallel ranks would
+    run them) sums to pars_kendall_tau's counts; the finish is finish_tau."""
+    import torch
+    from paper_2510_03243_b200 import distributed as D
+    rng = np.random.default_rng(8)
+    n = 3001
+    x = rng.integers(0, 100, n).astype(np.float64)
+    y = x * 0.5 + rng.integers(0, 60, n)
+    tau1, c1 = ctx.kendall_tau(x, y)
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    tau2, c2 = D.kendall_tau_gpu(ctx, dx, dy, n)
+    assert tau1 == tau2 and (c1 == c2).all()
+    otau, oc = oracle.kendall(x, y)
+    assert (c2 == oc).all() and tau2 == otau
