@@ -252,6 +252,48 @@ int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex,
                         double lr, uint64_t seed, uint64_t pairs_per_epoch,
                         double* w_out, double* bias_out, double* loss_trace);
 
+/* ---- comparison objectives (train.cpp:46-94, :168-205) -----------------
+ * The paper's baselines on the same engine. */
+#define PARS_OBJ_PAIRWISE 0
+#define PARS_OBJ_POINTWISE_L1 1
+#define PARS_OBJ_LISTMLE 2
+/* One PointwiseL1 epoch (train.cpp:168-183 with pointwise_l1_loss_grad
+ * :46-54 and apply :141-151): samples order[0..n) (rows of f), `batch` per
+ * step; target[f->rows] = pointwise_target(output_len) per row. w[dim] and
+ * *bias in/out; *epoch_loss = the sum of |r| (the caller divides by n).
+ * Bit-identical to the reference. */
+int pars_pointwise_epoch(pars_ctx* ctx, const pars_features* f,
+                         const uint32_t* order, int64_t n, const double* target,
+                         int32_t batch, double lr, double* w, double* bias,
+                         double* epoch_loss);
+/* One ListwiseListMLE epoch (train.cpp:185-205 with listmle_loss_grad
+ * :66-94): lists[nlists*k] rows, each list already longest-first
+ * (pars_listmle_lists), `batch` lists per step; bias is read, not trained.
+ * exp/log1p run in the CUDA libm (<= 1 ulp from glibc), so weights and loss
+ * match the reference to rounding (tests: 1e-12 relative), not bits. */
+int pars_listmle_epoch(pars_ctx* ctx, const pars_features* f,
+                       const uint32_t* lists, int64_t nlists, int32_t k,
+                       int32_t batch, double lr, double* w, double bias,
+                       double* epoch_loss);
+/* Host samplers (bit-identical): the PointwiseL1 epoch order (Rng(seed)
+ * shuffle of 0..n-1, train.cpp:169-172) and the ListMLE epoch lists
+ * (persistent-pool partial Fisher-Yates + sort_by_true_order,
+ * train.cpp:110-118, :186-200); lists[nlists * min(list_size, n)]. */
+int pars_pointwise_order(int64_t n, uint64_t seed, uint32_t* order);
+int pars_listmle_lists(const int64_t* output_len, const char* ids,
+                       const int64_t* id_offsets, int64_t n, int64_t nlists,
+                       int32_t list_size, uint64_t seed, uint32_t* lists);
+/* train() for PARS_OBJ_POINTWISE_L1 / PARS_OBJ_LISTMLE from all-zero
+ * weights: GPU extract_all, per-epoch derive_seed(seed, 0x10000+e) order or
+ * lists, GPU epochs. ids: arena + id_offsets[n+1] (ListMLE tiebreak). */
+int pars_train_baseline(pars_ctx* ctx, const pars_extractor* ex,
+                        const char* text, const int64_t* offsets,
+                        const int64_t* lengths, const char* ids,
+                        const int64_t* id_offsets, int64_t n, int32_t objective,
+                        int32_t epochs, int32_t batch, double lr, uint64_t seed,
+                        uint64_t lists_per_epoch, int32_t list_size,
+                        double* w_out, double* bias_out, double* loss_trace);
+
 /* ---- priority ordering (scheduler.cpp:33-60) --------------------------
  * Full select_batch order: boosted first by tie_rank; the rest ascending by
  * score then tie_rank; equal keys keep input order (stable LSD radix).

@@ -327,7 +327,8 @@ class Ref:
         L.ref_evaluate_ranking.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                            C.c_void_p, C.c_void_p]
         L.ref_train.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int,
-                                C.c_int, C.c_double, C.c_uint64, C.c_uint64, C.c_void_p,
+                                C.c_int, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
+                                C.c_int, C.c_void_p,
                                 C.c_void_p, C.c_void_p]
         L.ref_poisson.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_void_p]
         L.ref_set_threads.argtypes = [C.c_int]
@@ -414,12 +415,13 @@ class Ref:
         return tau.value, counts
 
     def train(self, ds, ex, objective=0, delta=0.2, margin=1.0, epochs=5, batch=128, lr=0.1,
-              seed=0, ppe=100000):
+              seed=0, ppe=100000, lists_per_epoch=2000, list_size=10):
         w = np.zeros(ex.dim, np.float64)
         bias = C.c_double()
         lt = np.zeros(max(epochs, 1), np.float64)
         rc = self.L.ref_train(ds.h, C.byref(ex), objective, delta, margin, epochs, batch, lr,
-                              seed, ppe, _ptr(w), C.byref(bias), _ptr(lt))
+                              seed, ppe, lists_per_epoch, list_size, _ptr(w), C.byref(bias),
+                              _ptr(lt))
         if rc != 0:
             raise self._err()
         return w, bias.value, lt[:epochs].copy()

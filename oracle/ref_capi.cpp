@@ -271,10 +271,12 @@ int ref_evaluate_ranking(const RefExtractor* e, void* h, const double* w,
 // ---- training -------------------------------------------------------------
 int ref_train(void* h, const RefExtractor* e, int objective, double delta,
               double margin, int epochs, int batch_size, double lr,
-              uint64_t seed, uint64_t pairs_per_epoch, double* w_out,
-              double* bias_out, double* loss_trace_out) {
+              uint64_t seed, uint64_t pairs_per_epoch, uint64_t lists_per_epoch,
+              int list_size, double* w_out, double* bias_out, double* loss_trace_out) {
   return guard([&] {
     TrainConfig cfg;
+    cfg.lists_per_epoch = lists_per_epoch;
+    cfg.list_size = list_size;
     cfg.objective = static_cast<Objective>(objective);
     cfg.delta = delta;
     cfg.margin = margin;

@@ -116,6 +116,12 @@ def _load() -> C.CDLL:
         "pars_dev_allpairs_plan": (C.c_int, [vp, vp, vp, dbl, i64, i64, vp, vp, vp, vp]),
         "pars_dev_allpairs": (C.c_int, [vp, vp, vp, i64, dbl, dbl, i64, i64, i64, vp, vp, vp, vp]),
         "pars_dev_xt_c": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
+        "pars_pointwise_epoch": (C.c_int, [vp, vp, vp, i64, vp, i32, dbl, vp, vp, vp]),
+        "pars_listmle_epoch": (C.c_int, [vp, vp, vp, i64, i32, i32, dbl, vp, dbl, vp]),
+        "pars_pointwise_order": (C.c_int, [i64, u64, vp]),
+        "pars_listmle_lists": (C.c_int, [vp, vp, vp, i64, i64, i32, u64, vp]),
+        "pars_train_baseline": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, dbl, u64,
+                                          u64, i32, vp, vp, vp]),
         "pars_sgd_epoch": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp]),
         "pars_sgd_epoch_algo": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, dbl, dbl, vp, dbl, vp, vp,
                                           C.c_int]),
@@ -543,6 +549,46 @@ class Context:
         _check(lib().pars_train_pairwise(self.h, C.byref(ex), _p(text), _p(offs), _p(lens),
                                          len(offs) - 1, delta, margin, epochs, batch, lr, seed,
                                          pairs_per_epoch, _p(w), C.byref(bias), _p(lt)))
+        return w, bias.value, lt[:epochs].copy()
+
+    def pointwise_epoch(self, feats: Features, order, target, batch: int, lr: float, w,
+                        bias: float = 0.0):
+        """One PointwiseL1 epoch (train.cpp:168-183): (w, bias, loss_sum)."""
+        w = np.array(w, np.float64, copy=True)
+        order, target = _c(order, np.uint32), _c(target, np.float64)
+        b, el = C.c_double(bias), C.c_double()
+        _check(lib().pars_pointwise_epoch(self.h, C.c_void_p(feats.h), _p(order), len(order),
+                                          _p(target), batch, lr, _p(w), C.byref(b), C.byref(el)))
+        return w, b.value, el.value
+
+    def listmle_epoch(self, feats: Features, lists, k: int, batch: int, lr: float, w,
+                      bias: float = 0.0):
+        """One ListwiseListMLE epoch (train.cpp:185-205): (w, loss_sum)."""
+        w = np.array(w, np.float64, copy=True)
+        lists = _c(lists, np.uint32)
+        el = C.c_double()
+        _check(lib().pars_listmle_epoch(self.h, C.c_void_p(feats.h), _p(lists), len(lists) // k,
+                                        k, batch, lr, _p(w), bias, C.byref(el)))
+        return w, el.value
+
+    def train_baseline(self, ex: Extractor, text, offsets, lengths, ids, objective: str,
+                       epochs=5, batch=128, lr=0.1, seed=0, lists_per_epoch=2000, list_size=10):
+        """train() with Objective::PointwiseL1 ("pointwise_l1") or
+        ListwiseListMLE ("listwise_listmle") (train.cpp:122-216)."""
+        obj = {"pointwise_l1": 1, "listwise_listmle": 2}[objective]
+        offs = _c(offsets, np.int64)
+        lens = _c(lengths, np.int64)
+        bs = [i.encode() if isinstance(i, str) else bytes(i) for i in ids]
+        id_offs = np.zeros(len(bs) + 1, np.int64)
+        id_offs[1:] = np.cumsum([len(x) for x in bs])
+        arena = np.frombuffer(b"".join(bs) + b"\0", np.uint8)
+        w = np.zeros(ex.dim, np.float64)
+        bias = C.c_double()
+        lt = np.zeros(max(epochs, 1), np.float64)
+        _check(lib().pars_train_baseline(self.h, C.byref(ex), _p(text), _p(offs), _p(lens),
+                                         _p(arena), _p(id_offs), len(offs) - 1, obj, epochs, batch,
+                                         lr, seed, lists_per_epoch, list_size, _p(w),
+                                         C.byref(bias), _p(lt)))
         return w, bias.value, lt[:epochs].copy()
 
     # -- scheduling / metrics ------------------------------------------------

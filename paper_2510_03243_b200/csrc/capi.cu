@@ -60,7 +60,7 @@ struct pars_ctx {
   std::atomic<uint64_t> launches{0};
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
-      gscratch, lists, plan_buf;
+      gscratch, lists, plan_buf, baseline;
   HostBuf h_offs[2], h_scores;
   std::vector<cudaEvent_t> ev_chunk;  // per-chunk score hand-off (grow-only)
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
@@ -408,7 +408,8 @@ void pars_ctx_destroy(pars_ctx* c) {
   cudaStreamSynchronize(c->copy_stream);
   DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
                     &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
-                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists, &c->plan_buf};
+                    &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists, &c->plan_buf,
+                    &c->baseline};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores})
@@ -1354,6 +1355,188 @@ int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex, const char* tex
     }
   }
   *bias_out = 0.0;  // pairwise bias gradient cancels (train.hpp:41-43)
+  pars_features_free(f);
+  return rc;
+}
+
+// ---- comparison objectives (train.cpp:46-94, :168-205) ---------------------
+
+namespace pars_b200 {
+namespace capi_detail {
+
+// One PointwiseL1 (kind 0) or ListMLE (kind 1) epoch on the device weights
+// d_w. rows[s] is the feature row of slot s; a batch is `batch` samples
+// (kind 0) or `batch` lists of k consecutive slots (kind 1). *bias in/out.
+int baseline_epoch_impl(pars_ctx* ctx, pars_features* f, int kind, const uint32_t* rows,
+                        int64_t nslots, int32_t k, int32_t batch, const double* d_target,
+                        double lr, double* d_w, double* bias, double* epoch_loss) {
+  const char* who = kind ? "listmle" : "pointwise";
+  if (batch < 1) {
+    set_error("train: batch_size must be >= 1");
+    return PARS_ERR_INVALID;
+  }
+  if (kind && k < 2) {
+    set_error("listmle: list needs >= 2 items");
+    return PARS_ERR_INVALID;
+  }
+  *epoch_loss = 0.0;
+  if (nslots <= 0) return PARS_OK;
+  if (kind && nslots % k) {
+    set_error("listmle: %lld rows are not whole lists of %d", (long long)nslots, k);
+    return PARS_ERR_INVALID;
+  }
+  const int64_t spb = (int64_t)batch * (kind ? k : 1);
+  if (baseline_smem_bytes(f->dim, std::min<int64_t>(spb, nslots)) > 227 * 1024) {
+    set_error("%s: %lld slots per batch at dim %u exceed the shared-memory step state", who,
+              (long long)spb, f->dim);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  for (int64_t s = 0; s < nslots; ++s)
+    if (rows[s] >= f->rows) {
+      set_error("%s: slot %lld references a row outside [0, %lld)", who, (long long)s,
+                (long long)f->rows);
+      return PARS_ERR_INVALID;
+    }
+  const int64_t nb = (nslots + spb - 1) / spb;
+  std::vector<int64_t> soff((size_t)nb + 1), ent_off((size_t)nb + 1, 0);
+  int64_t max_slots = 0;
+  for (int64_t q = 0; q <= nb; ++q) soff[q] = std::min(nslots, q * spb);
+  for (int64_t q = 0; q < nb; ++q) {
+    int64_t e = 0;
+    for (int64_t s = soff[q]; s < soff[q + 1]; ++s) e += f->h_rp[rows[s] + 1] - f->h_rp[rows[s]];
+    ent_off[q + 1] = ent_off[q] + e;
+    max_slots = std::max(max_slots, soff[q + 1] - soff[q]);
+  }
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->sgd, baseline_scratch_bytes(nb, nslots, f->dim, ent_off[nb]) + 4096));
+  PARS_TRY(ensure(ctx->pairs_in, 64));
+  double* d_out = (double*)ctx->pairs_in.p;  // {loss, bias}
+  PARS_TRY(launch_baseline_epoch(ctx, kind, f->d_rp, f->d_idx, f->d_val, f->dim, rows, soff.data(),
+                                 nb, k, d_target, lr, *bias, max_slots, ent_off.data(), d_w,
+                                 d_out + 1, d_out, ctx->sgd.p, st));
+  double out[2];
+  PARS_CUDA_CHECK(cudaMemcpyAsync(out, d_out, 16, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  *epoch_loss = out[0];
+  *bias = out[1];
+  return PARS_OK;
+}
+
+// target[r] = pointwise_target(output_len[r]) = log1p(len) (train.cpp:30-32),
+// evaluated with the host libm the reference uses, onto the device.
+int upload_targets(pars_ctx* ctx, const int64_t* lengths, int64_t n, double** d_target) {
+  std::vector<double> t((size_t)n);
+  for (int64_t i = 0; i < n; ++i) t[i] = std::log1p(static_cast<double>(lengths[i]));
+  PARS_TRY(ensure(ctx->baseline, (size_t)n * 8 + 64));
+  *d_target = (double*)ctx->baseline.p;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(*d_target, t.data(), (size_t)n * 8, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return PARS_OK;
+}
+
+}  // namespace capi_detail
+}  // namespace pars_b200
+
+int pars_pointwise_epoch(pars_ctx* ctx, const pars_features* fc, const uint32_t* order, int64_t n,
+                         const double* target, int32_t batch, double lr, double* w, double* bias,
+                         double* epoch_loss) {
+  PARS_TRY(check_ctx(ctx));
+  pars_features* f = const_cast<pars_features*>(fc);
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->misc2, (size_t)f->dim * 8));
+  PARS_TRY(ensure(ctx->baseline, (size_t)f->rows * 8 + 64));
+  double* d_w = (double*)ctx->misc2.p;
+  double* d_t = (double*)ctx->baseline.p;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_w, w, (size_t)f->dim * 8, cudaMemcpyHostToDevice, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, target, (size_t)f->rows * 8, cudaMemcpyHostToDevice, st));
+  PARS_TRY(baseline_epoch_impl(ctx, f, 0, order, n, 1, batch, d_t, lr, d_w, bias, epoch_loss));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(w, d_w, (size_t)f->dim * 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+int pars_listmle_epoch(pars_ctx* ctx, const pars_features* fc, const uint32_t* lists,
+                       int64_t nlists, int32_t k, int32_t batch, double lr, double* w, double bias,
+                       double* epoch_loss) {
+  PARS_TRY(check_ctx(ctx));
+  pars_features* f = const_cast<pars_features*>(fc);
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  PARS_TRY(ensure(ctx->misc2, (size_t)f->dim * 8));
+  double* d_w = (double*)ctx->misc2.p;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_w, w, (size_t)f->dim * 8, cudaMemcpyHostToDevice, st));
+  double b = bias;
+  PARS_TRY(baseline_epoch_impl(ctx, f, 1, lists, nlists * k, k, batch, nullptr, lr, d_w, &b,
+                               epoch_loss));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(w, d_w, (size_t)f->dim * 8, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
+// train() for Objective::PointwiseL1 / ListwiseListMLE (train.cpp:122-216).
+int pars_train_baseline(pars_ctx* ctx, const pars_extractor* ex, const char* text,
+                        const int64_t* offsets, const int64_t* lengths, const char* ids,
+                        const int64_t* id_offsets, int64_t n, int32_t objective, int32_t epochs,
+                        int32_t batch, double lr, uint64_t seed, uint64_t lists_per_epoch,
+                        int32_t list_size, double* w_out, double* bias_out, double* loss_trace) {
+  PARS_TRY(check_ctx(ctx));
+  if (objective != PARS_OBJ_POINTWISE_L1 && objective != PARS_OBJ_LISTMLE) {
+    set_error("train_baseline: objective %d is not pointwise_l1 or listwise_listmle", objective);
+    return PARS_ERR_INVALID;
+  }
+  if (epochs < 0) { set_error("train: epochs must be >= 0"); return PARS_ERR_INVALID; }
+  if (batch < 1) { set_error("train: batch_size must be >= 1"); return PARS_ERR_INVALID; }
+  if (!(lr > 0.0)) { set_error("train: learning_rate must be > 0"); return PARS_ERR_INVALID; }
+  if (lists_per_epoch < 1) { set_error("train: lists_per_epoch must be >= 1"); return PARS_ERR_INVALID; }
+  if (list_size < 2) { set_error("train: list_size must be >= 2"); return PARS_ERR_INVALID; }
+  if (n <= 0) { set_error("train: empty dataset"); return PARS_ERR_INVALID; }
+  const bool listwise = objective == PARS_OBJ_LISTMLE;
+  if (listwise && n < 2) { set_error("train: listwise needs >= 2 records"); return PARS_ERR_INVALID; }
+  pars_features* f = nullptr;
+  PARS_TRY(pars_extract(ctx, ex, text, offsets, n, nullptr, &f));
+  const uint32_t dim = ex->dim;
+  int rc = PARS_OK;
+  double bias = 0.0;
+  {
+    Guard g(ctx);
+    cudaStream_t st = ctx->stream;
+    rc = ensure(ctx->misc2, (size_t)dim * 8);
+    double* d_w = (double*)ctx->misc2.p;
+    if (rc == PARS_OK)
+      rc = cudaMemsetAsync(d_w, 0, (size_t)dim * 8, st) == cudaSuccess ? PARS_OK : PARS_ERR_CUDA;
+    double* d_t = nullptr;
+    if (rc == PARS_OK && !listwise) rc = upload_targets(ctx, lengths, n, &d_t);
+    const int32_t k = (int32_t)std::min<int64_t>(list_size, n);
+    std::vector<uint32_t> rows(listwise ? (size_t)lists_per_epoch * k : (size_t)n);
+    for (int e = 0; e < epochs && rc == PARS_OK; ++e) {
+      const uint64_t es = splitmix64(seed ^ splitmix64(0x10000u + (uint64_t)e));  // derive_seed
+      rc = listwise ? pars_listmle_lists(lengths, ids, id_offsets, n, (int64_t)lists_per_epoch,
+                                         list_size, es, rows.data())
+                    : pars_pointwise_order(n, es, rows.data());
+      if (rc != PARS_OK) break;
+      double el = 0.0;
+      rc = baseline_epoch_impl(ctx, f, listwise ? 1 : 0, rows.data(), (int64_t)rows.size(), k,
+                               batch, d_t, lr, d_w, &bias, &el);
+      if (rc != PARS_OK) break;
+      const double mean = el / (double)(listwise ? (int64_t)lists_per_epoch : n);
+      if (!std::isfinite(mean)) {
+        set_error("training diverged at epoch %d", e);
+        rc = PARS_ERR_INVALID;
+        break;
+      }
+      loss_trace[e] = mean;
+    }
+    if (rc == PARS_OK) {
+      if (cudaMemcpyAsync(w_out, d_w, (size_t)dim * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("CUDA error reading trained weights");
+        rc = PARS_ERR_CUDA;
+      }
+    }
+  }
+  *bias_out = bias;
   pars_features_free(f);
   return rc;
 }

@@ -16,6 +16,7 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -135,6 +136,54 @@ int64_t pars_build_pairs(const int64_t* lens, int64_t n, double delta, uint64_t 
     return PARS_ERR_INVALID;
   }
   return cnt;
+}
+
+// PointwiseL1 epoch order (train.cpp:169-172): iota shuffled by Rng(seed).
+int pars_pointwise_order(int64_t n, uint64_t seed, uint32_t* order) {
+  if (n < 0) {
+    set_error("pointwise_order: negative count");
+    return PARS_ERR_INVALID;
+  }
+  std::vector<uint32_t> v(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) v[i] = static_cast<uint32_t>(i);
+  Rng rng(seed);
+  rng.shuffle(v);
+  std::copy(v.begin(), v.end(), order);
+  return PARS_OK;
+}
+
+// ListMLE epoch lists (train.cpp:186-200): partial Fisher-Yates on a pool
+// that persists across the epoch's lists, each list then ordered longest
+// first with the id (unsigned bytes) as tiebreak (sort_by_true_order,
+// train.cpp:110-118). lists[nlists * k], k = min(list_size, n).
+int pars_listmle_lists(const int64_t* output_len, const char* ids, const int64_t* id_offsets,
+                       int64_t n, int64_t nlists, int32_t list_size, uint64_t seed,
+                       uint32_t* lists) {
+  if (n < 2) {
+    set_error("train: listwise needs >= 2 records");
+    return PARS_ERR_INVALID;
+  }
+  if (list_size < 2) {
+    set_error("train: list_size must be >= 2");
+    return PARS_ERR_INVALID;
+  }
+  const size_t k = std::min<size_t>(static_cast<size_t>(list_size), static_cast<size_t>(n));
+  Rng rng(seed);
+  std::vector<uint32_t> pool(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) pool[i] = static_cast<uint32_t>(i);
+  auto id_of = [&](uint32_t r) {
+    return std::string_view(ids + id_offsets[r], static_cast<size_t>(id_offsets[r + 1] - id_offsets[r]));
+  };
+  for (int64_t l = 0; l < nlists; ++l) {
+    for (size_t t = 0; t < k; ++t) std::swap(pool[t], pool[t + rng.below(n - t)]);
+    uint32_t* list = lists + l * static_cast<int64_t>(k);
+    std::copy(pool.begin(), pool.begin() + k, list);
+    std::sort(list, list + k, [&](uint32_t a, uint32_t b) {
+      if (output_len[a] != output_len[b]) return output_len[a] > output_len[b];
+      return id_of(a) < id_of(b);
+    });
+  }
+  return PARS_OK;
 }
 
 int pars_length_gap_table(double delta, int64_t max_len, int32_t* dmin) {

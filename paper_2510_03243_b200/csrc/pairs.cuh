@@ -76,4 +76,14 @@ int launch_sgd_epoch(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, cons
                      int64_t total_entries, void* scratch, size_t scratch_bytes,
                      cudaStream_t st);
 
+// PointwiseL1 / ListMLE epochs (baselines.cu). kind 0 = pointwise, 1 = ListMLE.
+size_t baseline_smem_bytes(uint32_t dim, int64_t max_slots);
+size_t baseline_scratch_bytes(int64_t nbatches, int64_t nslots, uint32_t dim, int64_t entries);
+int launch_baseline_epoch(pars_ctx* ctx, int kind, const int64_t* rp, const uint32_t* idx,
+                          const double* val, uint32_t dim, const uint32_t* h_srow,
+                          const int64_t* h_soff, int64_t nb, int32_t k, const double* d_target,
+                          double lr, double bias, int64_t max_slots, const int64_t* h_ent_off,
+                          double* d_w, double* d_bias_out, double* d_loss_out, void* scratch,
+                          cudaStream_t st);
+
 }  // namespace pars_b200

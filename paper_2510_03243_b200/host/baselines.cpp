@@ -1,9 +1,9 @@
 // The paper's comparison objectives (pointwise L1 regression on log length,
-// ListMLE) for train.hpp — outside the PARS hot path (SURVEY §2 row 6,
-// §8(f).4), kept so the shim is a complete drop-in for train.cpp. Host code
-// over GPU-extracted features; every floating-point expression keeps the
-// reference's evaluation order (train.cpp:46-94 and :141-151, :168-209), so
-// results match the CPU library.
+// ListMLE) for train.hpp. train() runs them on the GPU
+// engine (baselines.cu via pars_pointwise_epoch / pars_listmle_epoch); the
+// single-call loss/grad helpers below are host code over host FeatureVecs,
+// each floating-point expression in the reference's order
+// (train.cpp:46-94), so they match the CPU library.
 #include <algorithm>
 #include <cmath>
 #include <span>
@@ -16,38 +16,12 @@ namespace pars {
 
 namespace {
 
-// Minibatch accumulator: dense gradient + bias gradient, applied as
-// w[d] -= (lr / batch) * g[d] for g[d] != 0, then cleared.
-struct Minibatch {
-  std::vector<double> g;
-  double gb = 0.0;
-  explicit Minibatch(uint32_t dim) : g(dim, 0.0) {}
-  void add(const FeatureVec& x, double coef) {
-    for (const auto& [d, v] : x.entries) g[d] += coef * v;
-  }
-  void step(LinearScorer& s, double lr, size_t batch) {
-    const double scale = lr / static_cast<double>(batch);
-    std::vector<double>& w = s.weights();
-    for (size_t d = 0; d < g.size(); ++d) {
-      if (g[d] == 0.0) continue;
-      w[d] -= scale * g[d];
-      g[d] = 0.0;
-    }
-    s.bias() -= scale * gb;
-    gb = 0.0;
-  }
-};
-
-double dot_bias(const LinearScorer& s, const FeatureVec& x) {
-  return x.dot(s.weights()) + s.bias();
-}
-
 double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
 // log(exp(a) + exp(b)) evaluated around the larger argument.
 double lse2(double a, double b) {
-  const double m = a < b ? b : a;
-  const double r = a < b ? a : b;
+  const double m = a < b ? b : a;  // std::max / std::min (train.cpp:58-62)
+  const double r = b < a ? b : a;
   return m + std::log1p(std::exp(r - m));
 }
 
@@ -94,63 +68,50 @@ double listmle_loss_grad(const LinearScorer& scorer, const std::vector<FeatureVe
 
 namespace b200 {
 
-void train_baseline(const Dataset& ds, const TrainConfig& cfg, const std::vector<FeatureVec>& feats,
+// train() for the comparison objectives (train.cpp:168-209) on the GPU
+// engine: the epoch order / lists come from the reference's Rng on the host
+// (pars_pointwise_order / pars_listmle_lists, bit-identical), the epochs run
+// in baselines.cu over the device features.
+void train_baseline(const Dataset& ds, const TrainConfig& cfg, const DeviceFeatures& dev,
                     TrainedModel& model) {
   const size_t n = ds.records.size();
-  LinearScorer& sc = model.scorer;
-  Minibatch mb(cfg.extractor.dim);
   const bool listwise = cfg.objective == Objective::ListwiseListMLE;
   if (listwise && n < 2) throw Error("train: listwise needs >= 2 records");
-  std::vector<uint32_t> idx(n);
-  for (size_t i = 0; i < n; ++i) idx[i] = static_cast<uint32_t>(i);
-  for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
-    Rng rng(derive_seed(cfg.seed, 0x10000u + epoch));
-    double total = 0.0;
-    size_t samples = 0;
-    if (!listwise) {
-      // one shuffled pass, batch_size samples per step
-      std::vector<uint32_t> perm = idx;
-      rng.shuffle(perm);
-      for (size_t lo = 0; lo < n; lo += cfg.batch_size) {
-        const size_t hi = std::min(n, lo + static_cast<size_t>(cfg.batch_size));
-        for (size_t p = lo; p < hi; ++p) {
-          const FeatureVec& x = feats[perm[p]];
-          const double r = dot_bias(sc, x) - pointwise_target(ds.records[perm[p]].output_len);
-          const double g = sgn(r);
-          mb.add(x, g);
-          mb.gb += g;
-          total += std::fabs(r);
-        }
-        mb.step(sc, cfg.learning_rate, hi - lo);
-        samples += hi - lo;
-      }
-    } else {
-      // lists_per_epoch lists of list_size items drawn without replacement
-      // (partial Fisher-Yates on a persistent pool), ordered longest-first
-      // with id tiebreak; batch_size lists per step
-      const size_t k = std::min<size_t>(static_cast<size_t>(cfg.list_size), n);
-      std::vector<uint32_t> pool = idx, list(k);
-      std::vector<double> s(k), coef;
-      size_t pending = 0;
-      for (size_t l = 0; l < cfg.lists_per_epoch; ++l) {
-        for (size_t t = 0; t < k; ++t) std::swap(pool[t], pool[t + rng.below(n - t)]);
-        std::copy(pool.begin(), pool.begin() + k, list.begin());
-        std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t b) {
-          const PromptRecord& ra = ds.records[a];
-          const PromptRecord& rb = ds.records[b];
-          return ra.output_len != rb.output_len ? ra.output_len > rb.output_len : ra.id < rb.id;
-        });
-        for (size_t t = 0; t < k; ++t) s[t] = dot_bias(sc, feats[list[t]]);
-        total += listmle_nll(s, coef);
-        for (size_t t = 0; t < k; ++t) mb.add(feats[list[t]], coef[t]);
-        ++samples;
-        if (++pending == static_cast<size_t>(cfg.batch_size) || l + 1 == cfg.lists_per_epoch) {
-          mb.step(sc, cfg.learning_rate, pending);
-          pending = 0;
-        }
-      }
+  std::vector<int64_t> lens(n);
+  for (size_t i = 0; i < n; ++i) lens[i] = ds.records[i].output_len;
+  std::vector<double> target;
+  std::string ids;
+  std::vector<int64_t> id_offs(n + 1, 0);
+  if (listwise) {
+    for (size_t i = 0; i < n; ++i) {
+      ids += ds.records[i].id;
+      id_offs[i + 1] = static_cast<int64_t>(ids.size());
     }
-    const double mean = total / static_cast<double>(samples);
+  } else {
+    target.resize(n);
+    for (size_t i = 0; i < n; ++i) target[i] = pointwise_target(lens[i]);
+  }
+  const int32_t k = static_cast<int32_t>(std::min<size_t>(static_cast<size_t>(cfg.list_size), n));
+  std::vector<uint32_t> rows(listwise ? cfg.lists_per_epoch * k : n);
+  std::vector<double>& w = model.scorer.weights();
+  for (int epoch = 0; epoch < cfg.epochs; ++epoch) {
+    const uint64_t es = derive_seed(cfg.seed, 0x10000u + epoch);
+    double total = 0.0;
+    if (listwise) {
+      check(pars_listmle_lists(lens.data(), ids.data(), id_offs.data(), static_cast<int64_t>(n),
+                               static_cast<int64_t>(cfg.lists_per_epoch), cfg.list_size, es,
+                               rows.data()));
+      check(pars_listmle_epoch(ctx(), dev.f, rows.data(), static_cast<int64_t>(cfg.lists_per_epoch),
+                               k, cfg.batch_size, cfg.learning_rate, w.data(),
+                               model.scorer.bias(), &total));
+    } else {
+      check(pars_pointwise_order(static_cast<int64_t>(n), es, rows.data()));
+      check(pars_pointwise_epoch(ctx(), dev.f, rows.data(), static_cast<int64_t>(n), target.data(),
+                                 cfg.batch_size, cfg.learning_rate, w.data(),
+                                 &model.scorer.bias(), &total));
+    }
+    const double mean =
+        total / static_cast<double>(listwise ? cfg.lists_per_epoch : n);
     if (!std::isfinite(mean)) fail("training diverged at epoch %d", epoch);
     model.loss_trace.push_back(mean);
   }

@@ -8,8 +8,9 @@
 //   pairwise_loss_grad -> both scores on the GPU, the hinge and the sparse
 //                       update of the caller's host gradient as train.cpp:34-44
 //   PointwiseL1 / ListwiseListMLE (train.cpp:46-94, :168-209) are the
-//   paper's comparison baselines, outside the PARS hot path (SURVEY §2 row
-//   6): restated on the host over GPU-extracted features.
+//   paper's comparison baselines: host-sampled epoch order
+//   / lists, GPU epochs (baselines.cu); pointwise bit-identical, ListMLE to
+//   rounding (CUDA exp/log1p).
 #include <algorithm>
 #include <cmath>
 #include <span>
@@ -22,7 +23,7 @@
 namespace pars {
 
 namespace b200 {
-void train_baseline(const Dataset& ds, const TrainConfig& cfg, const std::vector<FeatureVec>& feats,
+void train_baseline(const Dataset& ds, const TrainConfig& cfg, const DeviceFeatures& dev,
                     TrainedModel& model);
 }
 using b200::train_baseline;
@@ -139,8 +140,8 @@ TrainedModel train(const Dataset& ds, const TrainConfig& cfg) {
     return model;
   }
 
-  // comparison baselines (train.cpp:168-209): host, over GPU-extracted features
-  train_baseline(ds, cfg, b200::download(dev), model);
+  // comparison baselines (train.cpp:168-209): GPU epochs (baselines.cu)
+  train_baseline(ds, cfg, dev, model);
   return model;
 }
 
