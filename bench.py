@@ -472,8 +472,11 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
 
 def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
     """Kendall tau-b counts (metrics.cpp:42-64) at compare_policies scale: the
-    PARS scores vs output lengths of 100,000 requests (C3-sized trace), all
-    4,999,950,000 pairs, tiles split over ranks + one exact all-reduce."""
+    PARS scores vs output lengths of 100,000 requests (C3-sized trace). The
+    default path counts by sorting (tau_sorted.cu, O(n log n), exact; every
+    rank computes the whole trace, no collective); the all-pairs tile path
+    (4,999,950,000 pairs split over ranks + one exact all-reduce) is timed
+    beside it. value = all-pairs-equivalent pairs per second."""
     from paper_2510_03243_b200 import distributed as D
     n = 100_000
     wl = P.Workload.synthesize(n, 23)
@@ -482,20 +485,28 @@ def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
     y = wl.output_len.astype(np.float64)
     dx, dy = torch.from_numpy(s).to(dev), torch.from_numpy(y).to(dev)
     sh = stream.cuda_stream
-    for _ in range(2):
-        tau, c = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
-    torch.cuda.synchronize()
-    barrier(world)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(3, args.steps)
-    a.record(stream)
-    for _ in range(k):
-        tau, c = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = barrier_max(world, a.elapsed_time(b)) / k
+
+    def timed(fn):
+        for _ in range(2):
+            r = fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            r = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return barrier_max(world, a.elapsed_time(b)) / k, r
+
+    ms, (tau, c) = timed(lambda: ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), n, stream=sh))
+    ms_pairs, (tau_p, c_p) = timed(lambda: D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh))
     pairs = n * (n - 1) // 2
     out = {"metric": "pairs/s", "value": pairs / (ms / 1e3), "ms_per_call": ms, "tau_b": tau,
+           "algorithm": "sorted counts (two radix sorts + merge inversion count), exact",
+           "pairs_path_ms": ms_pairs, "pairs_path_pairs_per_s": pairs / (ms_pairs / 1e3),
+           "paths_agree": bool((c == c_p).all()) and tau == tau_p,
            "workload": "kendall_tau_b(scores, output_len) over 100,000 requests "
                        "(4,999,950,000 pairs), exact integer counts"}
     if world == 1 and not args.no_cpu:
@@ -504,7 +515,8 @@ def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
         t0 = time.perf_counter()
         otau, oc = Oracle().kendall(s[:m], y[:m], threads=host_threads())
         dt = time.perf_counter() - t0
-        gt, gc = D.kendall_tau_gpu(ctx, dx[:m].contiguous(), dy[:m].contiguous(), m, stream=sh)
+        gt, gc = ctx.dev_kendall_tau(dx[:m].contiguous().data_ptr(), dy[:m].contiguous().data_ptr(),
+                                     m, stream=sh)
         out.update({"cpu_pairs_per_s": (m * (m - 1) // 2) / dt, "cpu_threads": host_threads(),
                     "cpu_sample": "first %d requests (port of metrics.cpp, OpenMP)" % m,
                     "sample_counts_match": bool((gc == oc).all()) and gt == otau})

@@ -317,6 +317,21 @@ int pars_tie_ranks(const double* arrival, const char* ids,
  * with the reference's message. */
 int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y,
                      int64_t n, uint64_t* counts, double* tau_b);
+/* Choosing the algorithm: PARS_TAU_SORTED counts by sorting (two stable
+ * radix sorts + a merge-sort inversion count, O(n log n); finite inputs
+ * only), PARS_TAU_PAIRS runs the all-pairs tiles, PARS_TAU_AUTO (what
+ * pars_kendall_tau does) sorts unless an input is inf/NaN. All give the
+ * reference's exact integers. */
+#define PARS_TAU_AUTO 0
+#define PARS_TAU_SORTED 1
+#define PARS_TAU_PAIRS 2
+int pars_kendall_tau_algo(pars_ctx* ctx, const double* x, const double* y,
+                          int64_t n, uint64_t* counts, double* tau_b, int algo);
+/* pars_kendall_tau on device arrays (stream-ordered; returns after the
+ * counts are on the host). */
+int pars_dev_kendall_tau(pars_ctx* ctx, const double* d_x, const double* d_y,
+                         int64_t n, uint64_t* counts, double* tau_b,
+                         void* stream);
 /* The same counts split over upper-triangle tiles (the all-pairs tiling):
  * {n_c, n_d, n1, n2} of tiles [tile_begin, tile_end) ACCUMULATED into
  * d_counts[4] on the device (for data-parallel ranks: sum the counts, an

@@ -133,6 +133,8 @@ def _load() -> C.CDLL:
         "pars_dev_priority_order": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
         "pars_tie_ranks": (C.c_int, [vp, vp, vp, i64, vp]),
         "pars_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp]),
+        "pars_kendall_tau_algo": (C.c_int, [vp, vp, vp, i64, vp, vp, C.c_int]),
+        "pars_dev_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
         "pars_workload_synthesize": (C.c_int, [u64, dbl, dbl, u64, i64, u64, vp]),
         "pars_workload_count": (i64, [vp]),
         "pars_workload_text_bytes": (i64, [vp]),
@@ -601,10 +603,21 @@ class Context:
         _check(lib().pars_priority_order(self.h, _p(s), _p(bst), _p(t), len(s), _p(out)))
         return out
 
-    def kendall_tau(self, x, y):
-        """kendall_tau_b (metrics.cpp:42-64): (tau_b, counts[n_c,n_d,n0,n1,n2])."""
+    def kendall_tau(self, x, y, algo: str = "auto"):
+        """kendall_tau_b (metrics.cpp:42-64): (tau_b, counts[n_c,n_d,n0,n1,n2]).
+        algo: "auto" (sorted unless an input is inf/NaN), "sorted" (O(n log n))
+        or "pairs" (all-pairs tiles)."""
         x, y = _c(x, np.float64), _c(y, np.float64)
         counts = np.zeros(5, np.uint64)
         tau = C.c_double()
-        _check(lib().pars_kendall_tau(self.h, _p(x), _p(y), len(x), _p(counts), C.byref(tau)))
+        code = {"auto": 0, "sorted": 1, "pairs": 2}[algo]
+        _check(lib().pars_kendall_tau_algo(self.h, _p(x), _p(y), len(x), _p(counts), C.byref(tau),
+                                           code))
+        return tau.value, counts
+
+    def dev_kendall_tau(self, d_x: int, d_y: int, n: int, stream=None):
+        """kendall_tau_b of device arrays (pointers), stream-ordered."""
+        counts = np.zeros(5, np.uint64)
+        tau = C.c_double()
+        _check(lib().pars_dev_kendall_tau(self.h, d_x, d_y, n, _p(counts), C.byref(tau), stream))
         return tau.value, counts

@@ -60,7 +60,7 @@ struct pars_ctx {
   std::atomic<uint64_t> launches{0};
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
-      gscratch, lists, plan_buf, baseline;
+      gscratch, lists, plan_buf, baseline, tau;
   HostBuf h_offs[2], h_scores;
   std::vector<cudaEvent_t> ev_chunk;  // per-chunk score hand-off (grow-only)
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
@@ -409,7 +409,7 @@ void pars_ctx_destroy(pars_ctx* c) {
   DevBuf* bufs[] = {&c->text[0], &c->text[1], &c->offs[0], &c->offs[1], &c->scores[0],
                     &c->scores[1], &c->w64, &c->w32, &c->misc, &c->misc2, &c->longl,
                     &c->sort, &c->sgd, &c->pairs_in, &c->dmin_buf, &c->gscratch, &c->lists, &c->plan_buf,
-                    &c->baseline};
+                    &c->baseline, &c->tau};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores})
@@ -1578,8 +1578,56 @@ int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores, const uint8_t
 
 // ---- Kendall tau-b (metrics.cpp:13-64) -----------------------------------
 
+namespace pars_b200 {
+namespace capi_detail {
+
+// tau-b of device arrays on `st`: the O(n log n) sorted counts (tau_sorted.cu)
+// unless an input is non-finite (or algo asks for it), else the all-pairs
+// tiles (pairs.cu). Both give the reference's exact integers.
+int kendall_dev_impl(pars_ctx* ctx, const double* d_x, const double* d_y, int64_t n,
+                     uint64_t* counts, double* tau_b, int algo, cudaStream_t st) {
+  if (n < 2) {
+    set_error("kendall_tau_b: need at least 2 items, got %zu", (size_t)n);
+    return PARS_ERR_INVALID;
+  }
+  if (algo < PARS_TAU_AUTO || algo > PARS_TAU_PAIRS) {
+    set_error("kendall_tau_b: unknown algorithm %d", algo);
+    return PARS_ERR_INVALID;
+  }
+  uint64_t c4[4] = {0, 0, 0, 0};
+  int rc = PARS_ERR_UNSUPPORTED;
+  if (algo != PARS_TAU_PAIRS) {
+    PARS_TRY(ensure(ctx->tau, tau_sorted_scratch_bytes(n) + 4096));
+    rc = launch_tau_sorted(ctx, d_x, d_y, n, c4, ctx->tau.p, st);
+    if (rc != PARS_OK && rc != PARS_ERR_UNSUPPORTED) return rc;
+    if (rc == PARS_ERR_UNSUPPORTED && algo == PARS_TAU_SORTED) {
+      set_error("kendall_tau_b: the sorted algorithm needs finite inputs");
+      return PARS_ERR_UNSUPPORTED;
+    }
+  }
+  if (rc != PARS_OK) {
+    PARS_TRY(ensure(ctx->tau, 64));
+    unsigned long long* d_c = (unsigned long long*)ctx->tau.p;
+    PARS_CUDA_CHECK(cudaMemsetAsync(d_c, 0, 32, st));
+    PARS_TRY(launch_tau(ctx, d_x, d_y, n, d_c, st));
+    unsigned long long c[4];
+    PARS_CUDA_CHECK(cudaMemcpyAsync(c, d_c, 32, cudaMemcpyDeviceToHost, st));
+    PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int k = 0; k < 4; ++k) c4[k] = c[k];
+  }
+  return pars_kendall_finish(c4, n, counts, tau_b);
+}
+
+}  // namespace capi_detail
+}  // namespace pars_b200
+
 int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n, uint64_t* counts,
                      double* tau_b) {
+  return pars_kendall_tau_algo(ctx, x, y, n, counts, tau_b, PARS_TAU_AUTO);
+}
+
+int pars_kendall_tau_algo(pars_ctx* ctx, const double* x, const double* y, int64_t n,
+                          uint64_t* counts, double* tau_b, int algo) {
   PARS_TRY(check_ctx(ctx));
   if (n < 2) {
     set_error("kendall_tau_b: need at least 2 items, got %zu", (size_t)n);
@@ -1590,16 +1638,16 @@ int pars_kendall_tau(pars_ctx* ctx, const double* x, const double* y, int64_t n,
   PARS_TRY(ensure(ctx->pairs_in, (size_t)n * 16 + 64));
   double* d_x = (double*)ctx->pairs_in.p;
   double* d_y = d_x + n;
-  unsigned long long* d_c = (unsigned long long*)(d_y + n);
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * 8, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(d_y, y, (size_t)n * 8, cudaMemcpyHostToDevice, st));
-  PARS_CUDA_CHECK(cudaMemsetAsync(d_c, 0, 32, st));
-  PARS_TRY(launch_tau(ctx, d_x, d_y, n, d_c, st));
-  unsigned long long c[4];
-  PARS_CUDA_CHECK(cudaMemcpyAsync(c, d_c, 32, cudaMemcpyDeviceToHost, st));
-  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
-  const uint64_t c4[4] = {c[0], c[1], c[2], c[3]};
-  return pars_kendall_finish(c4, n, counts, tau_b);
+  return kendall_dev_impl(ctx, d_x, d_y, n, counts, tau_b, algo, st);
+}
+
+int pars_dev_kendall_tau(pars_ctx* ctx, const double* d_x, const double* d_y, int64_t n,
+                         uint64_t* counts, double* tau_b, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  Guard g(ctx);
+  return kendall_dev_impl(ctx, d_x, d_y, n, counts, tau_b, PARS_TAU_AUTO, pick(ctx, stream));
 }
 
 // finish_tau (metrics.cpp:13-32) on counts {n_c, n_d, n1, n2} of all pairs

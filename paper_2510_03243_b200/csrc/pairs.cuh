@@ -76,6 +76,11 @@ int launch_sgd_epoch(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, cons
                      int64_t total_entries, void* scratch, size_t scratch_bytes,
                      cudaStream_t st);
 
+// Kendall tau-b counts by sorting (tau_sorted.cu); counts4 on the host.
+size_t tau_sorted_scratch_bytes(int64_t n);
+int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n,
+                      uint64_t* counts4, void* scratch, cudaStream_t st);
+
 // PointwiseL1 / ListMLE epochs (baselines.cu). kind 0 = pointwise, 1 = ListMLE.
 size_t baseline_smem_bytes(uint32_t dim, int64_t max_slots);
 size_t baseline_scratch_bytes(int64_t nbatches, int64_t nslots, uint32_t dim, int64_t entries);

@@ -60,13 +60,13 @@ __global__ void radix_init(const double* __restrict__ score, const uint8_t* __re
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool bst = boosted && boosted[i];
     const uint64_t hi = bst ? 0ull : ordered_bits(score[i]);
-    const uint32_t lo = tie[i];
+    const uint32_t lo = tie ? tie[i] : 0u;  // no tie ranks: order by score, then index
     khi[i] = hi;
     klo[i] = lo;
     val[i] = (uint32_t)i;
     // tie ranks already non-decreasing in input order -> the stable sort
     // by score alone yields the (score, tie, index) order: skip tie digits
-    if (i > 0 && tie[i] < tie[i - 1]) dh[12 * 256] = 1u;
+    if (tie && i > 0 && tie[i] < tie[i - 1]) dh[12 * 256] = 1u;
 #pragma unroll
     for (int p = 0; p < 12; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, p)], 1u);
   }
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kSmallThreads) small_sort_kernel(
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
     if (i < n) {
       hi[i] = (boosted && boosted[i]) ? 0ull : ordered_bits(score[i]);
-      lo[i] = ((uint64_t)tie[i] << 32) | (uint32_t)i;
+      lo[i] = ((uint64_t)(tie ? tie[i] : 0u) << 32) | (uint32_t)i;
     } else {
       hi[i] = ~0ull;
       lo[i] = ~0ull;

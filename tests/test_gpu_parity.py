@@ -2,6 +2,8 @@
 reference's golden fixtures. Bit-exact for features, exact-mode scores,
 masks, coefficients, counts, orders and the SGD trajectory; fast fp32 mode
 within 1e-5 of sum|w_i v_i| (the magnitude scale)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -194,17 +196,68 @@ def test_allpairs_c2_mask_count(ctx):
     assert loss == float(kept)
 
 
-def test_kendall_tau_matches_goldens_and_oracle(ctx, oracle):
+@pytest.mark.parametrize("algo", ["auto", "sorted", "pairs"])
+def test_kendall_tau_matches_goldens_and_oracle(ctx, oracle, algo):
     for c in golden("tau.json"):
-        tau, counts = ctx.kendall_tau(unhex(c["x"]), unhex(c["y"]))
+        tau, counts = ctx.kendall_tau(unhex(c["x"]), unhex(c["y"]), algo)
         assert counts.tolist() == c["counts"]
         assert float(tau).hex() == c["tau"]
     rng = np.random.default_rng(9)
     x = rng.integers(0, 50, size=5000).astype(float)
     y = rng.normal(size=5000).round(2)
-    tau, counts = ctx.kendall_tau(x, y)
+    tau, counts = ctx.kendall_tau(x, y, algo)
     otau, ocounts = oracle.kendall(x, y)
     assert counts.tolist() == ocounts.tolist() and tau == otau
+
+
+@pytest.mark.parametrize("n", [2, 3, 17, 2047, 2048, 2049, 4096, 6000, 30011])
+def test_kendall_sorted_counts_exact(ctx, oracle, n):
+    """The O(n log n) counts (tau_sorted.cu) equal the reference's all-pairs
+    integers across tile boundaries (2,048), heavy ties in x, y and both,
+    and signed zeros (-0.0 == +0.0 is a tie)."""
+    rng = np.random.default_rng(n)
+    for x, y in ((rng.normal(size=n), rng.normal(size=n)),
+                 (rng.integers(0, 7, n).astype(float), rng.integers(0, 5, n).astype(float)),
+                 (np.where(rng.random(n) < 0.4, 0.0, np.where(rng.random(n) < 0.5, -0.0, 1.0)),
+                  rng.normal(size=n).round(1)),
+                 (np.arange(n, dtype=float), -np.arange(n, dtype=float)),
+                 (np.arange(n, dtype=float) % 3, np.arange(n, dtype=float))):
+        if (x == x[0]).all() or (y == y[0]).all():
+            continue
+        otau, oc = oracle.kendall(x, y, threads=os.cpu_count() or 1)
+        tau, c = ctx.kendall_tau(x, y, "sorted")
+        assert c.tolist() == oc.tolist() and tau == otau
+
+
+def test_kendall_non_finite_falls_back_to_pairs(ctx, oracle):
+    """inf - inf = NaN is neither a tie nor negative in the reference, so the
+    sorted method does not apply: auto runs the all-pairs tiles."""
+    from paper_2510_03243_b200 import ParsError
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=3000)
+    y = rng.normal(size=3000)
+    x[[5, 9, 700]] = [np.inf, np.inf, -np.inf]
+    y[[11, 12]] = [np.nan, np.inf]
+    otau, oc = oracle.kendall(x, y)
+    tau, c = ctx.kendall_tau(x, y, "auto")
+    assert c.tolist() == oc.tolist() and tau == otau
+    with pytest.raises(ParsError, match="finite"):
+        ctx.kendall_tau(x, y, "sorted")
+
+
+def test_kendall_sorted_large_matches_pairs(ctx):
+    """At the C3 trace size both GPU algorithms give the same integers."""
+    import torch
+    from paper_2510_03243_b200 import Workload
+    wl = Workload.synthesize(100_000, 23)
+    x = np.random.default_rng(1).normal(size=100_000).round(3)
+    y = wl.output_len.astype(np.float64)
+    t1, c1 = ctx.kendall_tau(x, y, "sorted")
+    t2, c2 = ctx.kendall_tau(x, y, "pairs")
+    assert c1.tolist() == c2.tolist() and t1 == t2
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    t3, c3 = ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), len(x))
+    assert c3.tolist() == c1.tolist() and t3 == t1
 
 
 def test_kendall_degenerate_error(ctx):
