@@ -1771,10 +1771,11 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
     d_body = (uint8_t*)talloc((size_t)nb);
     const int64_t nblk = ingest_block_count(nb);
     uint32_t* d_blk = (uint32_t*)talloc((size_t)(nblk + 1) * 4);
-    if (!d_body || !d_blk) return oom();
+    void* d_scan = talloc(ingest_scan_scratch_bytes(std::max<int64_t>(nblk, nb + 2)));  // >= lines
+    if (!d_body || !d_blk || !d_scan) return oom();
     DS_CUDA(cudaMemcpyAsync(d_body, body, (size_t)nb, cudaMemcpyHostToDevice, st));
     int64_t nlc = 0;
-    if (ingest_count_newlines(d_body, nb, d_blk, &nlc, st) != PARS_OK) return done(PARS_ERR_CUDA);
+    if (ingest_count_newlines(d_body, nb, d_blk, &nlc, d_scan, st) != PARS_OK) return done(PARS_ERR_CUDA);
     nlines = nlc + 1;  // the segment after the last '\n' (empty when the file ends with one)
     d_nl = (int64_t*)talloc((size_t)nlines * 8);
     if (!d_nl) return oom();
@@ -1784,7 +1785,7 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
     uint32_t* d_rank = (uint32_t*)talloc((size_t)(nlines + 1) * 4);
     if (!d_rank) return oom();
     ingest_launch_line_flags(d_nl, nlines, nb, d_rank, st);
-    ingest_launch_scan(d_rank, nlines, st);
+    ingest_launch_scan(d_rank, nlines, d_scan, st);
     uint32_t total = 0;
     DS_CUDA(cudaMemcpyAsync(&total, d_rank + nlines, 4, cudaMemcpyDeviceToHost, st));
     DS_CUDA(cudaStreamSynchronize(st));
@@ -1818,8 +1819,8 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
       d_pro = d->d_offsets;
       d_ido = d->d_id_offsets;
       ingest_launch_lengths(nrec, R, d_pro, d_ido, st);
-      ingest_launch_scan_i64(d_pro, nrec, st);
-      ingest_launch_scan_i64(d_ido, nrec, st);
+      ingest_launch_scan_i64(d_pro, nrec, d_scan, st);
+      ingest_launch_scan_i64(d_ido, nrec, d_scan, st);
       int64_t tot[2] = {0, 0};
       DS_CUDA(cudaMemcpyAsync(&tot[0], d_pro + nrec, 8, cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaMemcpyAsync(&tot[1], d_ido + nrec, 8, cudaMemcpyDeviceToHost, st));

@@ -3,7 +3,8 @@
 // offsets the featurizer reads without ever becoming std::string records
 // (SURVEY §8(f).2).
 //
-//   1. line split: '\n' counts per 4 KB block, one scan, newline positions;
+//   1. line split: '\n' counts per 16 KB block (16-byte loads, a SWAR
+//      per-byte test), one scan, newline positions;
 //   2. non-empty lines in file order, truncated to `limit` records
 //      (dataset.cpp:98-100: empty lines are skipped, the limit is checked
 //      before a line is parsed);
@@ -33,68 +34,191 @@ namespace pars_b200 {
 
 namespace {
 
-constexpr int kBlockBytes = 4096;  // bytes per line-split block (256 threads x 16)
+constexpr int kLineThreads = 256;
+constexpr int kLineVec = 4;                                // 16-byte loads per thread
+constexpr int kBlockBytes = kLineThreads * kLineVec * 16;  // bytes per line-split block (16 KB)
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void nl_count_kernel(const uint8_t* __restrict__ b, int64_t n, uint32_t* __restrict__ cnt) {
-  __shared__ uint32_t s;
-  if (threadIdx.x == 0) s = 0;
-  __syncthreads();
-  const int64_t p0 = (int64_t)blockIdx.x * kBlockBytes + threadIdx.x * 16;
-  uint32_t c = 0;
-  for (int k = 0; k < 16; ++k)
-    if (p0 + k < n && b[p0 + k] == '\n') ++c;
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s, c);
-  __syncthreads();
-  if (threadIdx.x == 0) cnt[blockIdx.x] = s;
+// 16-bit mask of the '\n' bytes among the 16 at p0 (zeros past n); the
+// per-byte zero test ((b & 0x7f) + 0x7f) | b has no cross-byte carries
+__device__ __forceinline__ uint32_t nl_mask16(const uint8_t* __restrict__ b, int64_t p0, int64_t n) {
+  uint32_t w[4];
+  if (p0 + 16 <= n) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(b + p0));
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t q = p0 + 4 * k + j;
+        x |= (uint32_t)(q < n ? b[q] : 0u) << (8 * j);
+      }
+      w[k] = x;
+    }
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t t = w[k] ^ 0x0a0a0a0au;
+    const uint32_t z = ~(((t & 0x7f7f7f7fu) + 0x7f7f7f7fu) | t) & 0x80808080u;  // bit 7 per '\n'
+    // gather bits 7, 15, 23, 31 into 4 consecutive bits
+    m |= (((z >> 7) * 0x204081u) >> 21 & 0xfu) << (4 * k);
+  }
+  return p0 < n ? m : 0u;
 }
 
-// exclusive scan of nb block counts (one CTA); total at cnt[nb]
-__global__ void scan_u32_kernel(uint32_t* __restrict__ cnt, int64_t nb) {
-  __shared__ uint32_t part[1024];
+__global__ void __launch_bounds__(kLineThreads) nl_count_kernel(const uint8_t* __restrict__ b,
+                                                                int64_t n, uint32_t* __restrict__ cnt) {
+  const int64_t p0 = (int64_t)blockIdx.x * kBlockBytes + threadIdx.x * 16;
+  uint32_t c = 0;
+#pragma unroll
+  for (int v = 0; v < kLineVec; ++v) c += __popc(nl_mask16(b, p0 + (int64_t)v * kLineThreads * 16, n));
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ uint32_t ws[kLineThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kLineThreads / 32; ++w) t += ws[w];
+    cnt[blockIdx.x] = t;
+  }
+}
+
+// newline positions in file order: the block's 16-byte groups are visited
+// group-major (v, then thread), which is byte order within the block
+__global__ void __launch_bounds__(kLineThreads) nl_write_kernel(const uint8_t* __restrict__ b,
+                                                                int64_t n,
+                                                                const uint32_t* __restrict__ boff,
+                                                                int64_t* __restrict__ nl) {
+  __shared__ uint32_t warp_tot[kLineThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t base = boff[blockIdx.x];
+#pragma unroll
+  for (int v = 0; v < kLineVec; ++v) {
+    const int64_t p0 = (int64_t)blockIdx.x * kBlockBytes + ((int64_t)v * kLineThreads + threadIdx.x) * 16;
+    uint32_t m = nl_mask16(b, p0, n);
+    const uint32_t c = __popc(m);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    uint32_t pos = base + x - c, tot = 0;
+    for (int w = 0; w < kLineThreads / 32; ++w) {
+      const uint32_t t = warp_tot[w];
+      if (w < warp) pos += t;
+      tot += t;
+    }
+    for (; m; m &= m - 1) nl[pos++] = p0 + __ffs(m) - 1;
+    base += tot;
+    __syncthreads();
+  }
+}
+
+// Exclusive scan in three passes (tile sums, one CTA over the sums, tiles
+// with their offsets); the total lands at v[n].
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sum_kernel(const T* __restrict__ v, int64_t n,
+                                                                     T* __restrict__ part) {
+  __shared__ T ws[kScanThreads / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  T s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanThreads + threadIdx.x;
+    if (i < n) s += v[i];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) scan_parts_kernel(T* __restrict__ part, int64_t nb,
+                                                          T* __restrict__ total) {
+  __shared__ T sh[1024];
   const int t = threadIdx.x;
   const int64_t per = (nb + 1023) / 1024;
-  const int64_t a = t * per, e = min(nb, a + per);
-  uint32_t s = 0;
-  for (int64_t k = a; k < e; ++k) s += cnt[k];
-  part[t] = s;
+  const int64_t a = t * per, e = a + per < nb ? a + per : nb;
+  T s = 0;
+  for (int64_t k = a; k < e; ++k) s += part[k];
+  sh[t] = s;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
-    const uint32_t v = t >= o ? part[t - o] : 0u;
+    const T x = t >= o ? sh[t - o] : (T)0;
     __syncthreads();
-    part[t] += v;
+    sh[t] += x;
     __syncthreads();
   }
-  uint32_t run = part[t] - s;
+  T run = sh[t] - s;
   for (int64_t k = a; k < e; ++k) {
-    const uint32_t c = cnt[k];
-    cnt[k] = run;
+    const T c = part[k];
+    part[k] = run;
     run += c;
   }
-  if (t == 1023) cnt[nb] = part[1023];
+  if (t == 1023) *total = sh[1023];
 }
 
-__global__ void nl_write_kernel(const uint8_t* __restrict__ b, int64_t n,
-                                const uint32_t* __restrict__ boff, int64_t* __restrict__ nl) {
-  __shared__ uint32_t warp_tot[8];
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_apply_kernel(T* __restrict__ v, int64_t n,
+                                                                       const T* __restrict__ part) {
+  __shared__ T sh[kScanTile];
+  __shared__ T ws[kScanThreads / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int j = k * kScanThreads + threadIdx.x;
+    sh[j] = base + j < n ? v[base + j] : (T)0;
+  }
+  __syncthreads();
+  T loc[kScanItems];
+  T s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    loc[k] = s;
+    s += sh[threadIdx.x * kScanItems + k];
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t p0 = (int64_t)blockIdx.x * kBlockBytes + threadIdx.x * 16;
-  uint32_t c = 0;
-  for (int k = 0; k < 16; ++k)
-    if (p0 + k < n && b[p0 + k] == '\n') ++c;
-  uint32_t x = c;
+  T x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) warp_tot[warp] = x;
+  if (lane == 31) ws[warp] = x;
   __syncthreads();
-  uint32_t base = boff[blockIdx.x];
-  for (int w = 0; w < warp; ++w) base += warp_tot[w];
-  uint32_t pos = base + x - c;
-  for (int k = 0; k < 16; ++k)
-    if (p0 + k < n && b[p0 + k] == '\n') nl[pos++] = p0 + k;
+  T off = part[blockIdx.x] + x - s;
+  for (int w = 0; w < warp; ++w) off += ws[w];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) sh[threadIdx.x * kScanItems + k] = off + loc[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int j = k * kScanThreads + threadIdx.x;
+    if (base + j < n) v[base + j] = sh[j];
+  }
+}
+
+template <typename T>
+void launch_scan(T* v, int64_t n, void* scratch, cudaStream_t st) {
+  const int64_t nb = std::max<int64_t>(1, ceil_div(n, kScanTile));
+  T* part = static_cast<T*>(scratch);
+  scan_tile_sum_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(v, n, part);
+  scan_parts_kernel<T><<<1, 1024, 0, st>>>(part, nb, v + n);
+  scan_tile_apply_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(v, n, part);
 }
 
 // line i = [start, end): start = nl[i-1] + 1 (0 for i = 0), end = nl[i] (n for
@@ -169,6 +293,28 @@ __device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t
   esc = false;
   dlen = 0;
   while (c.i < c.e) {
+    // fast path: 8 bytes at a time while they are plain ASCII (no quote,
+    // backslash, control character or byte >= 0x80); the first special byte
+    // (exact: the lowest flagged byte of the haszero tests) goes the slow way
+    if (c.i + 16 <= c.e) {
+      const uintptr_t addr = reinterpret_cast<uintptr_t>(c.p + c.i);
+      const uint64_t* a = reinterpret_cast<const uint64_t*>(addr & ~(uintptr_t)7);
+      const unsigned off = (unsigned)(addr & 7) * 8;
+      const uint64_t lo = a[0], hi = a[1];
+      const uint64_t x = off ? (lo >> off) | (hi << (64 - off)) : lo;
+      constexpr uint64_t k01 = 0x0101010101010101ull, k80 = 0x8080808080808080ull;
+      const uint64_t q = x ^ (k01 * '"'), bs = x ^ (k01 * '\\');
+      const uint64_t special = (((x - k01 * 0x20) & ~x) | ((q - k01) & ~q) | ((bs - k01) & ~bs) |
+                                x) & k80;
+      if (special == 0) {
+        c.i += 8;
+        dlen += 8;
+        continue;
+      }
+      const int plain = __ffsll((long long)special) / 8 - 1;  // bytes before the first special
+      c.i += plain;
+      dlen += plain;
+    }
     const uint32_t ch = c.p[c.i];
     if (ch == '"') {
       se = c.i;
@@ -806,30 +952,6 @@ void ingest_launch_samples(const uint8_t* text, int64_t nrec, const RecordOut& r
 }
 
 // exclusive scan of n int64 values (one CTA); total at v[n]
-__global__ void scan_i64_kernel(int64_t* __restrict__ v, int64_t n) {
-  __shared__ int64_t part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (n + 1023) / 1024;
-  const int64_t a = t * per, e = min(n, a + per);
-  int64_t s = 0;
-  for (int64_t k = a; k < e; ++k) s += v[k];
-  part[t] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int64_t x = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += x;
-    __syncthreads();
-  }
-  int64_t run = part[t] - s;
-  for (int64_t k = a; k < e; ++k) {
-    const int64_t c = v[k];
-    v[k] = run;
-    run += c;
-  }
-  if (t == 1023) v[n] = part[1023];
-}
-
 // decoded lengths of the records that parsed (others contribute 0)
 __global__ void lengths_kernel(int64_t nrec, RecordOut rec, int64_t* __restrict__ pr_len,
                                int64_t* __restrict__ id_len) {
@@ -852,7 +974,13 @@ __global__ void first_fail_kernel(int64_t nrec, RecordOut rec, const uint32_t* _
   if (fail) atomicMin(first, (unsigned long long)r);
 }
 
-void ingest_launch_scan_i64(int64_t* v, int64_t n, cudaStream_t st) { scan_i64_kernel<<<1, 1024, 0, st>>>(v, n); }
+size_t ingest_scan_scratch_bytes(int64_t n) {
+  return (size_t)std::max<int64_t>(1, ceil_div(n, kScanTile)) * 8 + 256;
+}
+
+void ingest_launch_scan_i64(int64_t* v, int64_t n, void* scratch, cudaStream_t st) {
+  launch_scan<int64_t>(v, n, scratch, st);
+}
 
 void ingest_launch_lengths(int64_t nrec, const RecordOut& rec, int64_t* pr_len, int64_t* id_len,
                            cudaStream_t st) {
@@ -868,10 +996,10 @@ void ingest_launch_first_fail(int64_t nrec, const RecordOut& rec, const uint32_t
 }
 
 int ingest_count_newlines(const uint8_t* d_text, int64_t n, uint32_t* d_blk, int64_t* total,
-                          cudaStream_t st) {
+                          void* scratch, cudaStream_t st) {
   const int64_t nb = std::max<int64_t>(1, ceil_div(n, kBlockBytes));
-  nl_count_kernel<<<(unsigned)nb, 256, 0, st>>>(d_text, n, d_blk);
-  scan_u32_kernel<<<1, 1024, 0, st>>>(d_blk, nb);
+  nl_count_kernel<<<(unsigned)nb, kLineThreads, 0, st>>>(d_text, n, d_blk);
+  launch_scan<uint32_t>(d_blk, nb, scratch, st);
   uint32_t t = 0;
   PARS_CUDA_CHECK(cudaMemcpyAsync(&t, d_blk + nb, 4, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -882,7 +1010,7 @@ int ingest_count_newlines(const uint8_t* d_text, int64_t n, uint32_t* d_blk, int
 void ingest_write_newlines(const uint8_t* d_text, int64_t n, const uint32_t* d_blk, int64_t* d_nl,
                            cudaStream_t st) {
   const int64_t nb = std::max<int64_t>(1, ceil_div(n, kBlockBytes));
-  nl_write_kernel<<<(unsigned)nb, 256, 0, st>>>(d_text, n, d_blk, d_nl);
+  nl_write_kernel<<<(unsigned)nb, kLineThreads, 0, st>>>(d_text, n, d_blk, d_nl);
 }
 
 int64_t ingest_block_count(int64_t n) { return std::max<int64_t>(1, ceil_div(n, kBlockBytes)); }
@@ -893,8 +1021,8 @@ void ingest_launch_line_flags(const int64_t* nl, int64_t nlines, int64_t n, uint
       nl, nlines, n, nonempty);
 }
 
-void ingest_launch_scan(uint32_t* v, int64_t n, cudaStream_t st) {
-  scan_u32_kernel<<<1, 1024, 0, st>>>(v, n);
+void ingest_launch_scan(uint32_t* v, int64_t n, void* scratch, cudaStream_t st) {
+  launch_scan<uint32_t>(v, n, scratch, st);
 }
 
 void ingest_launch_record_lines(const int64_t* nl, int64_t nlines, int64_t n, const uint32_t* rank,

@@ -44,13 +44,15 @@ struct RecordOut {
 int64_t ingest_block_count(int64_t n);
 // '\n' count of n bytes (block counts scanned into d_blk[0..nb], total back
 // on the host), then the newline positions in file order
+// Scratch for the scans below: ingest_scan_scratch_bytes(n) for n elements.
+size_t ingest_scan_scratch_bytes(int64_t n);
 int ingest_count_newlines(const uint8_t* d_text, int64_t n, uint32_t* d_blk, int64_t* total,
-                          cudaStream_t st);
+                          void* scratch, cudaStream_t st);
 void ingest_write_newlines(const uint8_t* d_text, int64_t n, const uint32_t* d_blk, int64_t* d_nl,
                            cudaStream_t st);
 void ingest_launch_line_flags(const int64_t* nl, int64_t nlines, int64_t n, uint32_t* nonempty,
                               cudaStream_t st);
-void ingest_launch_scan(uint32_t* v, int64_t n, cudaStream_t st);  // exclusive, total at v[n]
+void ingest_launch_scan(uint32_t* v, int64_t n, void* scratch, cudaStream_t st);  // exclusive, total at v[n]
 void ingest_launch_record_lines(const int64_t* nl, int64_t nlines, int64_t n, const uint32_t* rank,
                                 int64_t limit, int64_t* rb, int64_t* re, int64_t* rline,
                                 cudaStream_t st);
@@ -68,7 +70,7 @@ void ingest_launch_dups(const uint8_t* ids, const int64_t* id_off, int64_t nrec,
                         uint64_t cap, unsigned long long* tkey, unsigned long long* tmin,
                         uint32_t* dup, cudaStream_t st);
 
-void ingest_launch_scan_i64(int64_t* v, int64_t n, cudaStream_t st);  // exclusive, total at v[n]
+void ingest_launch_scan_i64(int64_t* v, int64_t n, void* scratch, cudaStream_t st);  // exclusive, total at v[n]
 void ingest_launch_lengths(int64_t nrec, const RecordOut& rec, int64_t* pr_len, int64_t* id_len,
                            cudaStream_t st);
 void ingest_launch_first_fail(int64_t nrec, const RecordOut& rec, const uint32_t* dup,
