@@ -1768,7 +1768,7 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
   uint8_t* d_body = nullptr;
   int64_t* d_nl = nullptr;
   if (nb > 0) {
-    d_body = (uint8_t*)talloc((size_t)nb);
+    d_body = (uint8_t*)talloc((size_t)nb + 16);  // word reads may pass the last byte
     const int64_t nblk = ingest_block_count(nb);
     uint32_t* d_blk = (uint32_t*)talloc((size_t)(nblk + 1) * 4);
     void* d_scan = talloc(ingest_scan_scratch_bytes(std::max<int64_t>(nblk, nb + 2)));  // >= lines
@@ -1800,7 +1800,7 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
       RecordOut R;
       R.err = (uint32_t*)talloc((size_t)nrec * 4);
       R.flags = (uint32_t*)talloc((size_t)nrec * 4);
-      int64_t** i64s[] = {&R.id_b, &R.id_e, &R.id_len, &R.pr_b, &R.pr_e, &R.pr_len,
+      int64_t** i64s[] = {&R.id_b, &R.id_e, &R.id_len, &R.pr_b, &R.pr_e, &R.pr_len, &R.pr_tok,
                           &R.out_len, &R.prompt_len, &R.sm_b, &R.sm_e};
       for (int64_t** q : i64s) {
         *q = (int64_t*)talloc((size_t)nrec * 8);

@@ -286,12 +286,22 @@ __device__ __forceinline__ int read_u4(Cur& c) {  // after "\u"
 
 // A string starting at the opening quote. On success: [sb, se) is the raw
 // content, esc = it contains escapes, dlen = decoded byte length.
-__device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t& dlen) {
+// With `tok`, also the whitespace-token count of the DECODED string
+// (whitespace_token_count, dataset.cpp:32-44: C-locale isspace bytes).
+__device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t& dlen,
+                            int64_t* tok = nullptr) {
   if (c.peek() != '"') return false;
   ++c.i;
   sb = c.i;
   esc = false;
   dlen = 0;
+  int64_t tk = 0;
+  bool prev_sp = true;
+  auto note = [&](uint32_t d) {  // one decoded byte
+    const bool sp = d == 0x20u || (d >= 9u && d <= 13u);
+    tk += (!sp && prev_sp) ? 1 : 0;
+    prev_sp = sp;
+  };
   while (c.i < c.e) {
     // fast path: 8 bytes at a time while they are plain ASCII (no quote,
     // backslash, control character or byte >= 0x80); the first special byte
@@ -306,19 +316,26 @@ __device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t
       const uint64_t q = x ^ (k01 * '"'), bs = x ^ (k01 * '\\');
       const uint64_t special = (((x - k01 * 0x20) & ~x) | ((q - k01) & ~q) | ((bs - k01) & ~bs) |
                                 x) & k80;
-      if (special == 0) {
-        c.i += 8;
-        dlen += 8;
-        continue;
+      const int plain = special == 0 ? 8 : __ffsll((long long)special) / 8 - 1;
+      if (tok && plain) {
+        // plain bytes hold no control characters: the only whitespace is ' '
+        constexpr uint64_t k7f = 0x7f7f7f7f7f7f7f7full;
+        const uint64_t t = x ^ (k01 * 0x20);
+        const uint64_t ns = (((t & k7f) + k7f) | t) & k80;  // bit 7: byte != ' '
+        const uint64_t lim = plain == 8 ? ~0ull : ((1ull << (8 * plain)) - 1);
+        const uint64_t prev = (ns << 8) | (prev_sp ? 0ull : 0x80ull);
+        tk += __popcll(ns & ~prev & lim);
+        prev_sp = ((ns >> (8 * plain - 1)) & 1ull) == 0;
       }
-      const int plain = __ffsll((long long)special) / 8 - 1;  // bytes before the first special
       c.i += plain;
       dlen += plain;
+      if (special == 0) continue;
     }
     const uint32_t ch = c.p[c.i];
     if (ch == '"') {
       se = c.i;
       ++c.i;
+      if (tok) *tok = tk;
       return true;
     }
     if (ch < 0x20) return false;  // control characters must be escaped
@@ -330,6 +347,7 @@ __device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t
       if (x == '"' || x == '\\' || x == '/' || x == 'b' || x == 'f' || x == 'n' || x == 'r' ||
           x == 't') {
         dlen += 1;
+        note(x == 'b' ? 8u : x == 'f' ? 12u : x == 'n' ? 10u : x == 'r' ? 13u : x == 't' ? 9u : x);
       } else if (x == 'u') {
         int cp = read_u4(c);
         if (cp < 0) return false;
@@ -339,10 +357,12 @@ __device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t
           const int lo = read_u4(c);
           if (lo < 0xDC00 || lo > 0xDFFF) return false;
           dlen += 4;
+          note(0x80u);
         } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
           return false;
         } else {
           dlen += cp < 0x80 ? 1 : (cp < 0x800 ? 2 : 3);
+          note(cp < 0x80 ? (uint32_t)cp : 0x80u);
         }
       } else {
         return false;
@@ -384,6 +404,7 @@ __device__ bool scan_string(Cur& c, int64_t& sb, int64_t& se, bool& esc, int64_t
       ++c.i;
     }
     dlen += 1 + more;
+    note(more ? 0x80u : ch);
   }
   return false;  // unterminated
 }
@@ -548,7 +569,7 @@ __global__ void parse_records_kernel(const uint8_t* __restrict__ text, const int
   if (r >= nrec) return;
   Cur c{text, rb[r], re[r]};
   uint32_t err = kIngOk;
-  int64_t id_b = 0, id_e = 0, pr_b = 0, pr_e = 0, id_dl = 0, pr_dl = 0, ol = -1, pl = -1;
+  int64_t id_b = 0, id_e = 0, pr_b = 0, pr_e = 0, id_dl = 0, pr_dl = 0, pr_tk = 0, ol = -1, pl = -1;
   int64_t sm_b = -1, sm_e = -1;
   uint32_t flags = 0;
   // which fields are present, and whether each is well-typed
@@ -589,9 +610,9 @@ __global__ void parse_records_kernel(const uint8_t* __restrict__ text, const int
           const bool is_id = ke - kb == 2;
           bool typed = false;
           if (ch == '"') {
-            int64_t sb, se, dl;
+            int64_t sb, se, dl, tk = 0;
             bool esc;
-            if (!scan_string(c, sb, se, esc, dl)) {
+            if (!scan_string(c, sb, se, esc, dl, is_id ? nullptr : &tk)) {
               ok = false;
               break;
             }
@@ -600,7 +621,7 @@ __global__ void parse_records_kernel(const uint8_t* __restrict__ text, const int
               id_b = sb, id_e = se, id_dl = dl;
               flags = esc ? (flags | kIngIdEsc) : (flags & ~kIngIdEsc);
             } else {
-              pr_b = sb, pr_e = se, pr_dl = dl;
+              pr_b = sb, pr_e = se, pr_dl = dl, pr_tk = tk;
               flags = esc ? (flags | kIngPromptEsc) : (flags & ~kIngPromptEsc);
             }
           } else if (!skip_value(c)) {
@@ -734,6 +755,7 @@ __global__ void parse_records_kernel(const uint8_t* __restrict__ text, const int
   out.pr_b[r] = pr_b;
   out.pr_e[r] = pr_e;
   out.pr_len[r] = pr_dl;
+  out.pr_tok[r] = pr_tk;
   out.out_len[r] = ol;
   out.prompt_len[r] = pl;
   out.sm_b[r] = sm_b;
@@ -794,9 +816,31 @@ __device__ void decode_string(const uint8_t* __restrict__ p, int64_t b, int64_t 
 
 }  // namespace
 
+// Warp copy of len raw bytes to an arbitrarily aligned destination: byte
+// head up to 4-byte alignment of dst, then one 4-byte store per lane per
+// step (each assembled from two aligned source words with a funnel shift;
+// the source buffer is padded so the second word may pass its end), then
+// the byte tail.
+__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                          int64_t len, int lane) {
+  const int64_t h4 = (int64_t)((4u - ((uint32_t)(uintptr_t)dst & 3u)) & 3u);
+  const int64_t head = len < h4 ? len : h4;
+  if (lane < head) dst[lane] = src[lane];
+  const int64_t nw = (len - head) >> 2;
+  const uint8_t* s0 = src + head;
+  uint32_t* d0 = reinterpret_cast<uint32_t*>(dst + head);
+  const uint32_t sh = ((uint32_t)(uintptr_t)s0 & 3u) * 8u;
+  const uint32_t* a0 = reinterpret_cast<const uint32_t*>((uintptr_t)s0 & ~(uintptr_t)3);
+  for (int64_t q = lane; q < nw; q += 32) {
+    const uint32_t lo = a0[q], hi = a0[q + 1];
+    d0[q] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+  }
+  for (int64_t k = head + nw * 4 + lane; k < len; k += 32) dst[k] = src[k];
+}
+
 // One warp per record: copy (or decode) the prompt and the id into their
-// arenas; count whitespace tokens of the decoded prompt when prompt_len is
-// absent (dataset.cpp:32-44; C-locale isspace).
+// arenas; prompt_len defaults to the whitespace token count of the decoded
+// prompt (dataset.cpp:32-44), counted by the parser.
 __global__ void emit_records_kernel(const uint8_t* __restrict__ text, int64_t nrec, RecordOut rec,
                                     const int64_t* __restrict__ pr_off, uint8_t* __restrict__ arena,
                                     const int64_t* __restrict__ id_off, uint8_t* __restrict__ ids,
@@ -812,8 +856,7 @@ __global__ void emit_records_kernel(const uint8_t* __restrict__ text, int64_t nr
   } else if (fl & kIngPromptEsc) {
     if (lane == 0) decode_string(text, rec.pr_b[r], rec.pr_e[r], dst);
   } else {
-    const uint8_t* src = text + rec.pr_b[r];
-    for (int64_t k = lane; k < len; k += 32) dst[k] = src[k];
+    warp_copy(text + rec.pr_b[r], dst, len, lane);
   }
   uint8_t* idd = ids + id_off[r];
   if (id_off[r + 1] == id_off[r]) {
@@ -824,26 +867,7 @@ __global__ void emit_records_kernel(const uint8_t* __restrict__ text, int64_t nr
     const uint8_t* src = text + rec.id_b[r];
     for (int64_t k = lane; k < id_off[r + 1] - id_off[r]; k += 32) idd[k] = src[k];
   }
-  __syncwarp();
-  if (rec.prompt_len[r] < 0) {
-    // token starts: a non-space byte whose predecessor is a space (or none)
-    int64_t cnt = 0;
-    for (int64_t k = lane; k < len; k += 32) {
-      const uint8_t ch = dst[k];
-      const bool sp = ch == ' ' || (ch >= 9 && ch <= 13);
-      bool prev_sp = true;
-      if (k > 0) {
-        const uint8_t q = dst[k - 1];
-        prev_sp = q == ' ' || (q >= 9 && q <= 13);
-      }
-      cnt += (!sp && prev_sp) ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) tokens[r] = cnt;
-  } else if (lane == 0) {
-    tokens[r] = rec.prompt_len[r];
-  }
+  if (lane == 0) tokens[r] = rec.prompt_len[r] < 0 ? (len ? rec.pr_tok[r] : 0) : rec.prompt_len[r];
 }
 
 // Duplicate ids: open addressing on the 64-bit FNV-1a of the decoded id

@@ -36,6 +36,7 @@ struct RecordOut {
   uint32_t* flags;
   int64_t *id_b, *id_e, *id_len;  // raw span (file offsets) and decoded length
   int64_t *pr_b, *pr_e, *pr_len;
+  int64_t* pr_tok;  // whitespace tokens of the decoded prompt
   int64_t* out_len;     // -1 when absent
   int64_t* prompt_len;  // -1 when absent
   int64_t *sm_b, *sm_e;  // the samples array's span ('[' .. ']'), -1 when absent
