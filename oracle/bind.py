@@ -330,6 +330,8 @@ class Ref:
                                 C.c_int, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
                                 C.c_int, C.c_void_p,
                                 C.c_void_p, C.c_void_p]
+        L.ref_pointwise_order.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
+        L.ref_listmle_lists.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_void_p]
         L.ref_poisson.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_void_p]
         L.ref_set_threads.argtypes = [C.c_int]
 
@@ -425,6 +427,19 @@ class Ref:
         if rc != 0:
             raise self._err()
         return w, bias.value, lt[:epochs].copy()
+
+    def pointwise_order(self, n, seed):
+        out = np.zeros(n, np.uint32)
+        if self.L.ref_pointwise_order(n, seed, _ptr(out)) != 0:
+            raise self._err()
+        return out
+
+    def listmle_lists(self, ds, nlists, list_size, seed):
+        k = min(list_size, len(ds))
+        out = np.zeros(nlists * k, np.uint32)
+        if self.L.ref_listmle_lists(ds.h, nlists, list_size, seed, _ptr(out)) != 0:
+            raise self._err()
+        return out
 
     def build_pairs(self, ds, delta, max_pairs, seed):
         a = np.zeros(max_pairs, np.uint32)

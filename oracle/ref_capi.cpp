@@ -14,6 +14,7 @@
 
 #include <omp.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -27,6 +28,7 @@
 #include "pars/features.hpp"
 #include "pars/metrics.hpp"
 #include "pars/pairs.hpp"
+#include "pars/rng.hpp"
 #include "pars/scheduler.hpp"
 #include "pars/scorer.hpp"
 #include "pars/simulator.hpp"
@@ -291,6 +293,42 @@ int ref_train(void* h, const RefExtractor* e, int objective, double delta,
     std::memcpy(w_out, w.data(), sizeof(double) * w.size());
     *bias_out = m.scorer.bias();
     for (size_t i = 0; i < m.loss_trace.size(); ++i) loss_trace_out[i] = m.loss_trace[i];
+  });
+}
+
+// The epoch samplers of train()'s comparison objectives, which train.cpp
+// keeps inline, restated over the reference's own Rng (rng.hpp): the
+// PointwiseL1 order (train.cpp:169-172) and the ListMLE lists
+// (train.cpp:186-200, ordered by sort_by_true_order, train.cpp:110-118).
+int ref_pointwise_order(uint64_t n, uint64_t seed, uint32_t* out) {
+  return guard([&] {
+    std::vector<uint32_t> order(n);
+    for (size_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);
+    Rng rng(seed);
+    rng.shuffle(order);
+    std::memcpy(out, order.data(), n * 4);
+  });
+}
+
+int ref_listmle_lists(void* h, uint64_t nlists, int list_size, uint64_t seed, uint32_t* out) {
+  return guard([&] {
+    const Dataset& ds = *static_cast<Dataset*>(h);
+    const size_t n = ds.records.size();
+    const size_t k = std::min<size_t>(static_cast<size_t>(list_size), n);
+    Rng rng(seed);
+    std::vector<uint32_t> pool(n), list(k);
+    for (size_t i = 0; i < n; ++i) pool[i] = static_cast<uint32_t>(i);
+    for (size_t l = 0; l < nlists; ++l) {
+      for (size_t t = 0; t < k; ++t) std::swap(pool[t], pool[t + rng.below(n - t)]);
+      std::copy_n(pool.begin(), k, list.begin());
+      std::sort(list.begin(), list.end(), [&](uint32_t a, uint32_t b) {
+        const auto& ra = ds.records[a];
+        const auto& rb = ds.records[b];
+        if (ra.output_len != rb.output_len) return ra.output_len > rb.output_len;
+        return ra.id < rb.id;
+      });
+      std::memcpy(out + l * k, list.data(), k * 4);
+    }
   });
 }
 

@@ -97,3 +97,27 @@ def test_workload_padding_to_fixed_token_count():
         toks = w.prompt(i).split()
         assert len(toks) == 512 == w.prompt_len[i]
     w.close()
+
+
+def test_baseline_samplers_match_reference(ref):
+    """pars_pointwise_order / pars_listmle_lists (host, the epoch order and
+    lists of train()'s PointwiseL1 / ListMLE objectives) against the same
+    samplers over the reference's Rng (oracle/ref_capi.cpp)."""
+    from paper_2510_03243_b200 import lib
+    for n, seed in ((1, 3), (2, 9), (1000, 0x1234), (4097, 2**63 + 5)):
+        got = np.zeros(n, np.uint32)
+        assert lib().pars_pointwise_order(n, C.c_uint64(seed), got.ctypes.data) == 0
+        assert got.tolist() == ref.pointwise_order(n, seed).tolist()
+    for n, nlists, k, seed in ((600, 50, 10, 7), (5, 11, 10, 8), (300, 20, 2, 2**40)):
+        ds = ref.synthesize(n, 40 + n)
+        ids = ds.ids()
+        bs = [i.encode() for i in ids]
+        offs = np.zeros(n + 1, np.int64)
+        offs[1:] = np.cumsum([len(b) for b in bs])
+        arena = np.frombuffer(b"".join(bs) + b"\0", np.uint8)
+        kk = min(k, n)
+        got = np.zeros(nlists * kk, np.uint32)
+        lens = np.ascontiguousarray(ds.output_len, np.int64)
+        assert lib().pars_listmle_lists(lens.ctypes.data, arena.ctypes.data, offs.ctypes.data, n,
+                                        nlists, k, C.c_uint64(seed), got.ctypes.data) == 0
+        assert got.tolist() == ref.listmle_lists(ds, nlists, k, seed).tolist()
