@@ -19,11 +19,12 @@ from ._lib import (  # noqa: F401
     length_gap_table,
     lib,
     pack_texts,
+    pinned_empty,
     tie_ranks,
 )
 
 __all__ = [
     "MODE_EXACT", "MODE_FAST", "Context", "Extractor", "Features", "ParsError", "Workload",
     "build_pairs", "device_count", "ids_arena", "length_gap_table", "lib", "pack_texts",
-    "tie_ranks",
+    "pinned_empty", "tie_ranks",
 ]

@@ -205,6 +205,29 @@ def length_gap_table(delta: float, max_len: int) -> np.ndarray:
     return t
 
 
+class _PinnedOwner:
+    """Keeps a pars_host_alloc block alive for the arrays viewing it."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        _check(lib().pars_host_alloc(max(nbytes, 1), C.byref(self.ptr)))
+
+    def __del__(self):
+        if self.ptr and lib is not None:
+            lib().pars_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """An uninitialised page-locked host array (pars_host_alloc): result
+    buffers that the C ABI fills by direct DMA (e.g. score_order's out=)."""
+    dt = np.dtype(dtype)
+    owner = _PinnedOwner(n * dt.itemsize)
+    buf = (C.c_uint8 * max(n * dt.itemsize, 1)).from_address(owner.ptr.value)
+    buf._owner = owner  # the ctypes buffer keeps the allocation alive
+    return np.frombuffer(buf, dtype=dt, count=n)
+
+
 def ids_arena(ids):
     bs = [i.encode() if isinstance(i, str) else bytes(i) for i in ids]
     offs = np.zeros(len(bs) + 1, np.int64)
@@ -445,12 +468,20 @@ class Context:
         return out
 
     def score_order(self, ex: Extractor, text: np.ndarray, offsets: np.ndarray, weights,
-                    tie_rank, boosted=None, bias: float = 0.0, mode: int = MODE_EXACT):
-        """enqueue + select_batch in one call: (scores, full admission order)."""
+                    tie_rank, boosted=None, bias: float = 0.0, mode: int = MODE_EXACT, out=None):
+        """enqueue + select_batch in one call: (scores, full admission order).
+        out: optional caller-owned (scores float64[n], order int64[n]) arrays,
+        reused across calls by a serving loop."""
         offs = _c(offsets, np.int64)
         n = len(offs) - 1
-        scores = np.zeros(max(n, 0), np.float64)
-        order = np.zeros(max(n, 0), np.int64)
+        if out is None:
+            scores = np.zeros(max(n, 0), np.float64)
+            order = np.zeros(max(n, 0), np.int64)
+        else:
+            scores, order = out
+            assert scores.dtype == np.float64 and order.dtype == np.int64
+            assert len(scores) >= n and len(order) >= n
+            assert scores.flags.c_contiguous and order.flags.c_contiguous
         t = text if isinstance(text, np.ndarray) else np.frombuffer(bytes(text), np.uint8)
         bst = None if boosted is None else _c(boosted, np.uint8)
         _check(lib().pars_score_order(self.h, C.byref(ex), _p(t), _p(offs), n,

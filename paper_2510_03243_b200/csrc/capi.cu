@@ -184,6 +184,21 @@ int check_ctx(pars_ctx* ctx) {
   return PARS_OK;
 }
 
+__global__ void u32_to_i64_kernel(const uint32_t* in, int64_t* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+// true when p is page-locked host memory the device can DMA into directly
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 __global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (float)in[i];
@@ -580,25 +595,50 @@ int pars_score_order(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   }
   Guard g(ctx);
   cudaStream_t st = ctx->stream;
-  // device layout: scores[n] | tie[n] | order[n] | boosted[n]
-  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * (8 + 4 + 4 + 1) + 64));
+  // device layout: scores[n] | order64[n] | tie[n] | order[n] | boosted[n]
+  PARS_TRY(ensure(ctx->pairs_in, (size_t)n * (8 + 8 + 4 + 4 + 1) + 64));
   double* d_s = (double*)ctx->pairs_in.p;
-  uint32_t* d_t = (uint32_t*)(d_s + n);
+  int64_t* d_o64 = (int64_t*)(d_s + n);
+  uint32_t* d_t = (uint32_t*)(d_o64 + n);
   uint32_t* d_o = d_t + n;
   uint8_t* d_b = (uint8_t*)(d_o + n);
+  // page-locked result buffers (a serving loop's, reused across calls) take
+  // the device->host copies directly: no staging, no host-side widening
+  const bool pin_s = is_pinned(scores), pin_o = is_pinned(order);
   PARS_TRY(ensure(ctx->sort, sort_scratch_bytes(n) + 4096));
-  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 16));
+  // pinned staging: scores[n] | order[n] (u32) | tie[n] (u32) | boosted[n]
+  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 17 + 64));
   double* h_sc = static_cast<double*>(ctx->h_scores.p);
   uint32_t* h_o = reinterpret_cast<uint32_t*>(h_sc + n);
-  PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, tie_rank, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-  if (boosted) PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, boosted, (size_t)n, cudaMemcpyHostToDevice, st));
+  uint32_t* h_t = h_o + n;
+  uint8_t* h_b = reinterpret_cast<uint8_t*>(h_t + n);
   std::vector<int64_t> chunks;
-  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, d_s, h_sc, &chunks));
+  PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, d_s,
+                               pin_s ? scores : h_sc, &chunks));
+  // the sort keys' tie ranks (and boost flags) follow the text on the copy
+  // stream, staged while the last chunks are scored, so the first text chunk
+  // is not queued behind them
+  cudaStream_t cs = ctx->copy_stream;
+  std::memcpy(h_t, tie_rank, (size_t)n * 4);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_t, h_t, (size_t)n * 4, cudaMemcpyHostToDevice, cs));
+  if (boosted) {
+    std::memcpy(h_b, boosted, (size_t)n);
+    PARS_CUDA_CHECK(cudaMemcpyAsync(d_b, h_b, (size_t)n, cudaMemcpyHostToDevice, cs));
+  }
+  PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_copy[0], cs));
+  PARS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copy[0], 0));
   PARS_TRY(launch_priority_sort(ctx, d_s, boosted ? d_b : nullptr, d_t, n, d_o, ctx->sort.p, st));
-  PARS_CUDA_CHECK(cudaMemcpyAsync(h_o, d_o, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
-  PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));  // overlaps the sort
+  if (pin_o) {
+    u32_to_i64_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_o, d_o64, n);
+    count_launch(ctx);
+    PARS_CUDA_CHECK(cudaMemcpyAsync(order, d_o64, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  } else {
+    PARS_CUDA_CHECK(cudaMemcpyAsync(h_o, d_o, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  }
+  if (!pin_s) PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));  // overlaps the sort
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
-  for (int64_t i = 0; i < n; ++i) order[i] = h_o[i];
+  if (!pin_o)
+    for (int64_t i = 0; i < n; ++i) order[i] = h_o[i];
   return PARS_OK;
 }
 

@@ -480,6 +480,25 @@ def test_score_order_fused_matches_two_calls_and_oracle(ctx, oracle):
     assert (order == oracle.select_order(arrival, ids, s2, boosted, 0.0)).all()
 
 
+@pytest.mark.parametrize("n", [1, 3000, 300_000])
+def test_score_order_into_pinned_buffers(ctx, n):
+    """Page-locked caller buffers take the scores and the order by direct DMA
+    (no staging); results equal the pageable-buffer call, across chunk
+    boundaries of the host pipeline (300k prompts = several chunks)."""
+    from paper_2510_03243_b200 import Extractor, Workload, pinned_empty
+    wl = Workload.synthesize(n, 5)
+    w = np.random.default_rng(2).normal(size=4096) * 0.05
+    tie = np.arange(n, dtype=np.uint32)[::-1].copy()
+    s1, o1 = ctx.score_order(Extractor.make(), wl.text, wl.offsets, w, tie)
+    outs = (pinned_empty(n, np.float64), pinned_empty(n, np.int64))
+    for _ in range(2):  # reused buffers
+        outs[0][:] = np.nan
+        outs[1][:] = -1
+        s2, o2 = ctx.score_order(Extractor.make(), wl.text, wl.offsets, w, tie, out=outs)
+        assert (s2.view(np.uint64) == s1.view(np.uint64)).all()
+        assert (o2 == o1).all()
+
+
 def test_dev_features_score_compact_rows_bit_identical(ctx, oracle):
     """pars_dev_features_score (the scoring step of the DP training step)
     over the compact (idx, count16) rows, row shards included, equals the
