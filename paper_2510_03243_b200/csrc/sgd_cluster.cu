@@ -327,6 +327,10 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
 
 __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L, const EpochArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
+  // the same bytes as 32-bit words: indexing it makes the staged rows / CSC
+  // entries explicit shared-memory loads (the staged-or-global pointers are
+  // generic, and generic loads of shared memory are slower)
+  extern __shared__ __align__(16) uint32_t smw[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -371,12 +375,22 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
         const uint32_t* row = slotptr[k];
         const uint32_t len = slotlen[k];
         const double inv = slotinv[k];
+        const uint32_t* rbuf = reinterpret_cast<const uint32_t*>(sm + L.rowbuf) + (size_t)buf * L.rowcap;
         double acc = 0.0;
         uint32_t e = 0;
+        if (row >= rbuf && row < rbuf + L.rowcap) {  // staged: shared-memory loads
+          const uint32_t* rs = smw + (L.rowbuf >> 2) + (size_t)buf * L.rowcap + (uint32_t)(row - rbuf);
 #pragma unroll 8
-        for (; e < len; ++e) {
-          const uint32_t E = row[e];
-          acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)(int16_t)(E & 0xffffu), inv)));
+          for (; e < len; ++e) {
+            const uint32_t E = rs[e];
+            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)(int16_t)(E & 0xffffu), inv)));
+          }
+        } else {
+#pragma unroll 8
+          for (; e < len; ++e) {
+            const uint32_t E = row[e];
+            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)(int16_t)(E & 0xffffu), inv)));
+          }
         }
         score[k] = __dadd_rn(acc, a.bias);
       }
@@ -415,18 +429,32 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     // phase C: gradient folds of this CTA's buckets, in (pair, a-before-b)
     // order, and the update w[d] -= (lr/bn) * g[d] (train.cpp:141-151)
     const double scale = __ddiv_rn(a.lr, (double)bn);
+    const uint32_t* cbuf = reinterpret_cast<const uint32_t*>(sm + L.cscbuf) + (size_t)buf * L.csccap;
+    const bool csc_staged = d.csc == cbuf;
+    const bool runs_staged = d.runs == reinterpret_cast<const uint2*>(sm + L.runbuf) + (size_t)buf * L.runcap;
+    const uint2* runs_s = reinterpret_cast<const uint2*>(smw + (L.runbuf >> 2)) + (size_t)buf * L.runcap;
     for (uint32_t r = tid; r < d.nruns; r += kThreads) {
-      const uint2 run = d.runs[r];
-      const uint32_t e1 = (r + 1 < d.nruns) ? d.runs[r + 1].y : d.ent_end;
+      const uint2 run = runs_staged ? runs_s[r] : d.runs[r];
+      const uint32_t e1 =
+          (r + 1 < d.nruns) ? (runs_staged ? runs_s[r + 1].y : d.runs[r + 1].y) : d.ent_end;
       // g starts at +0.0 and is never -0.0 under round-to-nearest, so the
       // +-0.0 terms of inactive pairs leave it unchanged: branch-free fold
       double g = 0.0;
-      const uint32_t* csc = d.csc - d.ent_base;
       uint32_t e = run.y;
+      if (csc_staged) {  // shared-memory loads
+        const uint32_t* cs = smw + (L.cscbuf >> 2) + (size_t)buf * L.csccap - d.ent_base;
 #pragma unroll 8
-      for (; e < e1; ++e) {
-        const uint32_t E = csc[e];
-        g = __dadd_rn(g, __dmul_rn((double)(int16_t)(E & 0xffffu), sinv[E >> 16]));
+        for (; e < e1; ++e) {
+          const uint32_t E = cs[e];
+          g = __dadd_rn(g, __dmul_rn((double)(int16_t)(E & 0xffffu), sinv[E >> 16]));
+        }
+      } else {
+        const uint32_t* csc = d.csc - d.ent_base;
+#pragma unroll 8
+        for (; e < e1; ++e) {
+          const uint32_t E = csc[e];
+          g = __dadd_rn(g, __dmul_rn((double)(int16_t)(E & 0xffffu), sinv[E >> 16]));
+        }
       }
       if (g != 0.0) {
         const double nw = __dsub_rn(W[run.x], __dmul_rn(scale, g));
