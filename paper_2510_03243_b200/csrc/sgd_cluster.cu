@@ -160,6 +160,38 @@ __global__ void slot_table_kernel(const uint32_t* __restrict__ pa, const uint32_
                         (uint32_t)(iv >> 32));
 }
 
+// Score chain over a staged (shared-memory) row: the raw entries are read two
+// groups of 4 ahead and the weights one group ahead of the __dadd_rn chain,
+// so the chain does not wait on the load -> dependent gather latency.
+__device__ __forceinline__ double cnt_of(uint32_t E) { return (double)(int16_t)(E & 0xffffu); }
+
+__device__ __forceinline__ double chain_row_s(const uint32_t* __restrict__ rs, uint32_t len, double inv,
+                                              const double* __restrict__ W) {
+  double acc = 0.0;
+  const uint32_t ng = len >> 2;
+  if (ng >= 2) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(rs);
+    uint4 A = r4[0], B = r4[1];
+    double w0 = W[A.x >> 16], w1 = W[A.y >> 16], w2 = W[A.z >> 16], w3 = W[A.w >> 16];
+    for (uint32_t g = 0; g < ng; ++g) {
+      const uint4 Cn = g + 2 < ng ? r4[g + 2] : B;
+      const double v0 = W[B.x >> 16], v1 = W[B.y >> 16], v2 = W[B.z >> 16], v3 = W[B.w >> 16];
+      acc = __dadd_rn(acc, __dmul_rn(w0, __dmul_rn(cnt_of(A.x), inv)));
+      acc = __dadd_rn(acc, __dmul_rn(w1, __dmul_rn(cnt_of(A.y), inv)));
+      acc = __dadd_rn(acc, __dmul_rn(w2, __dmul_rn(cnt_of(A.z), inv)));
+      acc = __dadd_rn(acc, __dmul_rn(w3, __dmul_rn(cnt_of(A.w), inv)));
+      A = B;
+      B = Cn;
+      w0 = v0, w1 = v1, w2 = v2, w3 = v3;
+    }
+  }
+  for (uint32_t e = ng >= 2 ? ng << 2 : 0; e < len; ++e) {
+    const uint32_t E = rs[e];
+    acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn(cnt_of(E), inv)));
+  }
+  return acc;
+}
+
 // ---- the cluster epoch kernel ------------------------------------------------
 struct Layout {
   uint32_t dim, B, spc, ppc;  // slots / pairs per CTA
@@ -380,11 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
         uint32_t e = 0;
         if (row >= rbuf && row < rbuf + L.rowcap) {  // staged: shared-memory loads
           const uint32_t* rs = smw + (L.rowbuf >> 2) + (size_t)buf * L.rowcap + (uint32_t)(row - rbuf);
-#pragma unroll 8
-          for (; e < len; ++e) {
-            const uint32_t E = rs[e];
-            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)(int16_t)(E & 0xffffu), inv)));
-          }
+          acc = chain_row_s(rs, len, inv, W);
         } else {
 #pragma unroll 8
           for (; e < len; ++e) {
