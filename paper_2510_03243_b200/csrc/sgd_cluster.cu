@@ -192,6 +192,41 @@ __device__ __forceinline__ double chain_row_s(const uint32_t* __restrict__ rs, u
   return acc;
 }
 
+// Gradient fold of one bucket's run over staged (shared-memory) CSC entries,
+// same prefetch scheme: raw entries two groups of 4 ahead, the slots' signed
+// L2 factors one group ahead of the add chain.
+__device__ __forceinline__ double chain_run_s(const uint32_t* __restrict__ cs, uint32_t b, uint32_t e1,
+                                              const double* __restrict__ sinv) {
+  double g = 0.0;
+  uint32_t e = b;
+  const uint32_t ng = (e1 - b) >> 2;
+  if (ng >= 2) {
+    uint32_t a0 = cs[e], a1 = cs[e + 1], a2 = cs[e + 2], a3 = cs[e + 3];
+    uint32_t b0 = cs[e + 4], b1 = cs[e + 5], b2 = cs[e + 6], b3 = cs[e + 7];
+    double s0 = sinv[a0 >> 16], s1 = sinv[a1 >> 16], s2 = sinv[a2 >> 16], s3 = sinv[a3 >> 16];
+    for (uint32_t k = 0; k < ng; ++k) {
+      const uint32_t o = e + 8;
+      const bool more = k + 2 < ng;
+      const uint32_t c0 = more ? cs[o] : b0, c1 = more ? cs[o + 1] : b1;
+      const uint32_t c2 = more ? cs[o + 2] : b2, c3 = more ? cs[o + 3] : b3;
+      const double t0 = sinv[b0 >> 16], t1 = sinv[b1 >> 16], t2 = sinv[b2 >> 16], t3 = sinv[b3 >> 16];
+      g = __dadd_rn(g, __dmul_rn(cnt_of(a0), s0));
+      g = __dadd_rn(g, __dmul_rn(cnt_of(a1), s1));
+      g = __dadd_rn(g, __dmul_rn(cnt_of(a2), s2));
+      g = __dadd_rn(g, __dmul_rn(cnt_of(a3), s3));
+      a0 = b0, a1 = b1, a2 = b2, a3 = b3;
+      b0 = c0, b1 = c1, b2 = c2, b3 = c3;
+      s0 = t0, s1 = t1, s2 = t2, s3 = t3;
+      e += 4;
+    }
+  }
+  for (; e < e1; ++e) {
+    const uint32_t E = cs[e];
+    g = __dadd_rn(g, __dmul_rn(cnt_of(E), sinv[E >> 16]));
+  }
+  return g;
+}
+
 // ---- the cluster epoch kernel ------------------------------------------------
 struct Layout {
   uint32_t dim, B, spc, ppc;  // slots / pairs per CTA
@@ -471,11 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
       uint32_t e = run.y;
       if (csc_staged) {  // shared-memory loads
         const uint32_t* cs = smw + (L.cscbuf >> 2) + (size_t)buf * L.csccap - d.ent_base;
-#pragma unroll 8
-        for (; e < e1; ++e) {
-          const uint32_t E = cs[e];
-          g = __dadd_rn(g, __dmul_rn((double)(int16_t)(E & 0xffffu), sinv[E >> 16]));
-        }
+        g = chain_run_s(cs, e, e1, sinv);
       } else {
         const uint32_t* csc = d.csc - d.ent_base;
 #pragma unroll 8
