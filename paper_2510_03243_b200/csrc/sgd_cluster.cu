@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
   double epoch_loss = 0.0;
   unsigned long long active = 0;
 #ifdef PARS_SGD_TIMING
-  long long tt[6] = {0, 0, 0, 0, 0, 0};
+  long long tt[6] = {0, 0, 0, 0, 0, 0};  // [0] warp 0's chains, [5] the staging warps
 #endif
   for (int64_t q = 0; q < nb; ++q) {
 #ifdef PARS_SGD_TIMING
@@ -537,12 +537,12 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     cluster.sync();
 #ifdef PARS_SGD_TIMING
     long long c5 = clock64();
-    tt[0] += c1 - c0; tt[1] += c2 - c1; tt[2] += c3 - c2; tt[3] += c4 - c3; tt[4] += c5 - c4;
+    tt[warp == 0 ? 0 : 5] += c1 - c0; tt[1] += c2 - c1; tt[2] += c3 - c2; tt[3] += c4 - c3; tt[4] += c5 - c4;
 #endif
   }
 #ifdef PARS_SGD_TIMING
   if (a.timing) {
-    for (int k = 0; k < 5; ++k) atomicMax(&a.timing[(rank * kThreads + tid) * 0 + k * 8 + rank], tt[k]);
+    for (int k = 0; k < 6; ++k) atomicMax(&a.timing[k * 8 + rank], tt[k]);
   }
 #endif
   if (rank == 0) {
@@ -657,8 +657,8 @@ int launch_sgd_cluster(pars_ctx* ctx, const int64_t* rp, const uint32_t* cpk,
     long long h[64];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost);
-    const char* names[5] = {"phaseA+stage", "sync1", "phaseC", "cp.wait", "sync2"};
-    for (int k = 0; k < 5; ++k) {
+    const char* names[6] = {"chains(w0)", "sync1", "phaseC", "cp.wait", "sync2", "stage(w1-7)"};
+    for (int k = 0; k < 6; ++k) {
       fprintf(stderr, "%-14s", names[k]);
       for (int r = 0; r < kCL; ++r) fprintf(stderr, " %8.0f", (double)h[k * 8 + r] / (double)nb);
       fprintf(stderr, "\n");
