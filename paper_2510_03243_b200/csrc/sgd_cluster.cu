@@ -37,7 +37,9 @@ namespace {
 
 constexpr int kCL = kSgdCluster;  // CTAs per cluster
 constexpr int kThreads = 256;
-constexpr int kBuildThreads = 256;
+constexpr int kBuildThreads = 1024;  // one warp per slot of a placement round
+constexpr int kBuildWarps = kBuildThreads / 32;
+constexpr int kRegEntries = 12;      // row entries per lane kept in registers
 
 // ---- compact rows ----------------------------------------------------------
 __global__ void cpk_build_kernel(const int64_t* __restrict__ rp, const uint32_t* __restrict__ idx,
@@ -65,8 +67,10 @@ __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
     const uint32_t* __restrict__ cpk_off, uint32_t dim, const uint32_t* __restrict__ pa,
     const uint32_t* __restrict__ pb, int64_t npairs, int32_t B,
     const int64_t* __restrict__ ent_off, uint32_t* __restrict__ ent, uint2* __restrict__ runs,
-    uint32_t* __restrict__ nruns, uint32_t* __restrict__ rb, uint4* __restrict__ desc4) {
-  extern __shared__ uint32_t cur[];  // [dim] counts -> cursors
+    uint32_t* __restrict__ nruns, uint32_t* __restrict__ rb, uint4* __restrict__ desc4,
+    const uint4* __restrict__ slots) {
+  extern __shared__ uint32_t cur[];  // [dim] counts -> cursors, then [dim] slot masks
+  uint32_t* mask = cur + dim;
   __shared__ uint32_t part[kBuildThreads], rpart[kBuildThreads];
   const int64_t q = blockIdx.x;
   const int64_t p0 = q * B;
@@ -75,11 +79,14 @@ __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
   const int64_t base = ent_off[q];
   for (uint32_t d = threadIdx.x; d < dim; d += kBuildThreads) cur[d] = 0;
   __syncthreads();
-  for (int k = 0; k < S; ++k) {
-    const uint32_t r = (k & 1) ? pb[p0 + (k >> 1)] : pa[p0 + (k >> 1)];
-    const uint32_t* row = cpk + cpk_off[r];
-    const int len = (int)(rp[r + 1] - rp[r]);
-    for (int e = threadIdx.x; e < len; e += kBuildThreads) atomicAdd(&cur[row[e] >> 16], 1u);
+  // slot k's row from the epoch's slot table (slot_table_kernel): one warp
+  // per slot, coalesced over the row
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = w; k < S; k += kBuildWarps) {
+    const uint4 m = slots[2 * p0 + k];
+    const uint32_t* row = cpk + m.x;
+#pragma unroll 4
+    for (int e = lane; e < (int)m.y; e += 32) atomicAdd(&cur[row[e] >> 16], 1u);
   }
   __syncthreads();
   const uint32_t chunk = (dim + kBuildThreads - 1) / kBuildThreads;
@@ -130,17 +137,51 @@ __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
     desc4[q * kCL + threadIdx.x] =
         make_uint4(r0, r1, r0 < nr ? rq[r0].y : total, r1 < nr ? rq[r1].y : total);
   }
-  for (int k = 0; k < S; ++k) {
-    const uint32_t r = (k & 1) ? pb[p0 + (k >> 1)] : pa[p0 + (k >> 1)];
-    const uint32_t* row = cpk + cpk_off[r];
-    const int len = (int)(rp[r + 1] - rp[r]);
-    for (int e = threadIdx.x; e < len; e += kBuildThreads) {
-      const uint32_t E = row[e];
-      const uint32_t d = E >> 16;
-      const uint32_t pos = cur[d];
-      cur[d] = pos + 1;
-      ent[base + pos] = ((uint32_t)k << 16) | (E & 0xffffu);
+  // Stable placement, one warp per slot, kBuildWarps slots per round: a
+  // bucket's entries from the round's slots go in slot order, ranked by the
+  // bits of the lower warps in the bucket's slot mask (a row holds each bucket
+  // at most once); the lowest warp of each bucket then advances its cursor.
+  // A lane keeps its first kRegEntries entries of the row in registers across
+  // the three passes (longer rows re-read their tail).
+  for (uint32_t d = threadIdx.x; d < dim; d += kBuildThreads) mask[d] = 0;
+  __syncthreads();
+  const uint32_t below = (1u << w) - 1u;
+  for (int k0 = 0; k0 < S; k0 += kBuildWarps) {
+    const int k = k0 + w;
+    const uint32_t* row = nullptr;
+    int len = 0;
+    if (k < S) {
+      const uint4 m = slots[2 * p0 + k];
+      row = cpk + m.x;
+      len = (int)m.y;
     }
+    uint32_t R[kRegEntries];
+#pragma unroll
+    for (int j = 0; j < kRegEntries; ++j) {
+      const int e = lane + 32 * j;
+      R[j] = e < len ? row[e] : 0u;
+    }
+    auto each = [&](auto&& f) {
+#pragma unroll
+      for (int j = 0; j < kRegEntries; ++j)
+        if (lane + 32 * j < len) f(R[j]);
+      for (int e = lane + 32 * kRegEntries; e < len; e += 32) f(row[e]);
+    };
+    each([&](uint32_t E) { atomicOr(&mask[E >> 16], 1u << w); });
+    __syncthreads();
+    each([&](uint32_t E) {
+      const uint32_t d = E >> 16;
+      ent[base + cur[d] + __popc(mask[d] & below)] = ((uint32_t)k << 16) | (E & 0xffffu);
+    });
+    __syncthreads();
+    each([&](uint32_t E) {
+      const uint32_t d = E >> 16;
+      const uint32_t m = mask[d];
+      if (m && !(m & below)) {  // the bucket's lowest warp this round
+        cur[d] += __popc(m);
+        mask[d] = 0;
+      }
+    });
     __syncthreads();
   }
 }
@@ -598,13 +639,13 @@ int launch_sgd_cluster(pars_ctx* ctx, const int64_t* rp, const uint32_t* cpk,
   uint32_t* rb = (uint32_t*)take((size_t)nb * (kCL + 1) * 4);
   uint4* desc4 = (uint4*)take((size_t)nb * kCL * 16);
   uint4* slots = (uint4*)take((size_t)npairs * 2 * 16);
-  const size_t build_smem = (size_t)dim * 4;
+  const size_t build_smem = (size_t)dim * 8;  // cursors + slot masks
   PARS_CUDA_CHECK(cudaFuncSetAttribute(csc_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)build_smem));
-  csc_build_kernel<<<(unsigned)nb, kBuildThreads, build_smem, st>>>(
-      rp, cpk, cpk_off, dim, a, b, npairs, B, ent_off, ent, runs, nruns, rb, desc4);
   slot_table_kernel<<<(unsigned)ceil_div(2 * npairs, 256), 256, 0, st>>>(a, b, npairs, rp, cpk_off,
                                                                          inv_row, slots);
+  csc_build_kernel<<<(unsigned)nb, kBuildThreads, build_smem, st>>>(
+      rp, cpk, cpk_off, dim, a, b, npairs, B, ent_off, ent, runs, nruns, rb, desc4, slots);
   const Layout L = make_layout(dim, (uint32_t)B, kSgdRowCap, kSgdCscCap, kSgdRunCap);
   PARS_CUDA_CHECK(cudaFuncSetAttribute(sgd_cluster_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
