@@ -189,3 +189,23 @@ def test_loaded_dataset_scores_like_reference(ctx, ref, tmp_path):
     ref.L.ref_score_batch(ctypes.byref(OEx.make()), ds.h, w.ctypes.data, ctypes.c_double(0.0),
                           want.ctypes.data)
     assert (out.cpu().numpy().view(np.uint64) == want.view(np.uint64)).all()
+
+
+def test_loader_token_counts_and_escapes_at_every_offset(ctx, ref, tmp_path):
+    """prompt_len defaults to the whitespace-token count of the DECODED prompt:
+    escaped whitespace (\\t \\n \\r \\f \\u0020 \\u000b) splits tokens, escaped
+    non-space does not, and raw UTF-8 / escapes land at every offset
+    relative to the parser's 8-byte fast path."""
+    rng = np.random.default_rng(17)
+    pieces = ["a", "bb", "ccc ", " ", "  ", "\\t", "\\n", "\\r", "\\f", "\\u0020", "\\u000b",
+              "\\u00e9", "\\ud83d\\ude00", "\\\"", "\\\\", "\\/", "x" * 13, "é", "中",
+              "😀", "\\u0041", "\\b"]
+    lines = [HEADER]
+    for i in range(4000):
+        k = int(rng.integers(0, 60))
+        body = "".join(pieces[int(j)] for j in rng.integers(0, len(pieces), k))
+        body = " " * int(rng.integers(0, 9)) + body + "z"  # shift the alignment; >= 1 token
+        lines.append('{"id":"e%05d","prompt":"%s","output_len":%d}' % (i, body, 1 + i % 7))
+    p = tmp_path / "esc.jsonl"
+    _write(p, lines)
+    assert _compare(ctx, ref, p) == 4000
