@@ -41,7 +41,8 @@ namespace pars_b200 {
 
 namespace {
 
-constexpr int kBuildThreads = 256;
+constexpr int kBuildThreads = 1024;
+constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr int kStepThreads = 1024;
 constexpr int kG = 8;                        // lanes per slot in phase A
 constexpr int kD = 4;                        // entries in flight per lane
@@ -56,19 +57,21 @@ __global__ void __launch_bounds__(kBuildThreads) slot_build_kernel(
     const int64_t* __restrict__ soff, const int64_t* __restrict__ ent_off,
     uint32_t* __restrict__ ent_slot, double* __restrict__ ent_val, uint32_t* __restrict__ run_d,
     uint32_t* __restrict__ run_beg, uint32_t* __restrict__ nruns) {
-  extern __shared__ uint32_t cur[];  // [dim] counts -> cursors
+  extern __shared__ uint32_t cur[];  // [dim] counts -> cursors, then [dim] slot masks
+  uint32_t* mask = cur + dim;
   __shared__ uint32_t part[kBuildThreads];
   __shared__ uint32_t rpart[kBuildThreads];
   const int64_t q = blockIdx.x;
   const int64_t s0 = soff[q];
   const int S = (int)(soff[q + 1] - s0);
   const int64_t base = ent_off[q];
-  for (uint32_t d = threadIdx.x; d < dim; d += kBuildThreads) cur[d] = 0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t d = threadIdx.x; d < dim; d += kBuildThreads) cur[d] = 0, mask[d] = 0;
   __syncthreads();
-  for (int k = 0; k < S; ++k) {
+  for (int k = w; k < S; k += kBuildWarps) {  // one warp per slot
     const uint32_t r = srow[s0 + k];
-    for (int64_t e = rp[r] + threadIdx.x; e < rp[r + 1]; e += kBuildThreads)
-      atomicAdd(&cur[idx[e]], 1u);
+    const int64_t e0 = rp[r], e1 = rp[r + 1];
+    for (int64_t e = e0 + lane; e < e1; e += 32) atomicAdd(&cur[idx[e]], 1u);
   }
   __syncthreads();
   const uint32_t chunk = (dim + kBuildThreads - 1) / kBuildThreads;
@@ -104,14 +107,35 @@ __global__ void __launch_bounds__(kBuildThreads) slot_build_kernel(
   }
   if (threadIdx.x == kBuildThreads - 1) nruns[q] = rrun;
   __syncthreads();
-  for (int k = 0; k < S; ++k) {
-    const uint32_t r = srow[s0 + k];
-    for (int64_t e = rp[r] + threadIdx.x; e < rp[r + 1]; e += kBuildThreads) {
+  // Stable placement, kBuildWarps slots per round (one warp each): a
+  // bucket's entries from the round's slots go in slot order, ranked by the
+  // lower warps' bits in the bucket's slot mask (a row holds each bucket once);
+  // the lowest warp of each bucket then advances its cursor.
+  const uint32_t below = (1u << w) - 1u;
+  for (int k0 = 0; k0 < S; k0 += kBuildWarps) {
+    const int k = k0 + w;
+    int64_t e0 = 0, e1 = 0;
+    if (k < S) {
+      const uint32_t r = srow[s0 + k];
+      e0 = rp[r];
+      e1 = rp[r + 1];
+    }
+    for (int64_t e = e0 + lane; e < e1; e += 32) atomicOr(&mask[idx[e]], 1u << w);
+    __syncthreads();
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
       const uint32_t d = idx[e];
-      const uint32_t pos = cur[d];
-      cur[d] = pos + 1;
+      const uint32_t pos = cur[d] + __popc(mask[d] & below);
       ent_slot[base + pos] = (uint32_t)k;
       ent_val[base + pos] = val[e];
+    }
+    __syncthreads();
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const uint32_t d = idx[e];
+      const uint32_t m = mask[d];
+      if (m && !(m & below)) {  // the bucket's lowest warp this round
+        cur[d] += __popc(m);
+        mask[d] = 0;
+      }
     }
     __syncthreads();
   }
@@ -316,7 +340,7 @@ int launch_baseline_epoch(pars_ctx* ctx, int kind, const int64_t* rp, const uint
                                   cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(soff, h_soff, (size_t)(nb + 1) * 8, cudaMemcpyHostToDevice, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(srow, h_srow, (size_t)nslots * 4, cudaMemcpyHostToDevice, st));
-  const size_t build_smem = (size_t)dim * 4;
+  const size_t build_smem = (size_t)dim * 8;  // cursors + slot masks
   PARS_CUDA_CHECK(cudaFuncSetAttribute(slot_build_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)build_smem));
