@@ -592,8 +592,20 @@ __host__ inline bool use_seq(const FeatConfig& c) {
 
 // 4 bytes at aligned position r of the aligned base a0; the prompt occupies
 // [lo, hi), bytes outside it read as ' '.
-__device__ __forceinline__ uint32_t seq_word(const uint8_t* a0, int r, int lo, int hi) {
+// The 4 bytes at a0 + r (4-aligned) with those outside the prompt [lo, hi)
+// read as spaces. A word straddling a prompt edge is still one aligned load
+// when it lies inside the buffer's readable range [rlo, rhi); only a word
+// crossing the buffer's own ends is assembled byte by byte.
+__device__ __forceinline__ uint32_t seq_word(const uint8_t* a0, int r, int lo, int hi, int rlo,
+                                             int rhi) {
   if (r >= lo && r + 4 <= hi) return __ldg(reinterpret_cast<const uint32_t*>(a0 + r));
+  if (r + 4 <= lo || r >= hi) return 0x20202020u;
+  if (r >= rlo && r + 4 <= rhi) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a0 + r));
+    const int k0 = lo > r ? lo - r : 0, k1 = hi - r < 4 ? hi - r : 4;  // valid bytes [k0, k1)
+    const uint32_t keep = (k1 >= 4 ? 0xffffffffu : ((1u << (8 * k1)) - 1u)) & ~((1u << (8 * k0)) - 1u);
+    return (w & keep) | (0x20202020u & ~keep);
+  }
   uint32_t w = 0x20202020u;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -618,11 +630,17 @@ __device__ __forceinline__ void seq_emit(uint32_t cbase, uint32_t bbase, uint32_
 }
 
 __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpSmem& S,
-                                                const uint8_t* base, int len, int lane) {
+                                                const uint8_t* base, int len, int lane,
+                                                const uint8_t* buf_lo, const uint8_t* buf_hi) {
   if (len <= 0) return;
   const int mis = (int)(reinterpret_cast<uintptr_t>(base) & 3u);
   const uint8_t* a0 = base - mis;
   const int lo = mis, hi = mis + len;
+  // the buffer's readable bytes relative to a0 (clamped to this prompt's
+  // neighbourhood; the text of all prompts of the launch is readable)
+  const int64_t dlo = buf_lo - a0, dhi = buf_hi - a0;
+  const int rlo = dlo > 0 ? (int)dlo : 0;
+  const int rhi = dhi < (int64_t)hi + 8 ? (int)dhi : hi + 8;
   const int wpl = (((hi + 3) >> 2) + 31) >> 5;  // words per lane
   const int cs = lane * wpl * 4, ce = cs + wpl * 4;
   if (cs >= hi) return;
@@ -631,12 +649,12 @@ __device__ __forceinline__ void hash_prompt_seq(const FeatConfig& c, const WarpS
   const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(S.bitmap);
   const uint32_t dummy = bbase + (c.dim / 8) + 4u * lane;
   const uint32_t m1 = (c.dim / 2 - 1) << 2, m2 = (c.dim / 32 - 1) << 2;
-  uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi)) >> 2 : 0u;
+  uint32_t prev2 = cs > 0 ? nonspace_nibble(seq_word(a0, cs - 4, lo, hi, rlo, rhi)) >> 2 : 0u;
   uint32_t hw = sw, A = 0, B = 0, carry = 0;
   // two words (8 bytes) per iteration: the mask logic runs once per 8 bytes
-  uint32_t w0 = seq_word(a0, cs, lo, hi), w1 = seq_word(a0, cs + 4, lo, hi);
+  uint32_t w0 = seq_word(a0, cs, lo, hi, rlo, rhi), w1 = seq_word(a0, cs + 4, lo, hi, rlo, rhi);
   for (int r = cs;; r += 8) {
-    const uint32_t n0 = seq_word(a0, r + 8, lo, hi), n1 = seq_word(a0, r + 12, lo, hi);
+    const uint32_t n0 = seq_word(a0, r + 8, lo, hi, rlo, rhi), n1 = seq_word(a0, r + 12, lo, hi, rlo, rhi);
     const uint32_t ns = nonspace_nibble(w0) | (nonspace_nibble(w1) << 4);
     const uint32_t E = (ns << 2) | prev2;  // bit k+2: byte r+k is not a space
     const uint32_t start = ns & ~(E >> 1);
@@ -683,6 +701,9 @@ __global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, 
   uint16_t* c16 = reinterpret_cast<uint16_t*>(S.counts);
 
   uint32_t* lists = (MODE == kFeatScoreExact) ? a.lists + (size_t)gw * a.list_cap : nullptr;
+  // readable text of this launch: the bytes of its prompts, offsets[0] .. offsets[n]
+  const uint8_t* text_lo = a.text + a.offsets[0];
+  const uint8_t* text_hi = a.text + a.offsets[a.n];
   int gn = 0;
   uint32_t used = 0;
   int64_t g_prompt = 0;
@@ -709,7 +730,7 @@ __global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, 
           asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
       }
     }
-    hash_prompt_seq(c, S, a.text + beg, (int)len, lane);
+    hash_prompt_seq(c, S, a.text + beg, (int)len, lane, text_lo, text_hi);
     __syncwarp();
     // pass 1: this lane's entry count (CSR: non-zero counts, and sum(count^2))
     uint32_t mine = 0;
