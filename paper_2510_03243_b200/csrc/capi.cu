@@ -67,6 +67,10 @@ struct pars_ctx {
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
   int64_t dmin_max = -1;
+  // host copy of the weights last uploaded into w64 (and converted into w32):
+  // a serving loop that scores with unchanged weights skips the upload
+  std::vector<double> w_shadow;
+  bool w64_valid = false, w32_valid = false;
 };
 
 struct pars_features {
@@ -284,13 +288,22 @@ __global__ void dense_csr_kernel(const double* __restrict__ X, int64_t n, uint32
 
 int upload_weights(pars_ctx* ctx, const FeatConfig& cfg, const double* w, int mode,
                    cudaStream_t st) {
-  PARS_TRY(ensure(ctx->w64, (size_t)cfg.dim * 8));
-  PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->w64.p, w, (size_t)cfg.dim * 8, cudaMemcpyHostToDevice, st));
-  if (mode == PARS_MODE_FAST_F32) {
+  const size_t bytes = (size_t)cfg.dim * 8;
+  const bool same = ctx->w64_valid && ctx->w_shadow.size() == cfg.dim &&
+                    std::memcmp(ctx->w_shadow.data(), w, bytes) == 0;
+  if (!same) {
+    PARS_TRY(ensure(ctx->w64, bytes));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->w64.p, w, bytes, cudaMemcpyHostToDevice, st));
+    ctx->w_shadow.assign(w, w + cfg.dim);
+    ctx->w64_valid = true;
+    ctx->w32_valid = false;
+  }
+  if (mode == PARS_MODE_FAST_F32 && !ctx->w32_valid) {
     PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
     f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(
         (const double*)ctx->w64.p, (float*)ctx->w32.p, cfg.dim);
     count_launch(ctx);
+    ctx->w32_valid = true;
   }
   return PARS_OK;
 }
@@ -660,6 +673,7 @@ int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* d_t
   a.w64 = d_weights;
   if (mode == PARS_MODE_FAST_F32) {
     PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
+    ctx->w32_valid = false;  // overwritten with the caller's device weights
     f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(d_weights,
                                                                         (float*)ctx->w32.p, cfg.dim);
     count_launch(ctx);
@@ -708,6 +722,7 @@ int pars_dev_score_embeddings(pars_ctx* ctx, const pars_extractor* ex, const dou
   const float* w32 = nullptr;
   if (mode == PARS_MODE_FAST_F32) {
     PARS_TRY(ensure(ctx->w32, (size_t)cfg.dim * 4));
+    ctx->w32_valid = false;  // overwritten with the caller's device weights
     f64_to_f32_kernel<<<(unsigned)ceil_div(cfg.dim, 256), 256, 0, st>>>(d_weights, (float*)ctx->w32.p,
                                                                          cfg.dim);
     count_launch(ctx);
@@ -912,6 +927,7 @@ int pars_features_score(pars_ctx* ctx, const pars_features* f, const double* wei
   Guard g(ctx);
   cudaStream_t st = ctx->stream;
   PARS_TRY(ensure(ctx->w64, (size_t)f->dim * 8));
+  ctx->w64_valid = ctx->w32_valid = false;  // overwritten below
   PARS_TRY(ensure(ctx->scores[0], (size_t)f->rows * 8));
   PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->w64.p, weights, (size_t)f->dim * 8, cudaMemcpyHostToDevice, st));
   csr_score_kernel<<<(unsigned)ceil_div(f->rows, 128), 128, 0, st>>>(

@@ -536,3 +536,39 @@ def test_kendall_tau_tile_split_matches_single_call(ctx, oracle):
     assert tau1 == tau2 and (c1 == c2).all()
     otau, oc = oracle.kendall(x, y)
     assert (c2 == oc).all() and tau2 == otau
+
+
+def test_weights_upload_cache_is_invalidated(ctx):
+    """Host-buffer calls skip re-uploading unchanged weights; the cache must
+    follow every change (new weights, other device weights through the
+    pars_dev_* paths, fp32 conversions)."""
+    import torch
+    from paper_2510_03243_b200 import MODE_EXACT, MODE_FAST, Extractor, Workload
+    wl = Workload.synthesize(700, 3)
+    ex = Extractor.make()
+    rng = np.random.default_rng(8)
+    w1, w2 = rng.normal(size=4096), rng.normal(size=4096)
+    ref = {}
+    for name, w in (("w1", w1), ("w2", w2)):
+        for mode in (MODE_EXACT, MODE_FAST):
+            other = Context_fresh(ctx)
+            ref[name, mode] = other.score_text(ex, wl.text, wl.offsets, w, mode=mode)
+    seq = [("w1", MODE_EXACT), ("w1", MODE_FAST), ("w1", MODE_EXACT), ("w2", MODE_FAST),
+           ("w2", MODE_EXACT), ("w1", MODE_FAST), ("w1", MODE_FAST)]
+    d_text = torch.from_numpy(wl.text).cuda()
+    d_offs = torch.from_numpy(wl.offsets).cuda()
+    d_w2 = torch.from_numpy(w2).cuda()
+    d_out = torch.empty(len(wl), dtype=torch.float64, device="cuda")
+    for name, mode in seq:
+        w = w1 if name == "w1" else w2
+        got = ctx.score_text(ex, wl.text, wl.offsets, w.copy(), mode=mode)
+        assert (got.view(np.uint64) == ref[name, mode].view(np.uint64)).all(), (name, mode)
+        # device-weight scoring in fast mode overwrites the fp32 weight buffer
+        ctx.dev_score_text(ex, d_text.data_ptr(), d_offs.data_ptr(), len(wl), d_w2.data_ptr(), 0.0,
+                           MODE_FAST, d_out.data_ptr())
+        torch.cuda.synchronize()
+
+
+def Context_fresh(ctx):
+    from paper_2510_03243_b200 import Context
+    return Context(0)
