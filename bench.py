@@ -188,6 +188,16 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -216,6 +226,7 @@ def run_reference(args):
                                f"bounded sample of {sample} prompts per step)",
                    "global_batch": N_PROMPTS, "seq_len": PAD_TOKENS, "parallelism": "openmp"},
         "cpu_baseline": {"value": value, "unit": "prompts/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"first {sample} prompts of the C4 workload, score_batch + select_batch"},
         "e2e": {"value": value, "unit": "prompts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -373,6 +384,7 @@ def run_ours(args):
             ref.step()  # warm
             v, ts, tsel = ref.step()
             cpu = {"value": v, "unit": "prompts/s", "cores": thr, "kind": "reference",
+                   "cpu_model": cpu_model(),
                    "sample": f"first {ref.n} prompts of the same C4 workload: score_batch "
                              f"({ts:.2f} s, OpenMP {thr} threads) + select_batch ({tsel:.3f} s)"}
         line = {
