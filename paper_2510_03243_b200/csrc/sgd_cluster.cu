@@ -37,6 +37,8 @@ namespace {
 
 constexpr int kCL = kSgdCluster;  // CTAs per cluster
 constexpr int kThreads = 256;
+constexpr int kChainWarps = 2;  // warps running the step's score chains
+constexpr int kChainThreads = kChainWarps * 32;
 constexpr int kBuildThreads = 1024;  // one warp per slot of a placement round
 constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr int kRegEntries = 12;      // row entries per lane kept in registers
@@ -211,19 +213,25 @@ __device__ __forceinline__ double chain_row_s(const uint32_t* __restrict__ rs, u
   double acc = 0.0;
   const uint32_t ng = len >> 2;
   if (ng >= 2) {
+    // pipeline: raw entries of group g+2, weights of group g+1, products of
+    // group g, adds of group g
     const uint4* r4 = reinterpret_cast<const uint4*>(rs);
     uint4 A = r4[0], B = r4[1];
-    double w0 = W[A.x >> 16], w1 = W[A.y >> 16], w2 = W[A.z >> 16], w3 = W[A.w >> 16];
+    double p0 = __dmul_rn(W[A.x >> 16], __dmul_rn(cnt_of(A.x), inv));
+    double p1 = __dmul_rn(W[A.y >> 16], __dmul_rn(cnt_of(A.y), inv));
+    double p2 = __dmul_rn(W[A.z >> 16], __dmul_rn(cnt_of(A.z), inv));
+    double p3 = __dmul_rn(W[A.w >> 16], __dmul_rn(cnt_of(A.w), inv));
+    double w0 = W[B.x >> 16], w1 = W[B.y >> 16], w2 = W[B.z >> 16], w3 = W[B.w >> 16];
     for (uint32_t g = 0; g < ng; ++g) {
       const uint4 Cn = g + 2 < ng ? r4[g + 2] : B;
-      const double v0 = W[B.x >> 16], v1 = W[B.y >> 16], v2 = W[B.z >> 16], v3 = W[B.w >> 16];
-      acc = __dadd_rn(acc, __dmul_rn(w0, __dmul_rn(cnt_of(A.x), inv)));
-      acc = __dadd_rn(acc, __dmul_rn(w1, __dmul_rn(cnt_of(A.y), inv)));
-      acc = __dadd_rn(acc, __dmul_rn(w2, __dmul_rn(cnt_of(A.z), inv)));
-      acc = __dadd_rn(acc, __dmul_rn(w3, __dmul_rn(cnt_of(A.w), inv)));
-      A = B;
+      const double q0 = __dmul_rn(w0, __dmul_rn(cnt_of(B.x), inv));
+      const double q1 = __dmul_rn(w1, __dmul_rn(cnt_of(B.y), inv));
+      const double q2 = __dmul_rn(w2, __dmul_rn(cnt_of(B.z), inv));
+      const double q3 = __dmul_rn(w3, __dmul_rn(cnt_of(B.w), inv));
+      w0 = W[Cn.x >> 16], w1 = W[Cn.y >> 16], w2 = W[Cn.z >> 16], w3 = W[Cn.w >> 16];
+      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, p0), p1), p2), p3);
+      p0 = q0, p1 = q1, p2 = q2, p3 = q3;
       B = Cn;
-      w0 = v0, w1 = v1, w2 = v2, w3 = v3;
     }
   }
   for (uint32_t e = ng >= 2 ? ng << 2 : 0; e < len; ++e) {
@@ -451,8 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
   for (uint32_t d = tid; d < L.dim; d += kThreads) W[d] = a.w_io[d];
   const int64_t nb = (a.npairs + L.B - 1) / L.B;
   // stage step 0 with every warp but 0, wait, start
-  if (warp >= 1) {
-    stage_step(L, a, sm, 0, 0, rank, tid - 32, kThreads - 32);
+  if (warp >= kChainWarps) {
+    stage_step(L, a, sm, 0, 0, rank, tid - kChainThreads, kThreads - kChainThreads);
     __pipeline_wait_prior(0);
   }
   __syncthreads();
@@ -474,10 +482,15 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     const double* slotinv = reinterpret_cast<const double*>(sm + L.slotinv) + (size_t)buf * L.spc;
     const int32_t* pairy = reinterpret_cast<const int32_t*>(sm + L.pairy) + (size_t)buf * L.ppc;
     const StepDesc d = reinterpret_cast<const StepDesc*>(sm + L.desc)[buf];
-    if (warp == 0) {
-      // phase A: score chains of this CTA's slots (scorer.cpp:40-42), then
-      // the margin loss of its pairs (pairs.hpp:27-31)
-      for (uint32_t k = lane; k < L.spc; k += 32) {
+    if (warp < kChainWarps) {
+      // phase A: score chains of this CTA's slots (scorer.cpp:40-42), spread
+      // over kChainWarps warps (few lanes each: fewer bank conflicts on the
+      // weight gathers, one chain warp per scheduler), then the margin loss
+      // of its pairs (pairs.hpp:27-31)
+      const uint32_t per = (L.spc + kChainWarps - 1) / kChainWarps;
+      for (uint32_t j = lane; j < per; j += 32) {
+        const uint32_t k = warp * per + j;
+        if (k >= L.spc) break;
         const int s = rank * (int)L.spc + (int)k;
         if (s >= 2 * bn) continue;
         const uint32_t* row = slotptr[k];
@@ -498,8 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
         }
         score[k] = __dadd_rn(acc, a.bias);
       }
-      __syncwarp();
-      for (uint32_t k = lane; k < L.ppc; k += 32) {
+      asm volatile("bar.sync 2, %0;" ::"r"(kChainThreads));  // chain warps only
+      for (uint32_t k = tid; k < L.ppc; k += kChainThreads) {
         const int p = rank * (int)L.ppc + (int)k;
         if (p >= bn) continue;
         const int32_t y = pairy[k];
@@ -520,8 +533,8 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
         cluster.map_shared_rank(loss_all, 0)[p] = l;
       }
     } else if (q + 1 < nb) {
-      // stage the next step while warp 0 scores this one
-      stage_step(L, a, sm, q + 1, buf ^ 1, rank, tid - 32, kThreads - 32);
+      // stage the next step while the chain warps score this one
+      stage_step(L, a, sm, q + 1, buf ^ 1, rank, tid - kChainThreads, kThreads - kChainThreads);
     }
 #ifdef PARS_SGD_TIMING
     long long c1 = clock64();
@@ -570,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #ifdef PARS_SGD_TIMING
     long long c3 = clock64();
 #endif
-    if (warp >= 1) __pipeline_wait_prior(0);  // next step's staged data
+    if (warp >= kChainWarps) __pipeline_wait_prior(0);  // next step's staged data
 #ifdef PARS_SGD_TIMING
     long long c4 = clock64();
 #endif
@@ -578,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     cluster.sync();
 #ifdef PARS_SGD_TIMING
     long long c5 = clock64();
-    tt[warp == 0 ? 0 : 5] += c1 - c0; tt[1] += c2 - c1; tt[2] += c3 - c2; tt[3] += c4 - c3; tt[4] += c5 - c4;
+    tt[warp < kChainWarps ? 0 : 5] += c1 - c0; tt[1] += c2 - c1; tt[2] += c3 - c2; tt[3] += c4 - c3; tt[4] += c5 - c4;
 #endif
   }
 #ifdef PARS_SGD_TIMING
