@@ -206,7 +206,13 @@ __global__ void slot_table_kernel(const uint32_t* __restrict__ pa, const uint32_
 // Score chain over a staged (shared-memory) row: the raw entries are read two
 // groups of 4 ahead and the weights one group ahead of the __dadd_rn chain,
 // so the chain does not wait on the load -> dependent gather latency.
-__device__ __forceinline__ double cnt_of(uint32_t E) { return (double)(int16_t)(E & 0xffffu); }
+// The entry's signed 16-bit count as a double, exactly, without an I2F.F64
+// (a slow conversion pipe on this part): the bits of 2^52 + (c + 2^15), less
+// 2^52 + 2^15, in one DADD.
+__device__ __forceinline__ double cnt_of(uint32_t E) {
+  const double biased = __hiloint2double(0x43300000, (int)((E + 0x8000u) & 0xffffu));
+  return __dsub_rn(biased, 4503599627403264.0);  // 2^52 + 2^15
+}
 
 __device__ __forceinline__ double chain_row_s(const uint32_t* __restrict__ rs, uint32_t len, double inv,
                                               const double* __restrict__ W) {
