@@ -132,7 +132,8 @@ const int64_t* pars_dataset_dev_output_len(const pars_dataset* d);
 int pars_dataset_export(const pars_dataset* d, char* text, int64_t* offsets,
                         int64_t* output_len, int64_t* prompt_len, char* ids,
                         int64_t* id_offsets);
-/* output_len_samples of record i; returns the count (-1 if > cap) */
+/* output_len_samples of record i; returns the count (-1 if > cap or i is
+ * out of range) */
 int64_t pars_dataset_samples(const pars_dataset* d, int64_t i, int64_t* out,
                              int64_t cap);
 void pars_dataset_free(pars_dataset* d);

@@ -1829,9 +1829,29 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
     uint32_t* d_blk = (uint32_t*)talloc((size_t)(nblk + 1) * 4);
     void* d_scan = talloc(ingest_scan_scratch_bytes(std::max<int64_t>(nblk, nb + 2)));  // >= lines
     if (!d_body || !d_blk || !d_scan) return oom();
-    DS_CUDA(cudaMemcpyAsync(d_body, body, (size_t)nb, cudaMemcpyHostToDevice, st));
+    // the bytes go up in 64 MB pieces on the copy stream; each piece's
+    // newline blocks are counted as soon as it lands
+    {
+      const int64_t kPiece = (64ll << 20) / ingest_block_bytes() * ingest_block_bytes();
+      const int npieces = (int)((nb + kPiece - 1) / kPiece);
+      while ((int)ctx->ev_chunk.size() < npieces) {
+        cudaEvent_t e;
+        DS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ev_chunk.push_back(e);
+      }
+      for (int k = 0; k < npieces; ++k) {
+        const int64_t o = (int64_t)k * kPiece, len = std::min<int64_t>(kPiece, nb - o);
+        DS_CUDA(cudaMemcpyAsync(d_body + o, body + o, (size_t)len, cudaMemcpyHostToDevice,
+                                ctx->copy_stream));
+        DS_CUDA(cudaEventRecord(ctx->ev_chunk[k], ctx->copy_stream));
+        DS_CUDA(cudaStreamWaitEvent(st, ctx->ev_chunk[k], 0));
+        const int64_t b0 = o / ingest_block_bytes();
+        const int64_t b1 = std::min<int64_t>(nblk, (o + len + ingest_block_bytes() - 1) / ingest_block_bytes());
+        ingest_count_newlines_range(d_body, nb, b0, b1, d_blk, st);
+      }
+    }
     int64_t nlc = 0;
-    if (ingest_count_newlines(d_body, nb, d_blk, &nlc, d_scan, st) != PARS_OK) return done(PARS_ERR_CUDA);
+    if (ingest_scan_newline_blocks(d_blk, nb, &nlc, d_scan, st) != PARS_OK) return done(PARS_ERR_CUDA);
     nlines = nlc + 1;  // the segment after the last '\n' (empty when the file ends with one)
     d_nl = (int64_t*)talloc((size_t)nlines * 8);
     if (!d_nl) return oom();
@@ -1862,7 +1882,9 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
         *q = (int64_t*)talloc((size_t)nrec * 8);
         if (!*q) return oom();
       }
-      if (!R.err || !R.flags) return oom();
+      R.any_samples = (uint32_t*)talloc(4);
+      if (!R.err || !R.flags || !R.any_samples) return oom();
+      DS_CUDA(cudaMemsetAsync(R.any_samples, 0, 4, st));
       ingest_launch_parse(d_body, d_rb, d_re, nrec, R, st);
       // 4. arenas: decoded lengths -> offsets
       int64_t* d_pro = nullptr;
@@ -1909,7 +1931,9 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
       ingest_launch_first_fail(nrec, R, d_dup, d_mis, d_uns, d->d_prompt_len, d_first, st);
       DS_CUDA(cudaMemcpyAsync(d->d_output_len, R.out_len, (size_t)nrec * 8, cudaMemcpyDeviceToDevice, st));
       unsigned long long first = 0;
+      uint32_t any_samples = 0;
       DS_CUDA(cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaMemcpyAsync(&any_samples, R.any_samples, 4, cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaStreamSynchronize(st));
       count_launch(ctx, 14);
       if (first != ~0ull) {
@@ -1932,13 +1956,12 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
                   has_emb ? "'embedding' arrays" : "more than 256 output_len_samples");
         return done(PARS_ERR_UNSUPPORTED);
       }
-      // output_len_samples (host CSR, for export)
-      d->samples_rp.assign((size_t)nrec + 1, 0);
-      std::vector<uint32_t> fl((size_t)nrec);
-      DS_CUDA(cudaMemcpy(fl.data(), R.flags, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
-      bool any = false;
-      for (uint32_t f : fl) any = any || (f & kIngHasSamples);
-      if (any) {
+      // output_len_samples (host CSR, for export): only when some record has
+      // them (an empty CSR means "no samples anywhere")
+      if (any_samples) {
+        d->samples_rp.assign((size_t)nrec + 1, 0);
+        std::vector<uint32_t> fl((size_t)nrec);
+        DS_CUDA(cudaMemcpy(fl.data(), R.flags, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
         std::vector<int64_t> sb((size_t)nrec), se((size_t)nrec);
         DS_CUDA(cudaMemcpy(sb.data(), R.sm_b, (size_t)nrec * 8, cudaMemcpyDeviceToHost));
         DS_CUDA(cudaMemcpy(se.data(), R.sm_e, (size_t)nrec * 8, cudaMemcpyDeviceToHost));
@@ -1960,7 +1983,7 @@ int pars_load_dataset_bytes(pars_ctx* ctx, const char* path, const char* bytes, 
       return oom();
     cudaMemsetAsync(d->d_offsets, 0, 8, st);
     cudaMemsetAsync(d->d_id_offsets, 0, 8, st);
-    d->samples_rp.assign(1, 0);
+    d->samples_rp.clear();
   }
   cudaStreamSynchronize(st);
   return done(PARS_OK);
@@ -2017,6 +2040,8 @@ int pars_dataset_export(const pars_dataset* d, char* text, int64_t* offsets, int
 int64_t pars_dataset_id_bytes(const pars_dataset* d) { return d ? d->id_bytes : 0; }
 
 int64_t pars_dataset_samples(const pars_dataset* d, int64_t i, int64_t* out, int64_t cap) {
+  if (i < 0 || i >= d->n) return -1;
+  if (d->samples_rp.empty()) return 0;  // no record of the file has samples
   const int64_t b = d->samples_rp[i], e = d->samples_rp[i + 1];
   if (e - b > cap) return -1;
   for (int64_t k = b; k < e; ++k) out[k - b] = d->samples[k];

@@ -749,6 +749,7 @@ __global__ void parse_records_kernel(const uint8_t* __restrict__ text, const int
   }
   out.err[r] = err;
   out.flags[r] = flags | (has_sm ? kIngHasSamples : 0u) | (has_ol ? kIngHasOutputLen : 0u);
+  if (has_sm && out.any_samples) atomicOr(out.any_samples, 1u);  // the host exports them
   out.id_b[r] = id_b;
   out.id_e[r] = id_e;
   out.id_len[r] = id_dl;
@@ -1017,6 +1018,26 @@ void ingest_launch_first_fail(int64_t nrec, const RecordOut& rec, const uint32_t
                               unsigned long long* first, cudaStream_t st) {
   first_fail_kernel<<<(unsigned)ceil_div(std::max<int64_t>(nrec, 1), 256), 256, 0, st>>>(
       nrec, rec, dup, mismatch, unsup, tokens, first);
+}
+
+int64_t ingest_block_bytes() { return kBlockBytes; }
+
+void ingest_count_newlines_range(const uint8_t* d_text, int64_t n, int64_t b0, int64_t b1,
+                                 uint32_t* d_blk, cudaStream_t st) {
+  if (b1 <= b0) return;
+  const int64_t off = b0 * kBlockBytes;
+  nl_count_kernel<<<(unsigned)(b1 - b0), kLineThreads, 0, st>>>(d_text + off, n - off, d_blk + b0);
+}
+
+int ingest_scan_newline_blocks(uint32_t* d_blk, int64_t n, int64_t* total, void* scratch,
+                               cudaStream_t st) {
+  const int64_t nb = std::max<int64_t>(1, ceil_div(n, kBlockBytes));
+  launch_scan<uint32_t>(d_blk, nb, scratch, st);
+  uint32_t t = 0;
+  PARS_CUDA_CHECK(cudaMemcpyAsync(&t, d_blk + nb, 4, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  *total = t;
+  return PARS_OK;
 }
 
 int ingest_count_newlines(const uint8_t* d_text, int64_t n, uint32_t* d_blk, int64_t* total,

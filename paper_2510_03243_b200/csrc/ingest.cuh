@@ -40,6 +40,7 @@ struct RecordOut {
   int64_t* out_len;     // -1 when absent
   int64_t* prompt_len;  // -1 when absent
   int64_t *sm_b, *sm_e;  // the samples array's span ('[' .. ']'), -1 when absent
+  uint32_t* any_samples;  // set to 1 when any record has output_len_samples
 };
 
 int64_t ingest_block_count(int64_t n);
@@ -49,6 +50,13 @@ int64_t ingest_block_count(int64_t n);
 size_t ingest_scan_scratch_bytes(int64_t n);
 int ingest_count_newlines(const uint8_t* d_text, int64_t n, uint32_t* d_blk, int64_t* total,
                           void* scratch, cudaStream_t st);
+// The same in pieces: counts of blocks [b0, b1) (as their bytes land), then
+// the scan of all block counts with the total back on the host.
+int64_t ingest_block_bytes();
+void ingest_count_newlines_range(const uint8_t* d_text, int64_t n, int64_t b0, int64_t b1,
+                                 uint32_t* d_blk, cudaStream_t st);
+int ingest_scan_newline_blocks(uint32_t* d_blk, int64_t n, int64_t* total, void* scratch,
+                               cudaStream_t st);
 void ingest_write_newlines(const uint8_t* d_text, int64_t n, const uint32_t* d_blk, int64_t* d_nl,
                            cudaStream_t st);
 void ingest_launch_line_flags(const int64_t* nl, int64_t nlines, int64_t n, uint32_t* nonempty,
