@@ -1223,7 +1223,9 @@ int ensure_compact(pars_ctx* ctx, pars_features* f, cudaStream_t st) {
 int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uint32_t* b,
                    const int32_t* y, int64_t npairs, int32_t batch, double lr, double margin,
                    double* d_w, double bias, double* epoch_loss, uint64_t* active,
-                   int algo = PARS_SGD_AUTO) {
+                   int algo = PARS_SGD_AUTO, double* d_out = nullptr) {
+  // d_out (optional, device, 16 bytes): leave {loss, active} there and return
+  // without synchronising, so the caller can prepare the next epoch meanwhile
   if (batch < 1 || batch > 32767) {
     set_error("sgd: batch size %d outside [1, 32767]", batch);
     return PARS_ERR_UNSUPPORTED;
@@ -1235,7 +1237,10 @@ int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uin
   cudaStream_t st = ctx->stream;
   *epoch_loss = 0.0;
   *active = 0;
-  if (npairs <= 0) return PARS_OK;
+  if (npairs <= 0) {
+    if (d_out) PARS_CUDA_CHECK(cudaMemsetAsync(d_out, 0, 16, st));
+    return PARS_OK;
+  }
   for (int64_t p = 0; p < npairs; ++p)
     if (a[p] >= f->rows || b[p] >= f->rows) {
       set_error("sgd: pair %lld references a row outside [0, %lld)", (long long)p, (long long)f->rows);
@@ -1255,7 +1260,7 @@ int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uin
   uint32_t* d_a = (uint32_t*)ctx->pairs_in.p;
   uint32_t* d_b = d_a + npairs;
   int32_t* d_y = (int32_t*)(d_b + npairs);
-  double* d_loss = (double*)(((uintptr_t)(d_y + npairs) + 15) & ~(uintptr_t)15);
+  double* d_loss = d_out ? d_out : (double*)(((uintptr_t)(d_y + npairs) + 15) & ~(uintptr_t)15);
   unsigned long long* d_act = (unsigned long long*)(d_loss + 1);
   bool cluster = false;
   if (algo != PARS_SGD_SINGLE_CTA && 2 * (int64_t)batch <= 65535 &&
@@ -1284,6 +1289,7 @@ int sgd_epoch_impl(pars_ctx* ctx, pars_features* f, const uint32_t* a, const uin
                               batch, lr, margin, bias, d_w, d_loss, d_act, total, ctx->sgd.p, sb,
                               st));
   }
+  if (d_out) return PARS_OK;
   unsigned long long act = 0;
   PARS_CUDA_CHECK(cudaMemcpyAsync(epoch_loss, d_loss, 8, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaMemcpyAsync(&act, d_act, 8, cudaMemcpyDeviceToHost, st));
@@ -1381,6 +1387,16 @@ int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex, const char* tex
     if (rc == PARS_OK) rc = cudaMemsetAsync(d_w, 0, (size_t)dim * 8, st) == cudaSuccess ? PARS_OK : PARS_ERR_CUDA;
     std::vector<uint32_t> pa(pairs_per_epoch), pb(pairs_per_epoch);
     std::vector<int32_t> py(pairs_per_epoch);
+    // each epoch is enqueued without a sync; the next epoch's pairs are drawn
+    // on the host while it runs. Losses are checked in epoch order at the end
+    // (an epoch after a diverged one only costs time: the error is the same)
+    std::vector<int64_t> npe((size_t)std::max(epochs, 0), 0);
+    double* d_out = nullptr;
+    if (rc == PARS_OK && epochs > 0 && !pool_alloc(ctx, (void**)&d_out, (size_t)epochs * 16)) {
+      set_error("device allocation failed (loss slots)");
+      rc = PARS_ERR_OOM;
+    }
+    int done_epochs = 0;
     for (int e = 0; e < epochs && rc == PARS_OK; ++e) {
       const uint64_t es = splitmix64(seed ^ splitmix64(0x10000u + (uint64_t)e));  // derive_seed
       const int64_t np = pars_build_pairs(lengths, n, delta, pairs_per_epoch, es, pa.data(),
@@ -1392,16 +1408,36 @@ int pars_train_pairwise(pars_ctx* ctx, const pars_extractor* ex, const char* tex
       double el = 0.0;
       uint64_t act = 0;
       rc = sgd_epoch_impl(ctx, f, pa.data(), pb.data(), py.data(), np, batch, lr, margin, d_w, 0.0,
-                          &el, &act);
-      if (rc != PARS_OK) break;
-      const double mean = el / (double)np;
-      if (!std::isfinite(mean)) {
-        set_error("training diverged at epoch %d", e);
-        rc = PARS_ERR_INVALID;
-        break;
-      }
-      loss_trace[e] = mean;
+                          &el, &act, PARS_SGD_AUTO, d_out + 2 * e);
+      npe[e] = np;
+      if (rc == PARS_OK) done_epochs = e + 1;
     }
+    if (done_epochs > 0) {
+      std::vector<double> out((size_t)done_epochs * 2);
+      if (cudaMemcpyAsync(out.data(), d_out, out.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("CUDA error reading epoch losses");
+        rc = PARS_ERR_CUDA;
+      } else {
+        const int rc_later = rc;  // a failure after the last enqueued epoch
+        const std::string err_later = rc_later == PARS_OK ? "" : pars_last_error();
+        rc = PARS_OK;
+        for (int e = 0; e < done_epochs; ++e) {
+          const double mean = out[2 * e] / (double)npe[e];
+          if (!std::isfinite(mean)) {
+            set_error("training diverged at epoch %d", e);
+            rc = PARS_ERR_INVALID;
+            break;
+          }
+          loss_trace[e] = mean;
+        }
+        if (rc == PARS_OK && rc_later != PARS_OK) {
+          set_error("%s", err_later.c_str());
+          rc = rc_later;
+        }
+      }
+    }
+    if (d_out) pool_free(ctx, d_out);
     if (rc == PARS_OK) {
       if (cudaMemcpyAsync(w_out, d_w, (size_t)dim * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
           cudaStreamSynchronize(st) != cudaSuccess) {
