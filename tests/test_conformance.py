@@ -20,8 +20,12 @@ B200_BIN = ROOT / "oracle" / "_ref" / "conformance_b200"
 
 
 def run(binary):
+    # the suites write scratch files into their working directory
+    import tempfile
     env = dict(os.environ, OMP_NUM_THREADS="1")
-    p = subprocess.run([str(binary)], capture_output=True, text=True, env=env, timeout=900)
+    with tempfile.TemporaryDirectory() as cwd:
+        p = subprocess.run([str(binary)], capture_output=True, text=True, env=env, timeout=900,
+                           cwd=cwd)
     return p.returncode, p.stdout + p.stderr
 
 
