@@ -17,3 +17,18 @@ for label, kw in (("pageable", {}), ("pinned", {"out": outs})):
         ctx.score_order(ex, arena, offs, w, tie, **kw)
         lat.append(time.perf_counter() - t0)
     print(label, "median ms", 1e3 * float(np.median(lat[5:])))
+
+# fixed overhead: one tiny prompt
+a1, o1 = P.pack_texts([b"hello world"])
+lat = []
+for k in range(50):
+    t0 = time.perf_counter()
+    ctx.score_order(ex, a1, o1, w, np.zeros(1, np.uint32))
+    lat.append(time.perf_counter() - t0)
+print("n=1 median ms", 1e3 * float(np.median(lat[5:])))
+lat = []
+for k in range(50):
+    t0 = time.perf_counter()
+    ctx.score_text(ex, arena, offs, w)
+    lat.append(time.perf_counter() - t0)
+print("score_text 1024 median ms", 1e3 * float(np.median(lat[5:])))
