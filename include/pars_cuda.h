@@ -307,6 +307,17 @@ int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores,
                             const uint8_t* d_boosted,
                             const uint32_t* d_tie_rank, int64_t n,
                             uint32_t* d_order, void* stream);
+/* The global order from shard orders: prompts [run_offsets[r],
+ * run_offsets[r+1]) form shard r, d_run_orders holds each shard's
+ * pars_dev_priority_order result (indices relative to the shard start),
+ * concatenated; d_scores / d_boosted / d_tie cover all n = run_offsets[nruns]
+ * prompts. d_order[n] receives what pars_dev_priority_order over all n would
+ * (bit-identical), by merging the runs. run_offsets is a host array. Returns
+ * after the merge completes on `stream`. */
+int pars_dev_merge_orders(pars_ctx* ctx, const double* d_scores,
+                          const uint8_t* d_boosted, const uint32_t* d_tie,
+                          const uint32_t* d_run_orders, const int64_t* run_offsets,
+                          int nruns, uint32_t* d_order, void* stream);
 /* Host helper: dense ranks of (arrival, id) with equal keys sharing a rank.
  * ids: arena + offsets[n+1] (raw bytes, compared unsigned). */
 int pars_tie_ranks(const double* arrival, const char* ids,

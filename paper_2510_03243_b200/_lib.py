@@ -134,6 +134,7 @@ def _load() -> C.CDLL:
         "pars_tie_ranks": (C.c_int, [vp, vp, vp, i64, vp]),
         "pars_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp]),
         "pars_kendall_tau_algo": (C.c_int, [vp, vp, vp, i64, vp, vp, C.c_int]),
+        "pars_dev_merge_orders": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "pars_dev_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
         "pars_workload_synthesize": (C.c_int, [u64, dbl, dbl, u64, i64, u64, vp]),
         "pars_workload_count": (i64, [vp]),

@@ -1668,6 +1668,31 @@ int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores, const uint8_t
   return launch_priority_sort(ctx, d_scores, d_boosted, d_tie, n, d_order, ctx->sort.p, st);
 }
 
+// select_batch order of all prompts from the orders of contiguous shards
+// (each from pars_dev_priority_order on its own range): the sharded-scoring
+// path's global SJF order without re-sorting everything.
+int pars_dev_merge_orders(pars_ctx* ctx, const double* d_scores, const uint8_t* d_boosted,
+                          const uint32_t* d_tie, const uint32_t* d_run_orders,
+                          const int64_t* run_offsets, int nruns, uint32_t* d_order, void* stream) {
+  PARS_TRY(check_ctx(ctx));
+  if (nruns < 1 || run_offsets[0] != 0) {
+    set_error("merge_orders: need >= 1 run starting at offset 0");
+    return PARS_ERR_INVALID;
+  }
+  for (int r = 0; r < nruns; ++r)
+    if (run_offsets[r + 1] < run_offsets[r]) {
+      set_error("merge_orders: run offsets must be non-decreasing");
+      return PARS_ERR_INVALID;
+    }
+  const int64_t n = run_offsets[nruns];
+  if (n <= 0) return PARS_OK;
+  Guard g(ctx);
+  cudaStream_t st = pick(ctx, stream);
+  PARS_TRY(ensure(ctx->sort, std::max(sort_scratch_bytes(n), merge_runs_scratch_bytes(n, nruns)) + 4096));
+  return launch_merge_runs(ctx, d_scores, d_boosted, d_tie, d_run_orders, run_offsets, nruns, n,
+                           d_order, ctx->sort.p, st);
+}
+
 // ---- Kendall tau-b (metrics.cpp:13-64) -----------------------------------
 
 namespace pars_b200 {

@@ -76,6 +76,12 @@ int launch_sgd_epoch(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, cons
                      int64_t total_entries, void* scratch, size_t scratch_bytes,
                      cudaStream_t st);
 
+// Merge of per-shard select_batch orders into the global one (sort.cu).
+size_t merge_runs_scratch_bytes(int64_t n, int nruns);
+int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
+                      const uint32_t* run_order, const int64_t* h_off, int nruns, int64_t n,
+                      uint32_t* order, void* scratch, cudaStream_t st);
+
 // Kendall tau-b counts by sorting (tau_sorted.cu); counts4 on the host.
 size_t tau_sorted_scratch_bytes(int64_t n);
 int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n,

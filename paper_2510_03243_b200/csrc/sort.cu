@@ -214,6 +214,115 @@ __global__ void __launch_bounds__(kSmallThreads) small_sort_kernel(
 
 }  // namespace
 
+// ---- merging sorted runs (the global order of sharded scoring) -------------
+// Runs [off[r], off[r+1]) are each in select_batch order (run-local orders
+// from launch_priority_sort on the shard). Every element becomes the 128-bit
+// key (hi = boosted ? 0 : ordered_bits(score), lo = tie << 32 | index), a
+// total order equal to the global sort's (key, tie, then input index), and
+// adjacent runs are merged level by level: each element finds its place in
+// the sibling run by binary search (keys are unique, so no tie rule is needed).
+namespace {
+__global__ void merge_keys_kernel(const double* __restrict__ score, const uint8_t* __restrict__ boosted,
+                                  const uint32_t* __restrict__ tie, const uint32_t* __restrict__ run_order,
+                                  const int64_t* __restrict__ off, int nruns, int64_t n,
+                                  uint64_t* __restrict__ hi, uint64_t* __restrict__ lo) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int r = 0;
+  while (r + 1 < nruns && off[r + 1] <= k) ++r;  // nruns is the rank count: small
+  const uint32_t i = (uint32_t)(off[r] + run_order[k]);
+  hi[k] = (boosted && boosted[i]) ? 0ull : ordered_bits(score[i]);
+  lo[k] = ((uint64_t)(tie ? tie[i] : 0u) << 32) | i;
+}
+
+__device__ __forceinline__ bool key_less(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+
+// one level: runs (a, b) = (2m, 2m+1) of the current boundaries merge into
+// [off[2m], off[2m+2]); boundaries for the next level are every other one
+__global__ void merge_level_kernel(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo,
+                                   const int64_t* __restrict__ off, int nruns, int64_t n,
+                                   uint64_t* __restrict__ ohi, uint64_t* __restrict__ olo) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int r = 0;
+  while (r + 1 < nruns && off[r + 1] <= k) ++r;
+  const uint64_t h = hi[k], l = lo[k];
+  const int sib = r ^ 1;
+  if (sib >= nruns) {  // odd run out: copied through
+    ohi[k] = h;
+    olo[k] = l;
+    return;
+  }
+  const int64_t s0 = off[sib], s1 = off[sib + 1];
+  int64_t a = s0, b = s1;  // first sibling element greater than (h, l)
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (key_less(hi[m], lo[m], h, l)) a = m + 1; else b = m;
+  }
+  const int64_t base = off[r & ~1];
+  const int64_t pos = base + (k - off[r]) + (a - s0);
+  ohi[pos] = h;
+  olo[pos] = l;
+}
+
+__global__ void merge_out_kernel(const uint64_t* __restrict__ lo, int64_t n, uint32_t* __restrict__ order) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) order[k] = (uint32_t)lo[k];
+}
+
+}  // namespace
+
+size_t merge_runs_scratch_bytes(int64_t n, int nruns) {
+  return 4 * ((size_t)n * 8 + 256) + 2 * ((size_t)(nruns + 1) * 8 + 256);
+}
+
+int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
+                      const uint32_t* run_order, const int64_t* h_off, int nruns, int64_t n,
+                      uint32_t* order, void* scratch, cudaStream_t st) {
+  if (n == 0) return PARS_OK;
+  if (n > 0x7fffffffLL) {
+    set_error("priority order: n=%lld exceeds 2^31-1", (long long)n);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  uint64_t* hi[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
+  uint64_t* lo[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
+  int64_t* d_off[2] = {(int64_t*)take((nruns + 1) * 8), (int64_t*)take((nruns + 1) * 8)};
+  const unsigned g = (unsigned)ceil_div(n, 256);
+  std::vector<int64_t> off(h_off, h_off + nruns + 1);
+  PARS_CUDA_CHECK(cudaMemcpyAsync(d_off[0], off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+  merge_keys_kernel<<<g, 256, 0, st>>>(score, boosted, tie, run_order, d_off[0], nruns, n, hi[0], lo[0]);
+  count_launch(ctx);
+  int cur = 0, cb = 0;
+  int runs = nruns;
+  while (runs > 1) {
+    merge_level_kernel<<<g, 256, 0, st>>>(hi[cur], lo[cur], d_off[cb], runs, n, hi[cur ^ 1],
+                                          lo[cur ^ 1]);
+    count_launch(ctx);
+    cur ^= 1;
+    std::vector<int64_t> next;
+    for (int r = 0; r < runs; r += 2) next.push_back(off[r]);
+    next.push_back(off[runs]);
+    off.swap(next);
+    runs = (int)off.size() - 1;
+    cb ^= 1;
+    PARS_CUDA_CHECK(cudaMemcpyAsync(d_off[cb], off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+  }
+  merge_out_kernel<<<g, 256, 0, st>>>(lo[cur], n, order);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  // the boundary vectors are pageable host memory read by async copies
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return PARS_OK;
+}
+
 size_t sort_scratch_bytes(int64_t n) {
   const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kTileKeys);
   size_t b = 0;

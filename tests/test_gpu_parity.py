@@ -572,3 +572,38 @@ def test_weights_upload_cache_is_invalidated(ctx):
 def Context_fresh(ctx):
     from paper_2510_03243_b200 import Context
     return Context(0)
+
+
+@pytest.mark.parametrize("n,runs", [(1, 1), (1000, 2), (300_001, 4), (1_000_003, 8), (77, 3),
+                                    (4096, 5)])
+def test_merge_shard_orders_equals_global_order(ctx, n, runs):
+    """pars_dev_merge_orders: the select_batch order of all prompts from the
+    orders of contiguous shards equals one pars_dev_priority_order over all —
+    with equal scores, boosted prompts and repeated tie ranks."""
+    import ctypes
+    import torch
+    from paper_2510_03243_b200 import lib
+    rng = np.random.default_rng(n + runs)
+    s = rng.normal(size=n).round(2)  # many equal scores
+    s[rng.random(n) < 0.01] = -0.0
+    tie = rng.integers(0, max(1, n // 3), n).astype(np.uint32)
+    boosted = (rng.random(n) < 0.05).astype(np.uint8)
+    ds, dt, db = (torch.from_numpy(s).cuda(), torch.from_numpy(tie).cuda(),
+                  torch.from_numpy(boosted).cuda())
+    want = torch.empty(n, dtype=torch.int32, device="cuda")
+    assert lib().pars_dev_priority_order(ctx.h, ds.data_ptr(), db.data_ptr(), dt.data_ptr(), n,
+                                         want.data_ptr(), None) == 0
+    offs = np.linspace(0, n, runs + 1).astype(np.int64)
+    run_orders = torch.empty(n, dtype=torch.int32, device="cuda")
+    for r in range(runs):
+        a, b = int(offs[r]), int(offs[r + 1])
+        if b > a:
+            assert lib().pars_dev_priority_order(ctx.h, ds[a:].data_ptr(), db[a:].data_ptr(),
+                                                 dt[a:].data_ptr(), b - a,
+                                                 run_orders[a:].data_ptr(), None) == 0
+    got = torch.empty(n, dtype=torch.int32, device="cuda")
+    assert lib().pars_dev_merge_orders(ctx.h, ds.data_ptr(), db.data_ptr(), dt.data_ptr(),
+                                       run_orders.data_ptr(), offs.ctypes.data, runs,
+                                       got.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert (got.cpu().numpy() == want.cpu().numpy()).all()
