@@ -255,9 +255,30 @@ def run_ours(args):
     d_text = torch.from_numpy(wl.text[t0b:t1b]).to(dev)
     d_offs = torch.from_numpy(wl.offsets[b:e + 1] - t0b).to(dev)
     d_w = torch.from_numpy(w).to(dev)
-    d_scores = torch.empty(n, dtype=torch.float64, device=dev)
+    # shard buffers are `per` long (equal across ranks) so the all-gather of
+    # the global-order step needs no padding logic; this rank fills the first n
+    per = (N_PROMPTS + world - 1) // world
+    d_scores = torch.empty(per, dtype=torch.float64, device=dev)
     d_tie = torch.arange(b, e, dtype=torch.int32, device=dev)  # burst: rank of (0, id) = index
-    d_order = torch.empty(n, dtype=torch.int32, device=dev)
+    d_order = torch.zeros(per, dtype=torch.int32, device=dev)
+    if world > 1:
+        # the global SJF order of all N prompts: gather every
+        # shard's scores and shard order, then rank 0 merges the sorted runs
+        import torch.distributed as dist
+        g_scores = torch.empty(per * world, dtype=torch.float64, device=dev)
+        g_orders = torch.empty(per * world, dtype=torch.int32, device=dev)
+        g_tie = torch.arange(N_PROMPTS, dtype=torch.int32, device=dev)
+        g_order = torch.empty(N_PROMPTS, dtype=torch.int32, device=dev)
+        run_offs = np.array([min(N_PROMPTS, r * per) for r in range(world + 1)], np.int64)
+        nccl = os.environ.get("PARS_DIST_BACKEND", "nccl") == "nccl"
+
+        def gather_into(out, inp):
+            if nccl:
+                dist.all_gather_into_tensor(out, inp)
+            else:  # gloo test mode: through the host
+                parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+                dist.all_gather(parts, inp.cpu())
+                out.copy_(torch.cat(parts))
     L = P.lib()
     # a dedicated (non-NULL) stream: a NULL handle would mean "the ctx's own
     # stream" to the C ABI and torch's events would not see the kernels
@@ -279,6 +300,15 @@ def run_ours(args):
                                        d_order.data_ptr(), sh)
         if rc != 0:
             raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+        if world > 1:
+            gather_into(g_scores, d_scores)
+            gather_into(g_orders, d_order)
+            if rank == 0:
+                rc = L.pars_dev_merge_orders(ctx.h, g_scores.data_ptr(), None, g_tie.data_ptr(),
+                                             g_orders.data_ptr(), run_offs.ctypes.data, world,
+                                             g_order.data_ptr(), sh)
+                if rc != 0:
+                    raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
         if ev is not None:
             ev[2].record(stream)
 
@@ -294,6 +324,14 @@ def run_ours(args):
     so = o.score_batch(OEx.make(), wl.text, wl.offsets[b:b + chk + 1], w, 0.0)
     got = d_scores[:chk].cpu().numpy()
     parity_ok = bool((got.view(np.uint64) == so.view(np.uint64)).all())
+    global_order_ok = None
+    if world > 1 and rank == 0:
+        # the merged global order equals one sort of all N gathered scores
+        full = torch.empty(N_PROMPTS, dtype=torch.int32, device=dev)
+        L.pars_dev_priority_order(ctx.h, g_scores.data_ptr(), None, g_tie.data_ptr(), N_PROMPTS,
+                                  full.data_ptr(), sh)
+        torch.cuda.synchronize()
+        global_order_ok = bool(torch.equal(full, g_order))
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -395,7 +433,10 @@ def run_ours(args):
             "config": {"workload": "C4: score + SJF-sort 1M synthetic prompts x 512 tokens "
                                    "(exact fp64 mode, bit-identical to the reference)",
                        "global_batch": N_PROMPTS, "seq_len": PAD_TOKENS,
-                       "parallelism": f"shard{world}", "extractor": "hashed word{1}+char{3}, D=4096, L2",
+                       "parallelism": f"shard{world}",
+                       **({"global_order": "all-gather of shard scores + shard orders, merged on "
+                                           "rank 0 (pars_dev_merge_orders), inside the step"}
+                          if world > 1 else {}), "extractor": "hashed word{1}+char{3}, D=4096, L2",
                        "l2_flush": "inputs larger than L2 (%.2f GB text per rank)" % (text_bytes / 1e9)},
             "roofline": {"bound": "hbm", "kernel": "featurize_seq_kernel (fused tokenise+hash+histogram+L2+dot)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -407,7 +448,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
             "gpu_launches": int(launches),
             "clocks": clk,
-            "parity": {"scores_bitexact_sample": parity_ok, "sample": chk},
+            "parity": {"scores_bitexact_sample": parity_ok, "sample": chk,
+                       **({"global_order_equals_full_sort": global_order_ok} if world > 1 else {})},
             "pairs": pairs,
             "kendall_tau": tau,
             "embeddings": embed,
