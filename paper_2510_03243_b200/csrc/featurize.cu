@@ -43,7 +43,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRing = 256;                   // transition ring entries per warp
-constexpr int kGroup = 32;                   // prompts per exact chain group (one per lane)
+constexpr int kGroup = 16;                   // prompts per exact chain group (one per lane)
 constexpr uint32_t kBias2 = 0x80008000u;     // two biased 16-bit zero counters
 constexpr int64_t kNarrowMaxFeatures = 32767;  // |count| <= features: 16 bits cannot wrap
 constexpr size_t kMaxSmemPerBlock = 200 * 1024;
