@@ -14,7 +14,7 @@
 //     buckets (gradient folds + updates); updated weights, active flags and
 //     slot L2 factors are broadcast to the other CTAs' shared memory through
 //     DSMEM, with two cluster barriers per step;
-//   * while warp 0 runs the step's score chains, warps 1-7 stage the NEXT
+//   * while warps 0-1 run the step's score chains, warps 2-7 stage the NEXT
 //     step's rows, CSC entries and runs into the other half of a double
 //     buffer with cp.async, so the dependent chains read shared memory only.
 // Steps whose data does not fit the buffers read it from global memory.
@@ -366,8 +366,9 @@ struct EpochArgs {
   long long* timing;  // PARS_SGD_TIMING builds only: [5 phases][8 ranks] max over threads
 };
 
-// Stage step q's data for CTA `rank` into buffer `buf`; run by warps 1..7
-// (t = thread index within them, nt = 224) while warp 0 scores step q-1.
+// Stage step q's data for CTA `rank` into buffer `buf`; run by the staging
+// warps (t = thread index within them, nt = their thread count) while the
+// chain warps score step q-1.
 __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* sm, int64_t q,
                            int buf, int rank, int t, int nt) {
   const int64_t p0 = q * L.B;
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
   double epoch_loss = 0.0;
   unsigned long long active = 0;
 #ifdef PARS_SGD_TIMING
-  long long tt[6] = {0, 0, 0, 0, 0, 0};  // [0] warp 0's chains, [5] the staging warps
+  long long tt[6] = {0, 0, 0, 0, 0, 0};  // [0] the chain warps, [5] the staging warps
 #endif
   for (int64_t q = 0; q < nb; ++q) {
 #ifdef PARS_SGD_TIMING
