@@ -297,6 +297,7 @@ struct StepDesc {
   uint32_t ent_base;  // batch-relative index of csc[0]
   uint32_t ent_end;   // batch-relative end of this CTA's entries
   uint32_t pad;
+  uint32_t cshift;    // staged CSC: entry ent_base sits at cscbuf[cshift] (16-byte copies)
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -421,7 +422,9 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
     d.ent_end = q4.w;
     const uint2* rq = a.runs + q * (int64_t)L.dim;
     d.runs = (d.nruns <= L.runcap) ? runbuf : rq + q4.x;
-    d.csc = (d.ent_end - d.ent_base <= L.csccap) ? cscbuf : a.ent + a.ent_off[q] + d.ent_base;
+    const uint32_t* g0 = a.ent + a.ent_off[q] + d.ent_base;
+    d.cshift = (uint32_t)((reinterpret_cast<uintptr_t>(g0) >> 2) & 3u);
+    d.csc = (d.ent_end - d.ent_base + d.cshift + 3 <= L.csccap) ? cscbuf : g0;
     d.pad = q4.x;
     *desc = d;
   }
@@ -441,9 +444,12 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
     for (uint32_t c = t; c < d.nruns; c += nt) __pipeline_memcpy_async(runbuf + c, g + c, 8);
   }
   if (d.csc == cscbuf) {
-    const uint32_t* g = a.ent + a.ent_off[q] + d.ent_base;
-    for (uint32_t c = t; c < d.ent_end - d.ent_base; c += nt)
-      __pipeline_memcpy_async(cscbuf + c, g + c, 4);
+    // 16-byte copies from the aligned word at or before the first entry (the
+    // ent array is 256-byte aligned with slack after it, so the up to 3 words
+    // on either side are readable); entry ent_base lands at cscbuf[cshift]
+    const uint32_t* g = a.ent + a.ent_off[q] + d.ent_base - d.cshift;
+    const uint32_t n16 = (d.ent_end - d.ent_base + d.cshift + 3) / 4;
+    for (uint32_t c = t; c < n16; c += nt) __pipeline_memcpy_async(cscbuf + 4 * c, g + 4 * c, 16);
   }
   __pipeline_commit();
 }
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
       double g = 0.0;
       uint32_t e = run.y;
       if (csc_staged) {  // shared-memory loads
-        const uint32_t* cs = smw + (L.cscbuf >> 2) + (size_t)buf * L.csccap - d.ent_base;
+        const uint32_t* cs = smw + (L.cscbuf >> 2) + (size_t)buf * L.csccap + d.cshift - d.ent_base;
         g = chain_run_s(cs, e, e1, sinv);
       } else {
         const uint32_t* csc = d.csc - d.ent_base;
