@@ -504,21 +504,55 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
+    # the whole step (kernels, the torch update, NCCL collectives) as one CUDA
+    # graph replayed per step: the host launches nothing per kernel. Falls
+    # back to eager launches if capture is refused (e.g. a collective backend
+    # that cannot be captured).
+    graph = None
+    if world == 1 or os.environ.get("PARS_DIST_BACKEND", "nccl") == "nccl":
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step()
+            graph = g
+        except Exception as exc:  # noqa: BLE001
+            print("bench_pairs: CUDA graph capture failed (%s); timing eager steps" % exc,
+                  file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
     barrier(world)
     a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(3, args.steps)
     a.record(stream)
     for _ in range(k):
-        step()
+        run()
     bb.record(stream)
     torch.cuda.synchronize()
     ms = barrier_max(world, a.elapsed_time(bb)) / k
     cnt, part = res["out"]
+    graph_ok = None
+    if graph is not None:
+        # replaying the graph trains exactly like launching the steps
+        d_w.copy_(torch.from_numpy(w0).to(dev))
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        w_graph = d_w.clone()
+        d_w.copy_(torch.from_numpy(w0).to(dev))
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        graph_ok = bool(torch.equal(w_graph.view(torch.int64), d_w.view(torch.int64)))
     feats.free()
     return {"metric": "filtered pairs/s", "value": kept / (ms / 1e3), "unit": "pairs/s",
             "ms_per_step": ms, "kept": kept, "kept_expected": 1920977782,
             "active_last_step": int(cnt[1]), "first_step_matches_oracle": first_ok,
-            "plan_sorted": plan.sorted,
+            "plan_sorted": plan.sorted, "cuda_graph": graph is not None,
+            "cuda_graph_matches_eager": graph_ok,
             "workload": "C5: full-batch DP training step over all 2,147,450,880 unordered pairs "
                         "of 65,536 prompts (seed 25): CSR scoring of the rank's shard + score "
                         "all-gather, Eq.1 mask delta=0.2 + hinge + integer coefficients on the "

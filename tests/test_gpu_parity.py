@@ -607,3 +607,47 @@ def test_merge_shard_orders_equals_global_order(ctx, n, runs):
                                        got.data_ptr(), None) == 0
     torch.cuda.synchronize()
     assert (got.cpu().numpy() == want.cpu().numpy()).all()
+
+
+def test_dp_train_step_replays_as_a_cuda_graph(ctx):
+    """The C5 step (score, all-pairs plan tiles, X^T c, update) captured once as
+    a CUDA graph and replayed trains bit-identically to launching it."""
+    import torch
+    from paper_2510_03243_b200 import Extractor, Workload
+    from paper_2510_03243_b200 import distributed as D
+    n = 4000
+    wl = Workload.synthesize(n, 43)
+    f = ctx.extract(Extractor.make(), wl.text, wl.offsets)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    w0 = np.random.default_rng(3).normal(size=4096) * 0.05
+    with torch.cuda.stream(stream):
+        d_w = torch.from_numpy(w0).to(dev)
+        d_L = torch.from_numpy(wl.output_len.astype(np.int32)).to(dev)
+        scores = torch.zeros(n, dtype=torch.float64, device=dev)
+        plan = ctx.pair_plan(wl.output_len, 0.2)
+        sh = stream.cuda_stream
+        max_len = int(wl.output_len.max())
+
+        def step():
+            D.train_step_gpu(ctx, f, d_w, scores, d_L, n, 0.2, 1.0, max_len, 0.1 / plan.kept,
+                             stream=sh, plan=plan)
+
+        for _ in range(2):
+            step()  # warm-up: lazily built structures exist before capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step()
+        d_w.copy_(torch.from_numpy(w0).to(dev))
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        w_graph = d_w.clone()
+        d_w.copy_(torch.from_numpy(w0).to(dev))
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+    assert torch.equal(w_graph.view(torch.int64), d_w.view(torch.int64))
+    assert not torch.equal(d_w, torch.from_numpy(w0).to(dev))
+    f.free()
