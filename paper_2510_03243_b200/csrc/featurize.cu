@@ -717,12 +717,10 @@ __global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, 
       continue;
     }
     {
-      // every 128-byte line of this prompt into L1 at once (lane l: lines l,
-      // l+32, ...), and the warp's next prompt into L2, so the lanes'
-      // sequential word loads do not each expose a miss
-      const uintptr_t l0 = reinterpret_cast<uintptr_t>(a.text + beg) & ~(uintptr_t)127;
-      for (uintptr_t q = l0 + 128u * lane; q < reinterpret_cast<uintptr_t>(a.text + beg + len); q += 4096u)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+      // the warp's next prompt into L2, so the lanes' sequential word loads
+      // do not each expose a DRAM miss (an L1 prefetch of the current prompt
+      // measured slower: with 3 x 70 KB of shared memory per SM, L1 keeps
+      // less than one prompt per warp)
       if (i + nw < a.n) {
         const int64_t nb = a.offsets[i + nw], ne = a.offsets[i + nw + 1];
         const uintptr_t n0 = reinterpret_cast<uintptr_t>(a.text + nb) & ~(uintptr_t)127;
