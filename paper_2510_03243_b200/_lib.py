@@ -458,11 +458,15 @@ class Context:
 
     # -- scoring ---------------------------------------------------------------
     def score_text(self, ex: Extractor, text: np.ndarray, offsets: np.ndarray, weights,
-                   bias: float = 0.0, mode: int = MODE_EXACT) -> np.ndarray:
-        """Scorer::score_batch over prompts given as an arena + offsets."""
+                   bias: float = 0.0, mode: int = MODE_EXACT, out=None) -> np.ndarray:
+        """Scorer::score_batch over prompts given as an arena + offsets.
+        out: optional caller-owned float64[n] (page-locked: direct DMA)."""
         offs = _c(offsets, np.int64)
         n = len(offs) - 1
-        out = np.zeros(max(n, 0), np.float64)
+        if out is None:
+            out = np.zeros(max(n, 0), np.float64)
+        else:
+            assert out.dtype == np.float64 and out.flags.c_contiguous and len(out) >= n
         t = text if isinstance(text, np.ndarray) else np.frombuffer(bytes(text), np.uint8)
         _check(lib().pars_score_text(self.h, C.byref(ex), _p(t), _p(offs), n,
                                      _p(_c(weights, np.float64)), bias, mode, _p(out)))

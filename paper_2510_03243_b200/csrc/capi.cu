@@ -580,11 +580,16 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   PARS_TRY(check_text_call(ex, n, &cfg, "pars_score_text"));
   if (n == 0) return PARS_OK;
   Guard g(ctx);
-  PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
-  double* h_sc = static_cast<double*>(ctx->h_scores.p);
+  // a page-locked result buffer takes the per-chunk score copies directly
+  const bool pin = is_pinned(scores);
+  double* h_sc = scores;
+  if (!pin) {
+    PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
+    h_sc = static_cast<double*>(ctx->h_scores.p);
+  }
   std::vector<int64_t> chunks;
   PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, nullptr, h_sc, &chunks));
-  PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));
+  if (!pin) PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));
   PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   return PARS_OK;
 }

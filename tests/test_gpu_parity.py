@@ -491,6 +491,9 @@ def test_score_order_into_pinned_buffers(ctx, n):
     tie = np.arange(n, dtype=np.uint32)[::-1].copy()
     s1, o1 = ctx.score_order(Extractor.make(), wl.text, wl.offsets, w, tie)
     outs = (pinned_empty(n, np.float64), pinned_empty(n, np.int64))
+    outs[0][:] = np.nan
+    s3 = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w, out=outs[0])
+    assert (s3.view(np.uint64) == s1.view(np.uint64)).all()
     for _ in range(2):  # reused buffers
         outs[0][:] = np.nan
         outs[1][:] = -1
