@@ -21,7 +21,8 @@
 //                   histogram); tie-rank digits are skipped when the ranks
 //                   are already non-decreasing in input order;
 //   radix_scatter   stable rank within the CTA via warp __match_any_sync +
-//                   per-warp digit counters, then a scattered write.
+//                   per-warp digit counters; the tile is laid out in digit
+//                   order in shared memory and written run by run (coalesced).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -147,24 +148,55 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
     __syncwarp();
   }
   __syncthreads();
-  {  // exclusive prefix over warps per digit (thread = digit)
+  __shared__ uint32_t tstart[256];  // the tile's digit runs, exclusive prefix
+  __shared__ uint32_t wsum[kThreads / 32];
+  {  // thread = digit: each warp's offset inside the digit's run, the run length
     const int d = threadIdx.x;
-    uint32_t run = gbase[d];
+    uint32_t run = 0;
     for (int w = 0; w < kThreads / 32; ++w) {
       const uint32_t c = wcnt[w][d];
       wcnt[w][d] = run;
       run += c;
     }
+    // exclusive scan of the run lengths over the 256 digits
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t wb = 0;
+    for (int w = 0; w < warp; ++w) wb += wsum[w];
+    tstart[d] = wb + x - run;
   }
   __syncthreads();
+  // the tile in digit order in shared memory, then written out run by run:
+  // consecutive threads store consecutive addresses of a digit's run instead
+  // of every key landing in its own sector
+  __shared__ uint64_t s_hi[kTileKeys];
+  __shared__ uint32_t s_lo[kTileKeys], s_val[kTileKeys];
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     if (dg[r] < 256u) {
-      const uint32_t p = wcnt[warp][dg[r]] + rk[r];
-      khi_out[p] = hi[r];
-      klo_out[p] = lo[r];
-      val_out[p] = vv[r];
+      const uint32_t lp = tstart[dg[r]] + wcnt[warp][dg[r]] + rk[r];
+      s_hi[lp] = hi[r];
+      s_lo[lp] = lo[r];
+      s_val[lp] = vv[r];
     }
+  }
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kTileKeys;
+  const int cnt = (int)(n - t0 < kTileKeys ? n - t0 : (int64_t)kTileKeys);
+  for (int k = threadIdx.x; k < cnt; k += kThreads) {
+    const uint64_t h = s_hi[k];
+    const uint32_t l = s_lo[k];
+    const uint32_t d = digit_of(h, l, pos);
+    const uint32_t p = gbase[d] + (uint32_t)k - tstart[d];
+    khi_out[p] = h;
+    klo_out[p] = l;
+    val_out[p] = s_val[k];
   }
 }
 
