@@ -1,49 +1,15 @@
-// features.hpp over libpars_cuda (replaces proj/src/features.cpp and
-// proj/src/error.cpp). extract_features / extract_all run the fused GPU
-// featurizer (featurize.cu, CSR mode); results are bit-identical to the
+// features.hpp over libpars_cuda (replaces proj/src/features.cpp; the
+// reference's own error.cpp stays in the program — it is not on the hot path,
+// so pars::strf / pars::fail resolve against it at load time).
+// extract_features / extract_all run the fused GPU featurizer (featurize.cu, CSR mode); results are bit-identical to the
 // reference (tests: the reference's own test_features.cpp, compiled against
 // this file — oracle/Makefile `conformance`).
-#include <cstdarg>
-#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
 #include "shim.hpp"
 
 namespace pars {
-
-// ---- error.cpp ------------------------------------------------------------
-namespace {
-std::string vstrf(const char* fmt, va_list ap) {
-  va_list ap2;
-  va_copy(ap2, ap);
-  int len = std::vsnprintf(nullptr, 0, fmt, ap);
-  if (len < 0) {
-    va_end(ap2);
-    return fmt;
-  }
-  std::string out(static_cast<size_t>(len), '\0');
-  std::vsnprintf(out.data(), out.size() + 1, fmt, ap2);
-  va_end(ap2);
-  return out;
-}
-}  // namespace
-
-std::string strf(const char* fmt, ...) {
-  va_list ap;
-  va_start(ap, fmt);
-  std::string out = vstrf(fmt, ap);
-  va_end(ap);
-  return out;
-}
-
-void fail(const char* fmt, ...) {
-  va_list ap;
-  va_start(ap, fmt);
-  std::string out = vstrf(fmt, ap);
-  va_end(ap);
-  throw Error(out);
-}
 
 // ---- device context ---------------------------------------------------------
 namespace b200 {

@@ -2,10 +2,12 @@
 // LinearScorer scoring — single prompts, batches and FeatureVecs — runs the
 // GPU kernels in exact fp64 mode (bit-identical to features.hpp:31-35 +
 // scorer.cpp:40-42). Scorer::score_batch is non-virtual in the reference
-// header, so it dispatches on the dynamic type: LinearScorer -> one fused GPU
-// launch over the whole dataset; any other Scorer (OracleScorer, user
-// subclasses) is not a predictor and keeps the per-record virtual call.
+// header, so it dispatches on the exact dynamic type: LinearScorer -> one
+// fused GPU launch over the whole dataset; any other Scorer (OracleScorer,
+// user subclasses of Scorer or of LinearScorer) keeps the per-record virtual
+// call, so overrides are honoured as in scorer.cpp:13-21.
 #include <exception>
+#include <typeinfo>
 
 #include "pars/metrics.hpp"
 #include "pars/scorer.hpp"
@@ -43,7 +45,11 @@ std::vector<double> linear_scores(const LinearScorer& s, const Dataset& ds) {
 }  // namespace
 
 std::vector<double> Scorer::score_batch(const Dataset& ds) const {
-  if (const auto* lin = dynamic_cast<const LinearScorer*>(this)) return linear_scores(*lin, ds);
+  // exact type, not dynamic_cast: a subclass of LinearScorer may override
+  // score(const PromptRecord&), and the reference's loop (scorer.cpp:16)
+  // calls that override
+  if (typeid(*this) == typeid(LinearScorer))
+    return linear_scores(static_cast<const LinearScorer&>(*this), ds);
   std::vector<double> out(ds.records.size());
   for (size_t i = 0; i < ds.records.size(); ++i) out[i] = score(ds.records[i]);
   return out;
