@@ -22,6 +22,7 @@ Launch: python bench.py [--gpus N --steps K --warmup W] (torchrun for N>1).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -157,7 +158,8 @@ def shard(n, world, rank):
 class CpuReferenceScoring:
     """The reference library (oracle/_ref, compiled from /root/reference) on
     the host cores: Scorer::score_batch (OpenMP, all threads) + select_batch
-    over a bounded sample of the same workload."""
+    (ref_capi.cpp ref_score_order) over a bounded sample of the same
+    workload."""
 
     def __init__(self, wl, w, sample_n, threads):
         from oracle.bind import Extractor as OEx
@@ -168,17 +170,27 @@ class CpuReferenceScoring:
         offs = wl.offsets[: n + 1] - wl.offsets[0]
         text = wl.text[wl.offsets[0]:wl.offsets[n]]
         self.ds = R.from_arrays(text, offs, wl.output_len[:n], wl.prompt_len[:n])
-        self.ids = ["p%06d" % i for i in range(n)]
         self.ex = OEx.make()
         self.w = w
 
     def step(self):
         t0 = time.perf_counter()
-        s = self.R.score_batch(self.ex, self.ds, self.w)
-        t1 = time.perf_counter()
-        self.R.select_batch(np.zeros(self.n), self.ids, s, np.zeros(self.n, np.uint8), 0.0, self.n)
-        t2 = time.perf_counter()
-        return self.n / (t2 - t0), t1 - t0, t2 - t1
+        self.R.score_order(self.ex, self.ds, self.w)
+        return self.n / (time.perf_counter() - t0)
+
+
+def repo_native_loaded():
+    """Shared objects of this repository mapped into this process (evidence of
+    which native code ran: the product, the reference build, the tools)."""
+    out = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            path = ln.split()[-1] if ln.strip() else ""
+            if path.endswith(".so") and path.startswith(str(ROOT)):
+                out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 def host_threads():
@@ -199,36 +211,61 @@ def cpu_model():
 
 
 def run_reference(args):
+    """The reference's own CPU path on this host, clean: only oracle/_ref (the
+    reference library compiled from /root/reference, shipped prebuilt) and
+    numpy are loaded — no module or shared object of this repository's
+    product. Inputs come from the reference's own synthesize_dataset (seed 31)
+    padded to 512 tokens by the reference's Rng (ref_capi.cpp ref_pad_dataset),
+    i.e. the same 1M-prompt C4 workload as our arm (our generator is pinned
+    bit-identical to it). One step = Scorer::score_batch over all 1M prompts
+    (OpenMP, every host thread) + select_batch of the burst, the reference's
+    stock code path (ref_capi.cpp ref_score_order)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2510_03243_b200 import Workload
-    # the reference's own generator would produce the identical text; ours is
-    # pinned bit-identical to it (tests/test_abi.py) and much faster
-    sample = args.cpu_sample
-    wl = Workload.synthesize(sample, SEED, pad_tokens=PAD_TOKENS, pad_seed=PAD_SEED)
-    w = np.random.default_rng(1234).normal(size=DIM) * 0.05
+    from oracle.bind import Dataset as RefDataset
+    from oracle.bind import Extractor as OEx
+    from oracle.bind import Ref
+    R = Ref()
     threads = host_threads()
-    ref = CpuReferenceScoring(wl, w, sample, threads)
-    vals = []
+    R.set_threads(threads)
+    n = N_PROMPTS
+    t0 = time.perf_counter()
+    ds = RefDataset(R, R.L.ref_synthesize(n, 5.0, 1.2, SEED, 0, 0), export=False)
+    R.pad_dataset(ds, PAD_TOKENS, PAD_SEED)
+    t_gen = time.perf_counter() - t0
+    w = np.random.default_rng(1234).normal(size=DIM) * 0.05
+    ex = OEx.make()
     for _ in range(args.warmup):
-        ref.step()
+        R.score_order(ex, ds, w)
+    ts = []
     for _ in range(args.steps):
-        vals.append(ref.step()[0])
-    value = float(np.median(vals))
+        t0 = time.perf_counter()
+        s, order = R.score_order(ex, ds, w)
+        ts.append(time.perf_counter() - t0)
+    step_s = float(np.median(ts))
+    value = n / step_s
     line = {
         "impl": "reference", "metric": "prompts scored/s", "value": value, "unit": "prompts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sample / value, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * step_s, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C4: score + SJF-sort 1M prompts x 512 tokens (reference CPU, "
-                               f"bounded sample of {sample} prompts per step)",
-                   "global_batch": N_PROMPTS, "seq_len": PAD_TOKENS, "parallelism": "openmp"},
+        "config": {"workload": "C4: score + SJF-sort 1M synthetic prompts x 512 tokens "
+                               "(reference CPU: Scorer::score_batch + select_batch)",
+                   "global_batch": n, "seq_len": PAD_TOKENS, "parallelism": "openmp",
+                   "extractor": "hashed word{1}+char{3}, D=4096, L2",
+                   "inputs": f"reference synthesize_dataset({n}, seed 31) + C4 padding (Rng seed 5)"},
         "cpu_baseline": {"value": value, "unit": "prompts/s", "cores": threads, "kind": "reference",
                          "cpu_model": cpu_model(),
-                         "sample": f"first {sample} prompts of the C4 workload, score_batch + select_batch"},
+                         "sample": f"the full C4 workload ({n} prompts) per step; median of "
+                                   f"{args.steps} steps"},
         "e2e": {"value": value, "unit": "prompts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # digests of the last step's outputs, comparable with our arm's
+        "outputs": {"scores_sha256": hashlib.sha256(s.tobytes()).hexdigest()[:32],
+                    "order_sha256": hashlib.sha256(order.astype(np.int64).tobytes()).hexdigest()[:32]},
+        "workload_gen_s": t_gen,
+        "native_loaded": repo_native_loaded(),
     }
     print(json.dumps(line))
 
@@ -316,14 +353,25 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
 
-    # parity spot check of this shard against the oracle (small sample, untimed)
+    # full parity of this shard (untimed): every exact score bit-identical to
+    # the oracle (the C restatement, threaded over the host cores) and the
+    # shard's SJF order identical to the oracle's select_batch restatement
     from oracle.bind import Extractor as OEx
     from oracle.bind import Oracle
     o = Oracle()
-    chk = min(2000, n)
-    so = o.score_batch(OEx.make(), wl.text, wl.offsets[b:b + chk + 1], w, 0.0)
-    got = d_scores[:chk].cpu().numpy()
+    t_par = time.perf_counter()
+    got = d_scores[:n].cpu().numpy()
+    so = o.score_batch(OEx.make(), wl.text, wl.offsets[b:e + 1], w, 0.0, threads=host_threads())
     parity_ok = bool((got.view(np.uint64) == so.view(np.uint64)).all())
+    got_order = d_order[:n].cpu().numpy().astype(np.int64)
+    oorder = o.select_order(np.zeros(n), ["p%06d" % i for i in range(b, e)], so,
+                            np.zeros(n, np.uint8), 0.0)
+    order_ok = bool((got_order == oorder).all())
+    t_par = time.perf_counter() - t_par
+    outputs = None
+    if world == 1:
+        outputs = {"scores_sha256": hashlib.sha256(got.tobytes()).hexdigest()[:32],
+                   "order_sha256": hashlib.sha256(got_order.tobytes()).hexdigest()[:32]}
     global_order_ok = None
     if world > 1 and rank == 0:
         # the merged global order equals one sort of all N gathered scores
@@ -420,11 +468,11 @@ def run_ours(args):
             thr = host_threads()
             ref = CpuReferenceScoring(wl, w, args.cpu_sample, thr)
             ref.step()  # warm
-            v, ts, tsel = ref.step()
+            v = max(ref.step() for _ in range(3))  # best of 3
             cpu = {"value": v, "unit": "prompts/s", "cores": thr, "kind": "reference",
                    "cpu_model": cpu_model(),
                    "sample": f"first {ref.n} prompts of the same C4 workload: score_batch "
-                             f"({ts:.2f} s, OpenMP {thr} threads) + select_batch ({tsel:.3f} s)"}
+                             f"(OpenMP {thr} threads) + select_batch, best of 3"}
         line = {
             "metric": "prompts scored/s", "value": value, "unit": "prompts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -448,14 +496,22 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
             "gpu_launches": int(launches),
             "clocks": clk,
-            "parity": {"scores_bitexact_sample": parity_ok, "sample": chk,
+            "parity": {"c4_scores_all": parity_ok, "c4_order_all": order_ok, "prompts_checked": n,
+                       "check_s": t_par,
+                       "oracle": "oracle/pars_oracle.c score_batch + select_batch restatement",
                        **({"global_order_equals_full_sort": global_order_ok} if world > 1 else {})},
-            "pairs": pairs,
-            "kendall_tau": tau,
-            "embeddings": embed,
-            "configs": configs,
+            "outputs": outputs,
+            "native_loaded": repo_native_loaded(),
             "workload_gen_s": t_gen,
         }
+        # the bulky per-config detail goes on its own line first; the driver
+        # reads the last line, which stays compact
+        print(json.dumps({"detail": True, "pairs": pairs, "kendall_tau": tau,
+                          "embeddings": embed, "configs": configs}))
+        if pairs is not None:
+            print(json.dumps({"metric": "filtered pairs/s", "value": pairs["value"],
+                              "unit": "pairs/s", "n_gpus": world,
+                              "ms_per_step": pairs["ms_per_step"], "config": "C5"}))
         print(json.dumps(line))
     ctx.close()
     if world > 1:

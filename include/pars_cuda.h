@@ -46,7 +46,6 @@ extern "C" {
 
 typedef struct pars_ctx pars_ctx;
 typedef struct pars_features pars_features; /* device-resident CSR */
-typedef struct pars_workload pars_workload; /* host-resident synthetic prompts */
 
 /* pars::FeatureExtractor (features.hpp:17-25) as a C POD.
  * kind: 0 HashedText, 1 PrecomputedEmbedding; norm: 0 None, 1 L2. */
@@ -355,23 +354,6 @@ int pars_dev_kendall_counts(pars_ctx* ctx, const double* d_x, const double* d_y,
 /* finish_tau (metrics.cpp:13-32): counts5 = {n_c, n_d, n0, n1, n2}. */
 int pars_kendall_finish(const uint64_t* counts4, int64_t n, uint64_t* counts5,
                         double* tau_b);
-
-/* ---- synthetic workloads (host; dataset.cpp:204-297 restated) ----------
- * synthesize_dataset(n, lognormal(mu, sigma), seed) with the reference's
- * generator (bit-identical text and lengths); pad_tokens > 0 pads every
- * prompt with " w<k>" tokens, k = Rng(pad_seed).below(50), to exactly
- * pad_tokens whitespace tokens. */
-int pars_workload_synthesize(uint64_t n, double mu, double sigma,
-                             uint64_t seed, int64_t pad_tokens,
-                             uint64_t pad_seed, pars_workload** out);
-int64_t pars_workload_count(const pars_workload* w);
-int64_t pars_workload_text_bytes(const pars_workload* w);
-/* Pointers stay valid until pars_workload_free. */
-const char* pars_workload_text(const pars_workload* w);
-const int64_t* pars_workload_offsets(const pars_workload* w);
-const int64_t* pars_workload_output_len(const pars_workload* w);
-const int64_t* pars_workload_prompt_len(const pars_workload* w);
-void pars_workload_free(pars_workload* w);
 
 #ifdef __cplusplus
 }

@@ -239,12 +239,15 @@ def ids_arena(ids):
 class Dataset:
     """Flat view of a pars::Dataset living inside libpars_ref.so."""
 
-    def __init__(self, ref: "Ref", handle):
+    def __init__(self, ref: "Ref", handle, export=True):
         if not handle:
             raise OracleError(ref.L.ref_last_error().decode("utf-8", "replace"))
         self.ref, self.h = ref, handle
         L = ref.L
         n = L.ref_dataset_size(handle)
+        self.n = n
+        if not export:  # handle only (no flat copy of the records)
+            return
         nb = L.ref_dataset_text_bytes(handle)
         ed = L.ref_dataset_embed_dim(handle)
         self.text = np.zeros(max(nb, 1), np.uint8)
@@ -334,6 +337,9 @@ class Ref:
         L.ref_listmle_lists.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_void_p]
         L.ref_poisson.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_void_p]
         L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_pad_dataset.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
+        L.ref_score_order.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                      C.c_void_p]
 
     def _err(self):
         return OracleError(self.L.ref_last_error().decode("utf-8", "replace"))
@@ -450,6 +456,20 @@ class Ref:
         if n < 0:
             raise self._err()
         return a[:n].copy(), b[:n].copy(), y[:n].copy(), rel[:n].copy()
+
+    def pad_dataset(self, ds, pad_tokens, pad_seed):
+        """C4 padding of SURVEY §8(d) applied in place (ref_capi.cpp)."""
+        if self.L.ref_pad_dataset(ds.h, pad_tokens, pad_seed) != 0:
+            raise self._err()
+
+    def score_order(self, ex, ds, w, bias=0.0):
+        """score_batch + select_batch of a burst (ref_capi.cpp ref_score_order)."""
+        s = np.zeros(ds.n, np.float64)
+        o = np.zeros(ds.n, np.uint64)
+        if self.L.ref_score_order(C.byref(ex), ds.h, _ptr(np.ascontiguousarray(w, np.float64)),
+                                  bias, _ptr(s), _ptr(o)) != 0:
+            raise self._err()
+        return s, o.astype(np.int64)
 
     def select_batch(self, arrival, ids, score, boosted, now, free_slots):
         n = len(arrival)

@@ -375,6 +375,49 @@ int ref_pairwise_loss_grad(const double* w, uint32_t dim, double bias,
   });
 }
 
+// C4 padding: every prompt padded with " w<k>" tokens,
+// k = Rng(pad_seed).below(50) (the reference's own Rng, rng.hpp), to exactly
+// pad_tokens whitespace tokens, records in order. Used by bench.py's
+// reference arm on a dataset from the reference's synthesize_dataset.
+int ref_pad_dataset(void* h, int64_t pad_tokens, uint64_t pad_seed) {
+  return guard([&] {
+    Dataset& ds = *static_cast<Dataset*>(h);
+    Rng pad(pad_seed);
+    for (PromptRecord& r : ds.records) {
+      for (int64_t k = r.prompt_len; k < pad_tokens; ++k) {
+        r.prompt_text += " w";
+        r.prompt_text += std::to_string(pad.below(50));
+      }
+      r.prompt_len = std::max<int64_t>(r.prompt_len, pad_tokens);
+    }
+  });
+}
+
+// The C4 step on the reference's own code path: LinearScorer::score_batch
+// over the dataset (scorer.cpp:9-24, OpenMP), then the requests of a burst
+// (arrival 0, the record ids) ordered by select_batch (scheduler.cpp:33-60)
+// with every slot free. scores: n doubles, order: n indices.
+int ref_score_order(const RefExtractor* e, void* h, const double* w, double bias,
+                    double* scores, uint64_t* order) {
+  return guard([&] {
+    const Dataset& ds = *static_cast<Dataset*>(h);
+    FeatureExtractor ex = to_ex(e);
+    LinearScorer sc(ex, std::vector<double>(w, w + ex.dim), bias);
+    std::vector<double> s = sc.score_batch(ds);
+    std::vector<Request> q(ds.records.size());
+    for (size_t i = 0; i < q.size(); ++i) {
+      q[i].record_idx = static_cast<uint32_t>(i);
+      q[i].prompt_id = ds.records[i].id;
+      q[i].arrival_time = 0.0;
+      q[i].score = s[i];
+    }
+    PolicyConfig cfg;
+    auto sel = select_batch(q, 0.0, q.size(), cfg);
+    std::memcpy(scores, s.data(), sizeof(double) * s.size());
+    for (size_t i = 0; i < sel.size(); ++i) order[i] = sel[i];
+  });
+}
+
 // ---- scheduling -----------------------------------------------------------
 // ids: NUL-separated arena with offsets; out: selected indices.
 int64_t ref_select_batch(int64_t n, const double* arrival, const char* ids,

@@ -136,14 +136,6 @@ def _load() -> C.CDLL:
         "pars_kendall_tau_algo": (C.c_int, [vp, vp, vp, i64, vp, vp, C.c_int]),
         "pars_dev_merge_orders": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "pars_dev_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
-        "pars_workload_synthesize": (C.c_int, [u64, dbl, dbl, u64, i64, u64, vp]),
-        "pars_workload_count": (i64, [vp]),
-        "pars_workload_text_bytes": (i64, [vp]),
-        "pars_workload_text": (vp, [vp]),
-        "pars_workload_offsets": (vp, [vp]),
-        "pars_workload_output_len": (vp, [vp]),
-        "pars_workload_prompt_len": (vp, [vp]),
-        "pars_workload_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -244,9 +236,36 @@ def tie_ranks(arrival, ids) -> np.ndarray:
     return r
 
 
+WORKLOAD_LIB_PATH = Path(__file__).resolve().parents[1] / "tools" / "libpars_workload.so"
+_WL = None
+
+
+def workload_lib():
+    """The synthetic-workload TOOL library (tools/libpars_workload.so): input
+    generation for benchmarks and tests, not part of libpars_cuda.so."""
+    global _WL
+    if _WL is None:
+        if not WORKLOAD_LIB_PATH.exists():
+            raise FileNotFoundError(f"{WORKLOAD_LIB_PATH} not built (make -C tools/workload)")
+        L = C.CDLL(str(WORKLOAD_LIB_PATH))
+        vp, i64 = C.c_void_p, C.c_int64
+        for name, res, args in (
+                ("pars_workload_synthesize", C.c_int,
+                 [C.c_uint64, C.c_double, C.c_double, C.c_uint64, i64, C.c_uint64, vp]),
+                ("pars_workload_count", i64, [vp]), ("pars_workload_text_bytes", i64, [vp]),
+                ("pars_workload_text", vp, [vp]), ("pars_workload_offsets", vp, [vp]),
+                ("pars_workload_output_len", vp, [vp]), ("pars_workload_prompt_len", vp, [vp]),
+                ("pars_workload_free", None, [vp]), ("pars_workload_last_error", C.c_char_p, [])):
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _WL = L
+    return _WL
+
+
 @dataclass
 class Workload:
-    """Synthetic prompts (dataset.cpp:204-297 restated on the host)."""
+    """Synthetic prompts (dataset.cpp:204-297 restated on the host by the
+    workload tool library, tools/libpars_workload.so)."""
 
     text: np.ndarray  # uint8 view of the (pinned) arena
     offsets: np.ndarray
@@ -257,9 +276,11 @@ class Workload:
     @classmethod
     def synthesize(cls, n: int, seed: int, mu: float = 5.0, sigma: float = 1.2,
                    pad_tokens: int = 0, pad_seed: int = 5) -> "Workload":
-        L = lib()
+        L = workload_lib()
         h = C.c_void_p()
-        _check(L.pars_workload_synthesize(n, mu, sigma, seed, pad_tokens, pad_seed, C.byref(h)))
+        rc = L.pars_workload_synthesize(n, mu, sigma, seed, pad_tokens, pad_seed, C.byref(h))
+        if rc != 0:
+            raise ParsError(rc, L.pars_workload_last_error().decode("utf-8", "replace"))
         cnt = L.pars_workload_count(h)
         nb = L.pars_workload_text_bytes(h)
         text = np.ctypeslib.as_array(C.cast(L.pars_workload_text(h), C.POINTER(C.c_uint8)),
@@ -280,7 +301,7 @@ class Workload:
 
     def close(self):
         if self._h:
-            lib().pars_workload_free(C.c_void_p(self._h))
+            workload_lib().pars_workload_free(C.c_void_p(self._h))
             self._h = 0
             self.text = np.zeros(0, np.uint8)
 

@@ -2,9 +2,9 @@
 //   * build_pairs (pairs.cpp:8-36): one mt19937_64 stream, draw by draw;
 //   * the integer Eq. 1 table dmin[m] (pairs.hpp:21-24 evaluated on host with
 //     the reference's own double division, once per (delta, max_len));
-//   * tie ranks for the priority key (scheduler.cpp:44-49 tie_key);
-//   * the synthetic workload generator (dataset.cpp:204-297 and the C4
-//     padding of SURVEY §8(d)) used to produce inputs; bit-identical text.
+//   * tie ranks for the priority key (scheduler.cpp:44-49 tie_key).
+// (The synthetic workload generator is a tool, tools/workload, not part of
+// this library.)
 // Compiled with -ffp-contract=off (the reference objects contain no FMA).
 #include <algorithm>
 #include <cmath>
@@ -22,79 +22,21 @@
 #include <cuda_runtime.h>
 
 #include "pars_cuda.h"
+#include "rng_host.hpp"
 
 namespace pars_b200 {
 void set_error(const char* fmt, ...);
 }
 using pars_b200::set_error;
+using pars_b200::Rng;
 
 namespace {
-
-// The reference's Rng (rng.hpp:22-75): mt19937_64 + hand-coded samplers.
-class Rng {
- public:
-  explicit Rng(uint64_t seed) : eng_(seed) {}
-  uint64_t u64() { return eng_(); }
-  double uniform01() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
-  uint64_t below(uint64_t n) {
-    return static_cast<uint64_t>((static_cast<unsigned __int128>(eng_()) * n) >> 64);
-  }
-  double exponential(double rate) { return -std::log1p(-uniform01()) / rate; }
-  double normal() {
-    if (have_spare_) {
-      have_spare_ = false;
-      return spare_;
-    }
-    constexpr double kTwoPi = 6.283185307179586476925286766559;
-    double u1 = 1.0 - uniform01();
-    double u2 = uniform01();
-    double r = std::sqrt(-2.0 * std::log(u1));
-    double a = kTwoPi * u2;
-    spare_ = r * std::sin(a);
-    have_spare_ = true;
-    return r * std::cos(a);
-  }
-  template <class T>
-  void shuffle(std::vector<T>& v) {
-    for (size_t i = v.size(); i > 1; --i) std::swap(v[i - 1], v[below(i)]);
-  }
-
- private:
-  std::mt19937_64 eng_;
-  double spare_ = 0.0;
-  bool have_spare_ = false;
-};
 
 inline double rel_diff(int64_t a, int64_t b) {
   return static_cast<double>(std::llabs(a - b)) / static_cast<double>(std::max(a, b));
 }
 
-inline void append_u64(std::string& s, uint64_t v) {
-  char buf[24];
-  int n = 0;
-  do {
-    buf[n++] = (char)('0' + v % 10);
-    v /= 10;
-  } while (v);
-  while (n) s.push_back(buf[--n]);
-}
-inline void append_i64(std::string& s, int64_t v) {
-  if (v < 0) {
-    s.push_back('-');
-    append_u64(s, (uint64_t)(-(v + 1)) + 1);
-  } else {
-    append_u64(s, (uint64_t)v);
-  }
-}
-
 }  // namespace
-
-struct pars_workload {
-  char* text = nullptr;  // pinned when possible
-  bool pinned = false;
-  int64_t bytes = 0;
-  std::vector<int64_t> offsets, output_len, prompt_len;
-};
 
 extern "C" {
 
@@ -226,113 +168,6 @@ int pars_tie_ranks(const double* arrival, const char* ids, const int64_t* offs, 
     rank[o[k]] = r;
   }
   return PARS_OK;
-}
-
-int pars_workload_synthesize(uint64_t n, double mu, double sigma, uint64_t seed, int64_t pad_tokens,
-                             uint64_t pad_seed, pars_workload** out) {
-  *out = nullptr;
-  if (n < 1) {
-    set_error("synthesize: n must be >= 1");
-    return PARS_ERR_INVALID;
-  }
-  if (sigma <= 0.0) {
-    set_error("synthesize: sigma must be > 0 (got %g)", sigma);
-    return PARS_ERR_INVALID;
-  }
-  constexpr double kLatentStep = 0.05;  // dataset.cpp:196
-  const int64_t min_len = 1, max_len = 16384;
-  auto* w = new pars_workload();
-  w->offsets.resize(n + 1);
-  w->output_len.resize(n);
-  w->prompt_len.resize(n);
-  Rng rng(seed);
-  std::vector<std::string> texts(n);
-  auto clamp_len = [&](double v) {
-    int64_t len = static_cast<int64_t>(std::llround(v));
-    return std::clamp(len, min_len, max_len);
-  };
-  const int64_t q_cap =
-      static_cast<int64_t>(std::llround(std::log(static_cast<double>(max_len)) / kLatentStep));
-  std::vector<std::string> tokens;
-  for (uint64_t i = 0; i < n; ++i) {
-    (void)rng.uniform01();  // mixture pick (single component, dataset.cpp:229-239)
-    const double z = mu + sigma * rng.normal();
-    const int64_t q = static_cast<int64_t>(std::llround(z / kLatentStep));
-    const int64_t clean = clamp_len(std::exp(kLatentStep * static_cast<double>(q)));
-    w->output_len[i] = clean;
-    const int64_t q_therm = std::clamp<int64_t>(q, 0, q_cap);
-    tokens.clear();
-    std::string t = "len";
-    append_i64(t, q);
-    tokens.push_back(t);
-    for (int64_t lvl = 0; lvl <= q_therm; ++lvl) {
-      std::string s = "lvl";
-      append_i64(s, lvl);
-      tokens.push_back(std::move(s));
-    }
-    const size_t n_filler = 4 + rng.below(21);
-    for (size_t f = 0; f < n_filler; ++f) {
-      std::string s = "w";
-      append_u64(s, rng.below(50));
-      tokens.push_back(std::move(s));
-    }
-    rng.shuffle(tokens);
-    std::string& text = texts[i];
-    for (const std::string& tok : tokens) {
-      if (!text.empty()) text += ' ';
-      text += tok;
-    }
-    w->prompt_len[i] = static_cast<int64_t>(tokens.size());
-  }
-  if (pad_tokens > 0) {  // " w<k>", k = Rng(pad_seed).below(50)
-    Rng pad(pad_seed);
-    for (uint64_t i = 0; i < n; ++i) {
-      std::string& text = texts[i];
-      for (int64_t k = w->prompt_len[i]; k < pad_tokens; ++k) {
-        text += " w";
-        append_u64(text, pad.below(50));
-      }
-      w->prompt_len[i] = std::max<int64_t>(w->prompt_len[i], pad_tokens);
-    }
-  }
-  int64_t total = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    w->offsets[i] = total;
-    total += (int64_t)texts[i].size();
-  }
-  w->offsets[n] = total;
-  w->bytes = total;
-  if (cudaHostAlloc(reinterpret_cast<void**>(&w->text), std::max<int64_t>(total, 1),
-                    cudaHostAllocDefault) == cudaSuccess) {
-    w->pinned = true;
-  } else {
-    cudaGetLastError();
-    w->text = static_cast<char*>(std::malloc(std::max<int64_t>(total, 1)));
-    if (!w->text) {
-      delete w;
-      set_error("synthesize: out of host memory");
-      return PARS_ERR_OOM;
-    }
-  }
-  for (uint64_t i = 0; i < n; ++i)
-    std::memcpy(w->text + w->offsets[i], texts[i].data(), texts[i].size());
-  *out = w;
-  return PARS_OK;
-}
-
-int64_t pars_workload_count(const pars_workload* w) { return (int64_t)w->output_len.size(); }
-int64_t pars_workload_text_bytes(const pars_workload* w) { return w->bytes; }
-const char* pars_workload_text(const pars_workload* w) { return w->text; }
-const int64_t* pars_workload_offsets(const pars_workload* w) { return w->offsets.data(); }
-const int64_t* pars_workload_output_len(const pars_workload* w) { return w->output_len.data(); }
-const int64_t* pars_workload_prompt_len(const pars_workload* w) { return w->prompt_len.data(); }
-void pars_workload_free(pars_workload* w) {
-  if (!w) return;
-  if (w->pinned)
-    cudaFreeHost(w->text);
-  else
-    std::free(w->text);
-  delete w;
 }
 
 }  // extern "C"
