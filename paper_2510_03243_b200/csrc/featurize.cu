@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "featurize.cuh"
@@ -47,6 +48,7 @@ constexpr int kGroup = 16;                   // prompts per exact chain group (o
 constexpr uint32_t kBias2 = 0x80008000u;     // two biased 16-bit zero counters
 constexpr int64_t kNarrowMaxFeatures = 32767;  // |count| <= features: 16 bits cannot wrap
 constexpr size_t kMaxSmemPerBlock = 200 * 1024;
+constexpr size_t kMaxLaneSmem = 227 * 1024;  // per-CTA opt-in maximum on sm_100
 
 struct WarpSmem {
   uint32_t* counts;  // narrow: 2 x u16 biased per word; wide: int32
@@ -810,6 +812,364 @@ __global__ void __launch_bounds__(256) featurize_seq_kernel(const FeatConfig c, 
     chain_group(c, a, lists, true, lane, gn, g_prompt, g_off, g_cnt, g_inv);
 }
 
+// ---- lane-range front end, v2 (score modes; word {1} + char {3}, pow2 dims) ----
+//
+// Same per-lane decomposition as featurize_seq_kernel (lane l owns the
+// tokens that start in its word-aligned byte range and runs the reference's
+// per-byte loop over them, features.cpp:80-101), restructured for fewer
+// instructions per byte and for shared-memory text:
+//   * the prompt is staged into a per-warp shared buffer by cp.async (16-byte
+//     copies, L2 evict-first policy: the text streams through L2 once) while
+//     the previous prompt is walked and scored, and the buffer's bytes
+//     outside the prompt are overwritten with spaces, so the byte loop has
+//     no edge logic and reads 4 bytes per LDS (stride-wpl words per lane,
+//     no L1 tag traffic);
+//   * spaces are rewritten to 0x1f ('\x1f', the word separator the reference
+//     hashes after every word token) in the loaded word, so one expression
+//     gives both features a byte can emit: e = ((space ? hw : B) ^ b') * P is
+//     the trigram ending at a token byte and the word that ends at a space;
+//   * emission is predicated (no dummy target): the counter word address is
+//     one OR into the table (tables aligned to their size), the bitmap bit
+//     one funnel shift;
+// Prompts that do not fit the buffer run the same loop on global loads.
+constexpr int kLaneTextCap = 2560;   // prompt bytes staged in shared memory per warp
+constexpr int kLaneBuf = kLaneTextCap + 64;  // + 16-byte alignment slack and space padding
+
+__host__ __device__ inline size_t lane_warp_bytes(uint32_t dim) {
+  return (size_t)dim * 2 + dim / 8 + 128 /* dummy words */ + 32 /* increment table */ + kLaneBuf;
+}
+__host__ inline size_t lane_cta_bytes(uint32_t dim, int warps) {
+  return (size_t)dim * 2 /* alignment slack */ + (size_t)warps * lane_warp_bytes(dim);
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// SWAR: 0x80 in every byte of w that is not C-locale whitespace.
+__device__ __forceinline__ uint32_t nonspace_hi(uint32_t w) {
+  const uint32_t x = w ^ 0x20202020u;
+  const uint32_t not_blank = ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x;
+  const uint32_t lo7 = w & 0x7f7f7f7fu;
+  const uint32_t ctl = (0x8d8d8d8du - lo7) & ~w & (lo7 + 0x77777777u);
+  return not_blank & ~ctl & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t hi_to_nibble(uint32_t h) { return ((h >> 7) * 0x01020408u) >> 24; }
+// w with every whitespace byte replaced by 0x1f
+__device__ __forceinline__ uint32_t spaces_to_sep(uint32_t w, uint32_t nsh) {
+  const uint32_t m = (nsh << 1) - (nsh >> 7);  // 0xff in non-space bytes
+  return (w & m) | (0x1f1f1f1fu & ~m);
+}
+
+// One feature e (idx = (e >> 1) & mask, sign = e & 1; features.cpp:29-34):
+// +-1 into the bucket's biased 16-bit half and its touched bit, both as
+// fire-and-forget `red` operations; when ev == 0 both target the lane's own
+// dummy word (never read), so there is no branch (ptxas turns predicated
+// shared-memory reductions into branches). Right shifts are IMAD.HI and the
+// +-1 << (16 * half) product an IMAD, keeping the ALU pipe for the rest.
+// One feature e = z * P (idx = (e >> 1) & mask, sign = e & 1;
+// features.cpp:29-34): +-1 into the bucket's biased 16-bit half and its
+// touched bit, as two fire-and-forget `red` operations issued by every lane
+// (ptxas turns predicated shared-memory reductions into branches). A lane
+// without a feature at this byte (ev bit clear) adds 0 and ORs 0: the
+// increment comes from an 8-entry shared table indexed by (ev bit, e & 3)
+// = {0, 0, 0, 0, -1, +1, -1 << 16, +1 << 16} and the bit is ev << bucket.
+// Bit extraction and right shifts are multiplies (IMAD / IMAD.HI on the FMA
+// pipe), leaving the ALU pipe the xors, selects and address masks.
+template <int K>
+__device__ __forceinline__ void lane_emit(uint32_t lut, uint32_t cbase, uint32_t bbase,
+                                          uint32_t m1, uint32_t m2, uint32_t z, uint32_t ev) {
+  asm volatile(
+      "{\n\t.reg .u32 t, e, ca, ba, e1, e4, d, bt, k, la;\n\t"
+      "mul.lo.u32 k, %5, %6;\n\tmul.hi.u32 k, k, 2;\n\t"          // k = (ev >> K) & 1
+      "mul.lo.u32 e, %0, 435;\n\t"                                  // e = z * P
+      "mul.lo.u32 t, %0, -1073741824;\n\tmul.hi.u32 t, t, 16;\n\t"  // 4 * (e & 3): (z * (P << 30)) = (e & 3) << 30
+      "mad.lo.u32 la, k, 16, %7;\n\tadd.u32 la, la, t;\n\t"
+      "ld.shared.u32 d, [la];\n\t"
+      "and.b32 t, e, %3;\n\tor.b32 ca, t, %1;\n\t"
+      "mul.hi.u32 e1, e, -2147483648;\n\tmul.hi.u32 e4, e, 268435456;\n\t"
+      "and.b32 t, e4, %4;\n\tor.b32 ba, t, %2;\n\t"
+      "shf.l.wrap.b32 bt, k, k, e1;\n\t"
+      "red.shared.add.u32 [ca], d;\n\tred.shared.or.b32 [ba], bt;\n\t}" ::"r"(z),
+      "r"(cbase), "r"(bbase), "r"(m1), "r"(m2), "r"(ev), "n"(1u << (31 - K)), "r"(lut));
+}
+
+// Byte K of an 8-byte step: the rolling char states A (one byte), B (two
+// bytes), the word state hw (reset to the salt at spaces), and the feature
+// that ends at this byte (features.cpp:84-90, :96-99).
+template <int K>
+__device__ __forceinline__ void lane_bytes(uint32_t p, uint32_t ns, uint32_t ev, uint32_t sw,
+                                           uint32_t sc, uint32_t& hw, uint32_t& A, uint32_t& B,
+                                           uint32_t cbase, uint32_t bbase, uint32_t dummy,
+                                           uint32_t m1, uint32_t m2, uint32_t lut) {
+  const uint32_t b = __byte_perm(p, 0u, 0x4440u + (K & 3));
+  const bool sp = ((ns >> K) & 1u) == 0u;
+  const uint32_t An = (sc ^ b) * 0x1b3u;
+  const uint32_t Bn = (A ^ b) * 0x1b3u;
+  const uint32_t z = (sp ? hw : B) ^ b;  // the feature ending here: e = z * P
+  hw = sp ? sw : (hw ^ b) * 0x1b3u;
+  A = An;
+  B = Bn;
+  lane_emit<K>(lut, cbase, bbase, m1, m2, z, ev);
+}
+
+// The byte loop over lane l's range of a prompt occupying [lo, hi) of a
+// space-padded source: SMEM reads the staged buffer at shared address src;
+// otherwise 4-byte global words through seq_word (edges assembled there).
+template <bool SMEM>
+__device__ __forceinline__ void hash_lane(const FeatConfig& c, uint32_t src, const uint8_t* a0,
+                                          int lo, int hi, int rlo, int rhi, int lane, uint32_t cbase,
+                                          uint32_t bbase, uint32_t dummy, uint32_t lut) {
+  const int wpl = (((hi + 3) >> 2) + 31) >> 5;  // words per lane
+  const int cs = lane * wpl * 4, ce = cs + wpl * 4;
+  if (cs >= hi) return;
+  auto word = [&](int r) -> uint32_t {
+    if (SMEM) return lds32(src + (uint32_t)r);
+    return seq_word(a0, r, lo, hi, rlo, rhi);
+  };
+  const uint32_t sw = (uint32_t)c.word_salt[0], sc = (uint32_t)c.char_salt[0];
+  const uint32_t m1 = (c.dim / 2 - 1) << 2, m2 = (c.dim / 32 - 1) << 2;
+  uint32_t prev2 = cs > 0 ? hi_to_nibble(nonspace_hi(word(cs - 4))) >> 2 : 0u;
+  uint32_t hw = sw, A = 0, B = 0, carry = 0;
+  uint32_t w0 = word(cs), w1 = word(cs + 4);
+  for (int r = cs;; r += 8) {
+    const uint32_t n0 = word(r + 8), n1 = word(r + 12);
+    const uint32_t h0 = nonspace_hi(w0), h1 = nonspace_hi(w1);
+    const uint32_t ns = hi_to_nibble(h0) | (hi_to_nibble(h1) << 4);
+    const uint32_t E = (ns << 2) | prev2;  // bit k+2: byte r+k is not a space
+    const uint32_t start = ns & ~(E >> 1);
+    // tokens may start only inside [cs, ce): the second word can lie beyond ce
+    const uint32_t inr = r < ce ? (r + 4 < ce ? 0xffu : 0x0fu) : 0u;
+    const uint32_t own = (ns + ((start & inr) | carry)) ^ ns;
+    carry = own >> 8;
+    const uint32_t ev = ((ns & E) | ~ns) & (E >> 1) & own & 0xffu;  // trigram or word end
+    const uint32_t p0 = spaces_to_sep(w0, h0), p1 = spaces_to_sep(w1, h1);
+    lane_bytes<0>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<1>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<2>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<3>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<4>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<5>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<6>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<7>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    prev2 = ns >> 6;
+    if (!carry && (r + 8 >= ce || r + 8 >= hi)) break;
+    w0 = n0;
+    w1 = n1;
+  }
+}
+
+// Stage text[beg, end) into the warp's buffer (shared address buf): the
+// 16-byte-aligned chunks covering it, by cp.async with zero fill past the
+// launch's readable text; returns the prompt's offset lo inside the buffer.
+__device__ __forceinline__ int lane_stage(uint32_t buf, const uint8_t* text, int64_t beg, int64_t end,
+                                          const uint8_t* rlo, const uint8_t* rhi, int lane,
+                                          uint64_t pol) {
+  const uint8_t* p0 = text + beg;
+  const uint8_t* a0 = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p0) & ~(uintptr_t)15);
+  const int lo = (int)(p0 - a0);
+  const int nch = (lo + (int)(end - beg) + 15) >> 4;
+  for (int k = lane; k < nch; k += 32) {
+    const uint8_t* s = a0 + 16 * k;
+    const uint32_t d = buf + 16u * (uint32_t)k;
+    if (s < rlo) {  // chunk starts before the readable text: bytes one by one
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t v = (s + j >= rlo && s + j < rhi) ? (uint32_t)s[j] : 0x20u;
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(d + j), "r"(v));
+      }
+    } else {
+      const int64_t avail = rhi - s;
+      const uint32_t sz = avail >= 16 ? 16u : (uint32_t)avail;
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(d),
+                   "l"(s), "r"(sz), "l"(pol));
+    }
+  }
+  asm volatile("cp.async.commit_group;");
+  return lo;
+}
+
+// Wait for the staged prompt and pad it with spaces: [0, lo) and [hi, hi+32).
+__device__ __forceinline__ void lane_stage_finish(uint32_t buf, int lo, int hi, int lane) {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();  // every lane's copies have landed before the padding is written
+  if (lane < lo) asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + lane), "r"(0x20u));
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + hi + lane), "r"(0x20u));
+  __syncwarp();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig c, const FeatArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * nwc + warp;
+  const int64_t nw = (int64_t)gridDim.x * nwc;
+  // tables aligned to their size, so a counter address is base | offset
+  const uint32_t tsz = c.dim * 2;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t tb = (s0 + tsz - 1) & ~(tsz - 1);
+  const uint32_t cbase = tb + (uint32_t)warp * tsz;
+  const uint32_t bbase = tb + (uint32_t)nwc * tsz + (uint32_t)warp * (c.dim / 8);
+  const uint32_t dummy = tb + (uint32_t)nwc * (tsz + c.dim / 8) + (uint32_t)warp * 128u + 4u * lane;
+  // increments by (ev bit, half, sign): 0 x4, then -1, +1, -1 << 16, +1 << 16
+  const uint32_t lut = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 128u) + (uint32_t)warp * 32u;
+  const uint32_t buf = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 160u) + (uint32_t)warp * kLaneBuf;
+  if (lane < 8) {
+    const uint32_t dv =
+        lane < 4 ? 0u : ((lane & 1) ? 1u : 0xffffffffu) << ((lane & 2) ? 16 : 0);
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(lut + 4u * lane), "r"(dv));
+  }
+  uint32_t* counts = reinterpret_cast<uint32_t*>(smem + (cbase - s0));
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + (bbase - s0));
+  for (uint32_t k = lane; k < c.dim / 2; k += 32) counts[k] = kBias2;
+  for (uint32_t k = lane; k < c.dim / 32; k += 32) bitmap[k] = 0u;
+  __syncwarp();
+  const uint32_t nb = c.dim >> 10;
+  uint32_t* bm = bitmap + lane * nb;
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(counts);
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+
+  uint32_t* lists = (MODE == kFeatScoreExact) ? a.lists + (size_t)gw * a.list_cap : nullptr;
+  const uint8_t* text_lo = a.text + a.offsets[0];
+  const uint8_t* text_hi = a.text + a.offsets[a.n];
+  auto fits = [&](int64_t beg, int64_t len) {
+    return (int64_t)(reinterpret_cast<uintptr_t>(a.text + beg) & 15u) + len + 32 <= kLaneBuf;
+  };
+  int st_lo = -1;  // buffer offset of the staged prompt (-1: nothing staged)
+  if (gw < a.n) {
+    const int64_t beg = a.offsets[gw], len = a.offsets[gw + 1] - beg;
+    if (fits(beg, len)) st_lo = lane_stage(buf, a.text, beg, beg + len, text_lo, text_hi, lane, pol);
+  }
+  for (int64_t i = gw; i < a.n; i += nw) {
+    const int64_t beg = a.offsets[i], len = a.offsets[i + 1] - beg;
+    if (((len + 1) / 2) + len > kNarrowMaxFeatures) {  // 16-bit counters could wrap
+      if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
+      st_lo = -1;
+    } else if (st_lo >= 0) {
+      lane_stage_finish(buf, st_lo, st_lo + (int)len, lane);
+      hash_lane<true>(c, buf, nullptr, st_lo, st_lo + (int)len, 0, 0, lane, cbase, bbase, dummy, lut);
+    } else if (len > 0) {
+      const uint8_t* base = a.text + beg;
+      const int mis = (int)(reinterpret_cast<uintptr_t>(base) & 3u);
+      const uint8_t* a0 = base - mis;
+      const int lo = mis, hi = mis + (int)len;
+      const int64_t dlo = text_lo - a0, dhi = text_hi - a0;
+      const int rlo = dlo > 0 ? (int)dlo : 0;
+      const int rhi = dhi < (int64_t)hi + 8 ? (int)dhi : hi + 8;
+      hash_lane<false>(c, 0, a0, lo, hi, rlo, rhi, lane, cbase, bbase, dummy, lut);
+    }
+    __syncwarp();
+    // the next prompt streams into the (now free) buffer while this one is
+    // walked and scored
+    st_lo = -1;
+    if (i + nw < a.n) {
+      const int64_t nb2 = a.offsets[i + nw], nl = a.offsets[i + nw + 1] - nb2;
+      if (fits(nb2, nl)) st_lo = lane_stage(buf, a.text, nb2, nb2 + nl, text_lo, text_hi, lane, pol);
+    }
+    if (((len + 1) / 2) + len > kNarrowMaxFeatures) continue;
+    // pass 1: this lane's entry count
+    uint32_t mine = 0;
+    for (uint32_t j = 0; j < nb; ++j) mine += __popc(bm[j]);
+    int tot;
+    const uint32_t off = (uint32_t)warp_excl_scan((int)mine, lane, &tot);
+    // exact mode: the prompt's ascending (idx, count) list goes to its own
+    // slot for the chain kernel (chain_slots_kernel); a prompt with more
+    // entries than a slot holds is chained here from the warp's arena
+    const bool in_slot = (uint32_t)tot <= a.slot_cap;
+    uint32_t* L = nullptr;
+    if (MODE == kFeatScoreExact) L = lists;
+    // pass 2: ascending entries (lane-major = bucket order); resets the table
+    uint32_t pos = off;
+    float facc = 0.f;
+    long long sq = 0;
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint32_t m = bm[j];
+      if (!m) continue;
+      bm[j] = 0u;
+      const uint32_t b0 = (lane * nb + j) * 32;
+      for (uint32_t t = m; t; t &= t - 1) {
+        const uint32_t idx = b0 + __ffs(t) - 1;
+        const int cnt = (int)c16[idx] - 0x8000;
+        c16[idx] = 0x8000;
+        sq += (long long)cnt * cnt;
+        if (MODE == kFeatScoreExact) {
+          const uint32_t ent = (idx << 16) | (uint32_t)(cnt + 0x8000);
+          // slot layout: 4-entry chunk q of prompt i at (q * n + i), so
+          // the chain kernel's threads (one per prompt) read coalesced
+          if (in_slot)
+            a.slots[((size_t)(pos >> 2) * (size_t)a.n + (size_t)i) * 4 + (pos & 3)] = ent;
+          else
+            L[pos] = ent;
+          ++pos;
+        } else {
+          facc += __ldg(a.w32 + idx) * (float)cnt;
+        }
+      }
+    }
+    const double inv = inv_norm(c, warp_sum_i64(sq));
+    if (MODE == kFeatScoreExact) {
+      if (lane == 0) {
+        a.slot_nnz[i] = in_slot ? tot : -1;
+        a.slot_inv[i] = inv;
+      }
+      if (!in_slot) {
+        __syncwarp();
+        chain_group(c, a, lists, true, lane, 1, i, 0, (uint32_t)tot, inv);
+      }
+    } else {
+      facc = warp_sum_f32(facc);
+      if (lane == 0) a.scores[i] = (double)(facc * (float)inv) + a.bias;
+    }
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Exact mode, second pass: one thread per prompt runs the reference's
+// sequential dot (features.hpp:31-35: s += w[idx] * v in ascending index
+// order, v = count * inv as in features.cpp:113-120; then + bias,
+// scorer.cpp:40-42) over the slot the lane kernel wrote. Separate from the
+// hashing kernel so that the dependent fp64 chains (and their list loads)
+// run at full occupancy instead of stalling the shared-memory-limited
+// hashing warps; entries are read 16 bytes at a time, one chunk ahead.
+__global__ void __launch_bounds__(256) chain_slots_kernel(const FeatConfig c, const FeatArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const int32_t m = a.slot_nnz[i];
+  if (m < 0) return;  // chained by the hashing kernel
+  const double inv = a.slot_inv[i];
+  const double* __restrict__ w = a.w64;
+  // chunk q of this prompt at (q * n + i): a warp's loads are contiguous
+  const uint4* L = reinterpret_cast<const uint4*>(a.slots) + i;
+  const size_t stride = (size_t)a.n;
+  double s = 0.0;
+  const int nq = (m + 3) >> 2;
+  uint4 c0 = nq > 0 ? __ldcs(L) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 c1 = nq > 1 ? __ldcs(L + stride) : c0;
+  for (int q = 0; q < nq; ++q) {
+    const uint4 c2 = q + 2 < nq ? __ldcs(L + (size_t)(q + 2) * stride) : c1;
+    const uint32_t ev[4] = {c0.x, c0.y, c0.z, c0.w};
+    const int lim = m - 4 * q;  // entries of this chunk that exist
+    double p[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cn = (int)(ev[j] & 0xffffu) - 0x8000;
+      const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+      // (bytes past the last entry are never written: mask the index so a
+      // speculated load stays inside w; dim is a power of two here)
+      p[j] = (j < lim && cn != 0) ? __dmul_rn(__ldg(w + ((ev[j] >> 16) & c.mask)), v) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < lim) s = __dadd_rn(s, p[j]);
+    c0 = c1;
+    c1 = c2;
+  }
+  a.scores[i] = __dadd_rn(s, a.bias);
+}
+
 struct Plan {
   bool global_tables;
   int warps;
@@ -889,17 +1249,30 @@ int launch_one(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream
   return PARS_OK;
 }
 
+// The score modes run the v2 lane kernel (featurize_lane_kernel) unless
+// PARS_FEAT_V1=1 selects the round-1 kernel (kept for A/B measurements);
+// CSR mode runs featurize_seq_kernel.
+__host__ inline bool use_lane(int mode) {
+  static const bool v1 = [] {
+    const char* e = std::getenv("PARS_FEAT_V1");
+    return e && e[0] == '1';
+  }();
+  return mode != kFeatCsr && !v1;
+}
+
 template <int MODE>
 int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
-  const size_t per = seq_table_bytes(c.dim);
+  const bool lane = use_lane(MODE);
+  const size_t per = lane ? lane_warp_bytes(c.dim) : seq_table_bytes(c.dim);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto kern = featurize_seq_kernel<MODE>;
+  auto kern = lane ? featurize_lane_kernel<MODE> : featurize_seq_kernel<MODE>;
   int warps = 1, per_sm = 1, best = 0;
-  for (int w : {8, 4, 2, 1}) {
-    const size_t sm_bytes = per * w;
-    if (sm_bytes > kMaxSmemPerBlock) continue;
+  for (int w : {18, 16, 12, 9, 8, 6, 4, 2, 1}) {
+    if (!lane && w > 8) continue;
+    const size_t sm_bytes = lane ? lane_cta_bytes(c.dim, w) : per * w;
+    if (sm_bytes > kMaxLaneSmem) continue;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes) !=
         cudaSuccess)
       continue;
@@ -918,25 +1291,49 @@ int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
   }
   p->global_tables = false;
   p->warps = warps;
-  p->smem = per * warps;
+  p->smem = lane ? lane_cta_bytes(c.dim, warps) : per * warps;
   p->grid = std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(std::max<int64_t>(items, 1), warps), (int64_t)sms * per_sm));
   return PARS_OK;
 }
 
+// Exact-mode lane path scratch after the per-warp arenas: per-prompt slots of
+// kSlotCap packed entries, then the per-prompt (nnz, inv) of each slot.
+constexpr uint32_t kSlotCap = 512;
+__host__ inline size_t lane_slot_bytes(int64_t n) {
+  return (size_t)n * kSlotCap * 4 + (size_t)n * 8 + (size_t)n * 4 + 64;
+}
+
 template <int MODE>
-int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a, cudaStream_t st) {
+int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStream_t st) {
   Plan p;
-  PARS_TRY(plan_seq<MODE>(c, a.n, &p));
-  if (MODE == kFeatScoreExact && a.lists_bytes < (size_t)a.list_cap * 4 * (size_t)p.grid * p.warps) {
+  PARS_TRY(plan_seq<MODE>(c, a0.n, &p));
+  const size_t arenas = (size_t)a0.list_cap * 4 * (size_t)p.grid * p.warps;
+  const bool slots = MODE == kFeatScoreExact && use_lane(MODE);
+  if (MODE == kFeatScoreExact && a0.lists_bytes < arenas + (slots ? lane_slot_bytes(a0.n) : 0)) {
     set_error("featurize: list scratch too small");
     return PARS_ERR_INVALID;
   }
-  auto kern = featurize_seq_kernel<MODE>;
+  FeatArgs a = a0;
+  if (slots) {
+    unsigned char* b = reinterpret_cast<unsigned char*>(a0.lists) + ((arenas + 15) & ~(size_t)15);
+    a.slots = reinterpret_cast<uint32_t*>(b);
+    a.slot_cap = kSlotCap;
+    b += (size_t)a0.n * kSlotCap * 4;
+    a.slot_inv = reinterpret_cast<double*>(b);
+    b += (size_t)a0.n * 8;
+    a.slot_nnz = reinterpret_cast<int32_t*>(b);
+  }
+  auto kern = use_lane(MODE) ? featurize_lane_kernel<MODE> : featurize_seq_kernel<MODE>;
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a);
   count_launch(ctx);
   PARS_CUDA_CHECK(cudaGetLastError());
+  if (slots) {
+    chain_slots_kernel<<<(unsigned)ceil_div(a.n, 256), 256, 0, st>>>(c, a);
+    count_launch(ctx);
+    PARS_CUDA_CHECK(cudaGetLastError());
+  }
   return PARS_OK;
 }
 
@@ -967,7 +1364,8 @@ int scratch_pair(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
     Plan p;
     PARS_TRY(plan_seq<MODE>(c, n, &p));
     if (MODE == kFeatScoreExact)
-      *ls = std::max(*ls, (size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps);
+      *ls = std::max(*ls, (((size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps + 15) & ~(size_t)15) +
+                              (use_lane(MODE) ? lane_slot_bytes(n) : 0));
   }
   return PARS_OK;
 }

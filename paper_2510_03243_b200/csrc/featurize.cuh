@@ -52,6 +52,12 @@ struct FeatArgs {
   uint32_t* lists;
   size_t lists_bytes;
   uint32_t list_cap;
+  // exact mode, lane kernel: per-prompt entry slots for the chain kernel
+  // (carved out of the lists scratch by the launcher)
+  uint32_t* slots;
+  uint32_t slot_cap;
+  int32_t* slot_nnz;
+  double* slot_inv;
 };
 
 bool build_feat_config(const pars_extractor* ex, FeatConfig* cfg);
