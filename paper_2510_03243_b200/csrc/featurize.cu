@@ -836,10 +836,13 @@ constexpr int kLaneTextCap = 2560;   // prompt bytes staged in shared memory per
 constexpr int kLaneBuf = kLaneTextCap + 64;  // + 16-byte alignment slack and space padding
 
 __host__ __device__ inline size_t lane_warp_bytes(uint32_t dim) {
-  return (size_t)dim * 2 + dim / 8 + 128 /* dummy words */ + 32 /* increment table */ + kLaneBuf;
+  return (size_t)dim * 2 + dim / 8 + 32 /* increment table */ + kLaneBuf;
 }
-__host__ inline size_t lane_cta_bytes(uint32_t dim, int warps) {
-  return (size_t)dim * 2 /* alignment slack */ + (size_t)warps * lane_warp_bytes(dim);
+// + (fast mode) the fp32 weights in shared memory: the walk gathers w[idx]
+// for every entry, and an L2 round trip per gather would serialise it
+__host__ inline size_t lane_cta_bytes(uint32_t dim, int warps, int mode) {
+  return (size_t)dim * 2 /* alignment slack */ + (size_t)warps * lane_warp_bytes(dim) +
+         (mode == 1 ? (size_t)dim * 4 : 0);
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -902,8 +905,8 @@ __device__ __forceinline__ void lane_emit(uint32_t lut, uint32_t cbase, uint32_t
 template <int K>
 __device__ __forceinline__ void lane_bytes(uint32_t p, uint32_t ns, uint32_t ev, uint32_t sw,
                                            uint32_t sc, uint32_t& hw, uint32_t& A, uint32_t& B,
-                                           uint32_t cbase, uint32_t bbase, uint32_t dummy,
-                                           uint32_t m1, uint32_t m2, uint32_t lut) {
+                                           uint32_t cbase, uint32_t bbase, uint32_t m1, uint32_t m2,
+                                           uint32_t lut) {
   const uint32_t b = __byte_perm(p, 0u, 0x4440u + (K & 3));
   const bool sp = ((ns >> K) & 1u) == 0u;
   const uint32_t An = (sc ^ b) * 0x1b3u;
@@ -921,7 +924,7 @@ __device__ __forceinline__ void lane_bytes(uint32_t p, uint32_t ns, uint32_t ev,
 template <bool SMEM>
 __device__ __forceinline__ void hash_lane(const FeatConfig& c, uint32_t src, const uint8_t* a0,
                                           int lo, int hi, int rlo, int rhi, int lane, uint32_t cbase,
-                                          uint32_t bbase, uint32_t dummy, uint32_t lut) {
+                                          uint32_t bbase, uint32_t lut) {
   const int wpl = (((hi + 3) >> 2) + 31) >> 5;  // words per lane
   const int cs = lane * wpl * 4, ce = cs + wpl * 4;
   if (cs >= hi) return;
@@ -946,14 +949,14 @@ __device__ __forceinline__ void hash_lane(const FeatConfig& c, uint32_t src, con
     carry = own >> 8;
     const uint32_t ev = ((ns & E) | ~ns) & (E >> 1) & own & 0xffu;  // trigram or word end
     const uint32_t p0 = spaces_to_sep(w0, h0), p1 = spaces_to_sep(w1, h1);
-    lane_bytes<0>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<1>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<2>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<3>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<4>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<5>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<6>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
-    lane_bytes<7>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, dummy, m1, m2, lut);
+    lane_bytes<0>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<1>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<2>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<3>(p0, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<4>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<5>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<6>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
+    lane_bytes<7>(p1, ns, ev, sw, sc, hw, A, B, cbase, bbase, m1, m2, lut);
     prev2 = ns >> 6;
     if (!carry && (r + 8 >= ce || r + 8 >= hi)) break;
     w0 = n0;
@@ -999,22 +1002,40 @@ __device__ __forceinline__ void lane_stage_finish(uint32_t buf, int lo, int hi, 
   __syncwarp();
 }
 
+// Exact mode: a prompt whose (idx, count) list fits kSlotCap entries writes
+// it to its own slot (plus its entry count and L2 factor) for
+// chain_slots_kernel; a longer list is chained by the hashing warp itself.
+constexpr uint32_t kSlotCap = 512;
+
+__host__ inline size_t lane_slot_bytes(int64_t n) {
+  return (size_t)n * kSlotCap * 4 + (size_t)n * 8 + (size_t)n * 4 + 256;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+  constexpr bool kChain = MODE == kFeatScoreExact;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwc = blockDim.x >> 5;  // hashing warps per CTA
   const int64_t gw = (int64_t)blockIdx.x * nwc + warp;
   const int64_t nw = (int64_t)gridDim.x * nwc;
   // tables aligned to their size, so a counter address is base | offset
   const uint32_t tsz = c.dim * 2;
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t tb = (s0 + tsz - 1) & ~(tsz - 1);
+  // fast mode: the fp32 weights in shared memory after the warps' regions
+  // (the walk gathers w[idx] per entry; an L2 round trip each would
+  // serialise it)
+  float* sw32 = reinterpret_cast<float*>(smem + (tb - s0) + (size_t)nwc * lane_warp_bytes(c.dim));
+  if (!kChain) {
+    for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw32[k] = a.w32[k];
+    __syncthreads();
+  }
   const uint32_t cbase = tb + (uint32_t)warp * tsz;
   const uint32_t bbase = tb + (uint32_t)nwc * tsz + (uint32_t)warp * (c.dim / 8);
-  const uint32_t dummy = tb + (uint32_t)nwc * (tsz + c.dim / 8) + (uint32_t)warp * 128u + 4u * lane;
   // increments by (ev bit, half, sign): 0 x4, then -1, +1, -1 << 16, +1 << 16
-  const uint32_t lut = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 128u) + (uint32_t)warp * 32u;
-  const uint32_t buf = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 160u) + (uint32_t)warp * kLaneBuf;
+  const uint32_t lut = tb + (uint32_t)nwc * (tsz + c.dim / 8) + (uint32_t)warp * 32u;
+  const uint32_t buf = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 32u) + (uint32_t)warp * kLaneBuf;
   if (lane < 8) {
     const uint32_t dv =
         lane < 4 ? 0u : ((lane & 1) ? 1u : 0xffffffffu) << ((lane & 2) ? 16 : 0);
@@ -1031,25 +1052,25 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 
-  uint32_t* lists = (MODE == kFeatScoreExact) ? a.lists + (size_t)gw * a.list_cap : nullptr;
+  uint32_t* lists = kChain ? a.lists + (size_t)gw * a.list_cap : nullptr;
   const uint8_t* text_lo = a.text + a.offsets[0];
   const uint8_t* text_hi = a.text + a.offsets[a.n];
   auto fits = [&](int64_t beg, int64_t len) {
     return (int64_t)(reinterpret_cast<uintptr_t>(a.text + beg) & 15u) + len + 32 <= kLaneBuf;
   };
   int st_lo = -1;  // buffer offset of the staged prompt (-1: nothing staged)
-  if (gw < a.n) {
-    const int64_t beg = a.offsets[gw], len = a.offsets[gw + 1] - beg;
+  if (a.first + gw < a.n) {
+    const int64_t beg = a.offsets[a.first + gw], len = a.offsets[a.first + gw + 1] - beg;
     if (fits(beg, len)) st_lo = lane_stage(buf, a.text, beg, beg + len, text_lo, text_hi, lane, pol);
   }
-  for (int64_t i = gw; i < a.n; i += nw) {
+  for (int64_t i = a.first + gw; i < a.n; i += nw) {
     const int64_t beg = a.offsets[i], len = a.offsets[i + 1] - beg;
     if (((len + 1) / 2) + len > kNarrowMaxFeatures) {  // 16-bit counters could wrap
       if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
       st_lo = -1;
     } else if (st_lo >= 0) {
       lane_stage_finish(buf, st_lo, st_lo + (int)len, lane);
-      hash_lane<true>(c, buf, nullptr, st_lo, st_lo + (int)len, 0, 0, lane, cbase, bbase, dummy, lut);
+      hash_lane<true>(c, buf, nullptr, st_lo, st_lo + (int)len, 0, 0, lane, cbase, bbase, lut);
     } else if (len > 0) {
       const uint8_t* base = a.text + beg;
       const int mis = (int)(reinterpret_cast<uintptr_t>(base) & 3u);
@@ -1058,7 +1079,7 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
       const int64_t dlo = text_lo - a0, dhi = text_hi - a0;
       const int rlo = dlo > 0 ? (int)dlo : 0;
       const int rhi = dhi < (int64_t)hi + 8 ? (int)dhi : hi + 8;
-      hash_lane<false>(c, 0, a0, lo, hi, rlo, rhi, lane, cbase, bbase, dummy, lut);
+      hash_lane<false>(c, 0, a0, lo, hi, rlo, rhi, lane, cbase, bbase, lut);
     }
     __syncwarp();
     // the next prompt streams into the (now free) buffer while this one is
@@ -1069,21 +1090,18 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
       if (fits(nb2, nl)) st_lo = lane_stage(buf, a.text, nb2, nb2 + nl, text_lo, text_hi, lane, pol);
     }
     if (((len + 1) / 2) + len > kNarrowMaxFeatures) continue;
-    // pass 1: this lane's entry count
+    // pass 1: this lane's entries (bitmap popcount)
     uint32_t mine = 0;
     for (uint32_t j = 0; j < nb; ++j) mine += __popc(bm[j]);
     int tot;
     const uint32_t off = (uint32_t)warp_excl_scan((int)mine, lane, &tot);
-    // exact mode: the prompt's ascending (idx, count) list goes to its own
-    // slot for the chain kernel (chain_slots_kernel); a prompt with more
-    // entries than a slot holds is chained here from the warp's arena
-    const bool in_slot = (uint32_t)tot <= a.slot_cap;
-    uint32_t* L = nullptr;
-    if (MODE == kFeatScoreExact) L = lists;
+    long long sq = 0;
+    // exact: the prompt's own slot, or (long lists) the warp's arena
+    const bool in_slot = kChain && (uint32_t)tot <= kSlotCap;
+    uint32_t* L = in_slot ? a.slots + (size_t)(i - a.first) * kSlotCap : lists;
     // pass 2: ascending entries (lane-major = bucket order); resets the table
     uint32_t pos = off;
     float facc = 0.f;
-    long long sq = 0;
     for (uint32_t j = 0; j < nb; ++j) {
       const uint32_t m = bm[j];
       if (!m) continue;
@@ -1094,25 +1112,18 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
         const int cnt = (int)c16[idx] - 0x8000;
         c16[idx] = 0x8000;
         sq += (long long)cnt * cnt;
-        if (MODE == kFeatScoreExact) {
-          const uint32_t ent = (idx << 16) | (uint32_t)(cnt + 0x8000);
-          // slot layout: 4-entry chunk q of prompt i at (q * n + i), so
-          // the chain kernel's threads (one per prompt) read coalesced
-          if (in_slot)
-            a.slots[((size_t)(pos >> 2) * (size_t)a.n + (size_t)i) * 4 + (pos & 3)] = ent;
-          else
-            L[pos] = ent;
-          ++pos;
+        if (kChain) {
+          L[pos++] = (idx << 16) | (uint32_t)(cnt + 0x8000);
         } else {
-          facc += __ldg(a.w32 + idx) * (float)cnt;
+          facc += sw32[idx] * (float)cnt;
         }
       }
     }
     const double inv = inv_norm(c, warp_sum_i64(sq));
-    if (MODE == kFeatScoreExact) {
+    if (kChain) {
       if (lane == 0) {
-        a.slot_nnz[i] = in_slot ? tot : -1;
-        a.slot_inv[i] = inv;
+        a.slot_nnz[i - a.first] = in_slot ? tot : -1;
+        a.slot_inv[i - a.first] = inv;
       }
       if (!in_slot) {
         __syncwarp();
@@ -1127,45 +1138,67 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// Exact mode, second pass: one thread per prompt runs the reference's
-// sequential dot (features.hpp:31-35: s += w[idx] * v in ascending index
-// order, v = count * inv as in features.cpp:113-120; then + bias,
-// scorer.cpp:40-42) over the slot the lane kernel wrote. Separate from the
-// hashing kernel so that the dependent fp64 chains (and their list loads)
-// run at full occupancy instead of stalling the shared-memory-limited
-// hashing warps; entries are read 16 bytes at a time, one chunk ahead.
-__global__ void __launch_bounds__(256) chain_slots_kernel(const FeatConfig c, const FeatArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const int32_t m = a.slot_nnz[i];
+// Exact mode, second pass (features.hpp:31-35, scorer.cpp:40-42): thread k
+// runs the sequential fp64 dot of the prompt in slot k — s = +0.0, then
+// s += w[idx] * (count * inv) in ascending index order, then + bias — with
+// 16-byte entry loads issued four ahead and the weights in shared memory.
+// It runs right after the hashing kernel on the same chunk of prompts, so
+// the slots it reads were written moments ago and are still in L2.
+// Products of one 4-entry chunk (entries past the list's end give +0.0,
+// which leaves a sum that started at +0.0 unchanged under round-to-nearest).
+__device__ __forceinline__ void chain_products(const FeatConfig& c, const double* sw, uint4 q4,
+                                               int lim, double inv, double p[4]) {
+  const uint32_t ev[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int cn = (int)(ev[t] & 0xffffu) - 0x8000;
+    const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+    const double pr = __dmul_rn(sw[(ev[t] >> 16) & c.mask], v);
+    p[t] = (t < lim && cn != 0) ? pr : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) chain_slots_thread_kernel(const FeatConfig c, const FeatArgs a) {
+  extern __shared__ __align__(16) unsigned char csm[];
+  double* sw = reinterpret_cast<double*>(csm);
+  for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw[k] = a.w64[k];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // slot
+  if (a.first + k >= a.n) return;
+  const int64_t i = a.first + k;
+  const int32_t m = a.slot_nnz[k];
   if (m < 0) return;  // chained by the hashing kernel
-  const double inv = a.slot_inv[i];
-  const double* __restrict__ w = a.w64;
-  // chunk q of this prompt at (q * n + i): a warp's loads are contiguous
-  const uint4* L = reinterpret_cast<const uint4*>(a.slots) + i;
-  const size_t stride = (size_t)a.n;
-  double s = 0.0;
+  const double inv = a.slot_inv[k];
+  const uint4* L = reinterpret_cast<const uint4*>(a.slots + (size_t)k * kSlotCap);
   const int nq = (m + 3) >> 2;
-  uint4 c0 = nq > 0 ? __ldcs(L) : make_uint4(0u, 0u, 0u, 0u);
-  uint4 c1 = nq > 1 ? __ldcs(L + stride) : c0;
-  for (int q = 0; q < nq; ++q) {
-    const uint4 c2 = q + 2 < nq ? __ldcs(L + (size_t)(q + 2) * stride) : c1;
-    const uint32_t ev[4] = {c0.x, c0.y, c0.z, c0.w};
-    const int lim = m - 4 * q;  // entries of this chunk that exist
-    double p[4];
+  // software pipeline: chunk q's four adds (the only dependent chain) run
+  // while chunk q+1's products are formed; entry loads run kAhead chunks
+  // ahead (DRAM latency x bandwidth needs many bytes in flight per thread)
+  constexpr int kAhead = 8;
+  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+  uint4 r[kAhead];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int cn = (int)(ev[j] & 0xffffu) - 0x8000;
-      const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
-      // (bytes past the last entry are never written: mask the index so a
-      // speculated load stays inside w; dim is a power of two here)
-      p[j] = (j < lim && cn != 0) ? __dmul_rn(__ldg(w + ((ev[j] >> 16) & c.mask)), v) : 0.0;
+  for (int j = 0; j < kAhead; ++j) r[j] = j < nq ? __ldcs(L + j) : z4;
+  double pa[4];
+  chain_products(c, sw, r[0], m, inv, pa);
+  double s = 0.0;
+  for (int q0 = 0; q0 < nq; q0 += kAhead) {
+#pragma unroll
+    for (int j = 0; j < kAhead; ++j) {
+      const int q = q0 + j;
+      if (q < nq) {
+        // chunk q's slot r[j] is done: refill it with chunk q + kAhead
+        r[j] = q + kAhead < nq ? __ldcs(L + q + kAhead) : z4;
+        double pb[4];
+        chain_products(c, sw, r[(j + 1) % kAhead], m - 4 * (q + 1), inv, pb);
+        s = __dadd_rn(s, pa[0]);
+        s = __dadd_rn(s, pa[1]);
+        s = __dadd_rn(s, pa[2]);
+        s = __dadd_rn(s, pa[3]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) pa[t] = pb[t];
+      }
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < lim) s = __dadd_rn(s, p[j]);
-    c0 = c1;
-    c1 = c2;
   }
   a.scores[i] = __dadd_rn(s, a.bias);
 }
@@ -1271,13 +1304,14 @@ int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
   int warps = 1, per_sm = 1, best = 0;
   for (int w : {18, 16, 12, 9, 8, 6, 4, 2, 1}) {
     if (!lane && w > 8) continue;
-    const size_t sm_bytes = lane ? lane_cta_bytes(c.dim, w) : per * w;
+    const size_t sm_bytes = lane ? lane_cta_bytes(c.dim, w, MODE) : per * w;
     if (sm_bytes > kMaxLaneSmem) continue;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes) !=
         cudaSuccess)
       continue;
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32, sm_bytes);
+    const int threads = w * 32;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, sm_bytes);
     if (b * w > best) {
       best = b * w;
       warps = w;
@@ -1291,47 +1325,67 @@ int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
   }
   p->global_tables = false;
   p->warps = warps;
-  p->smem = lane ? lane_cta_bytes(c.dim, warps) : per * warps;
+  p->smem = lane ? lane_cta_bytes(c.dim, warps, MODE) : per * warps;
   p->grid = std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(std::max<int64_t>(items, 1), warps), (int64_t)sms * per_sm));
   return PARS_OK;
 }
 
-// Exact-mode lane path scratch after the per-warp arenas: per-prompt slots of
-// kSlotCap packed entries, then the per-prompt (nnz, inv) of each slot.
-constexpr uint32_t kSlotCap = 512;
-__host__ inline size_t lane_slot_bytes(int64_t n) {
-  return (size_t)n * kSlotCap * 4 + (size_t)n * 8 + (size_t)n * 4 + 64;
+// Exact mode on the lane path runs in chunks of chain_chunk() prompts
+// (default 2^20; PARS_CHAIN_CHUNK overrides): the hashing kernel writes each
+// prompt's (idx, count) list to its slot, then chain_slots_thread_kernel
+// scores the chunk. Measured on C4 (1M prompts): chunks small enough for the
+// lists to stay L2-resident (65,536) lose more to the chain kernel's low
+// occupancy than they gain from L2 (5.92 vs 5.38 ms), so the default chunk
+// is large and bounds the scratch (2 KB per prompt).
+// Scratch after the per-warp arenas: chain_chunk() slots of kSlotCap packed
+// entries, then each slot's L2 factor and entry count.
+static int64_t chain_chunk() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PARS_CHAIN_CHUNK");
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : (int64_t)1 << 20;
+  }();
+  return v;
 }
 
 template <int MODE>
 int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStream_t st) {
   Plan p;
   PARS_TRY(plan_seq<MODE>(c, a0.n, &p));
-  const size_t arenas = (size_t)a0.list_cap * 4 * (size_t)p.grid * p.warps;
+  const size_t arenas = (((size_t)a0.list_cap * 4 * (size_t)p.grid * p.warps) + 255) & ~(size_t)255;
   const bool slots = MODE == kFeatScoreExact && use_lane(MODE);
-  if (MODE == kFeatScoreExact && a0.lists_bytes < arenas + (slots ? lane_slot_bytes(a0.n) : 0)) {
+  const int64_t chunk = std::min<int64_t>(a0.n, chain_chunk());
+  if (MODE == kFeatScoreExact && a0.lists_bytes < arenas + (slots ? lane_slot_bytes(chunk) : 0)) {
     set_error("featurize: list scratch too small");
     return PARS_ERR_INVALID;
   }
-  FeatArgs a = a0;
-  if (slots) {
-    unsigned char* b = reinterpret_cast<unsigned char*>(a0.lists) + ((arenas + 15) & ~(size_t)15);
-    a.slots = reinterpret_cast<uint32_t*>(b);
-    a.slot_cap = kSlotCap;
-    b += (size_t)a0.n * kSlotCap * 4;
-    a.slot_inv = reinterpret_cast<double*>(b);
-    b += (size_t)a0.n * 8;
-    a.slot_nnz = reinterpret_cast<int32_t*>(b);
-  }
   auto kern = use_lane(MODE) ? featurize_lane_kernel<MODE> : featurize_seq_kernel<MODE>;
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a);
-  count_launch(ctx);
-  PARS_CUDA_CHECK(cudaGetLastError());
-  if (slots) {
-    chain_slots_kernel<<<(unsigned)ceil_div(a.n, 256), 256, 0, st>>>(c, a);
+  if (!slots) {
+    kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a0);
     count_launch(ctx);
+    PARS_CUDA_CHECK(cudaGetLastError());
+    return PARS_OK;
+  }
+  FeatArgs a = a0;
+  unsigned char* b = reinterpret_cast<unsigned char*>(a0.lists) + arenas;
+  a.slots = reinterpret_cast<uint32_t*>(b);
+  b += (size_t)chunk * kSlotCap * 4;
+  a.slot_inv = reinterpret_cast<double*>(b);
+  b += (size_t)chunk * 8;
+  a.slot_nnz = reinterpret_cast<int32_t*>(b);
+  const size_t csm = (size_t)c.dim * 8;
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(chain_slots_thread_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+  Plan pc;
+  PARS_TRY(plan_seq<MODE>(c, chunk, &pc));  // (plan_seq leaves the attribute at its last probe)
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc.smem));
+  for (int64_t f = 0; f < a0.n; f += chunk) {
+    a.first = f;
+    a.n = std::min<int64_t>(a0.n, f + chunk);
+    kern<<<(unsigned)pc.grid, pc.warps * 32, pc.smem, st>>>(c, a);
+    chain_slots_thread_kernel<<<(unsigned)ceil_div(a.n - f, 256), 256, csm, st>>>(c, a);
+    count_launch(ctx, 2);
     PARS_CUDA_CHECK(cudaGetLastError());
   }
   return PARS_OK;
@@ -1364,8 +1418,8 @@ int scratch_pair(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
     Plan p;
     PARS_TRY(plan_seq<MODE>(c, n, &p));
     if (MODE == kFeatScoreExact)
-      *ls = std::max(*ls, (((size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps + 15) & ~(size_t)15) +
-                              (use_lane(MODE) ? lane_slot_bytes(n) : 0));
+      *ls = std::max(*ls, (((size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps + 255) & ~(size_t)255) +
+                              (use_lane(MODE) ? lane_slot_bytes(std::min<int64_t>(n, chain_chunk())) : 0));
   }
   return PARS_OK;
 }

@@ -52,12 +52,14 @@ struct FeatArgs {
   uint32_t* lists;
   size_t lists_bytes;
   uint32_t list_cap;
-  // exact mode, lane kernel: per-prompt entry slots for the chain kernel
+  // exact mode, lane kernel: per-prompt entry slots for chain_slots_kernel
   // (carved out of the lists scratch by the launcher)
   uint32_t* slots;
-  uint32_t slot_cap;
   int32_t* slot_nnz;
   double* slot_inv;
+  // lane kernel + chain kernel: this launch covers prompts [first, n) (slot
+  // k holds prompt first + k); every other kernel requires first == 0
+  int64_t first;
 };
 
 bool build_feat_config(const pars_extractor* ex, FeatConfig* cfg);
