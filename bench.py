@@ -298,54 +298,64 @@ def run_ours(args):
     d_scores = torch.empty(per, dtype=torch.float64, device=dev)
     d_tie = torch.arange(b, e, dtype=torch.int32, device=dev)  # burst: rank of (0, id) = index
     d_order = torch.zeros(per, dtype=torch.int32, device=dev)
-    if world > 1:
-        # the global SJF order of all N prompts: gather every
-        # shard's scores and shard order, then rank 0 merges the sorted runs
-        import torch.distributed as dist
-        g_scores = torch.empty(per * world, dtype=torch.float64, device=dev)
-        g_orders = torch.empty(per * world, dtype=torch.int32, device=dev)
-        g_tie = torch.arange(N_PROMPTS, dtype=torch.int32, device=dev)
-        g_order = torch.empty(N_PROMPTS, dtype=torch.int32, device=dev)
-        run_offs = np.array([min(N_PROMPTS, r * per) for r in range(world + 1)], np.int64)
-        nccl = os.environ.get("PARS_DIST_BACKEND", "nccl") == "nccl"
-
-        def gather_into(out, inp):
-            if nccl:
-                dist.all_gather_into_tensor(out, inp)
-            else:  # gloo test mode: through the host
-                parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
-                dist.all_gather(parts, inp.cpu())
-                out.copy_(torch.cat(parts))
     L = P.lib()
     # a dedicated (non-NULL) stream: a NULL handle would mean "the ctx's own
     # stream" to the C ABI and torch's events would not see the kernels
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
+    dp = make_dp(P, ctx, world, rank)
+    if world > 1:
+        # the global SJF order of all N prompts: every rank
+        # ends with all N scores and the global order
+        g_scores = torch.empty(N_PROMPTS, dtype=torch.float64, device=dev)
+        g_order = torch.empty(N_PROMPTS, dtype=torch.int32, device=dev)
+        g_tie = torch.arange(N_PROMPTS, dtype=torch.int32, device=dev)
+        if dp is None:  # gloo test mode: gather through torch, merge on rank 0
+            import torch.distributed as dist
+            g_pad = torch.empty(per * world, dtype=torch.float64, device=dev)
+            g_orders = torch.empty(per * world, dtype=torch.int32, device=dev)
+            run_offs = np.array([min(N_PROMPTS, r * per) for r in range(world + 1)], np.int64)
+
+            def gather_into(out, inp):
+                parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+                dist.all_gather(parts, inp.cpu())
+                out.copy_(torch.cat(parts))
+
+    def check(rc):
+        if rc != 0:
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+
+    def score_shard():
+        check(L.pars_dev_score_text(ctx.h, __import__("ctypes").byref(ex), d_text.data_ptr(),
+                                    d_offs.data_ptr(), n, d_w.data_ptr(), 0.0, P.MODE_EXACT,
+                                    d_scores.data_ptr(), sh))
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        rc = L.pars_dev_score_text(ctx.h, __import__("ctypes").byref(ex), d_text.data_ptr(),
-                                   d_offs.data_ptr(), n, d_w.data_ptr(), 0.0, P.MODE_EXACT,
-                                   d_scores.data_ptr(), sh)
-        if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+        if world > 1 and dp is not None:
+            # pars_dp_score_order: shard score + shard order, all-gather, each
+            # rank places its own run, one uint32 all-reduce
+            dp.score_order(ex, d_text.data_ptr(), d_offs.data_ptr(), N_PROMPTS, d_w.data_ptr(), 0.0,
+                           P.MODE_EXACT, g_scores.data_ptr(), g_order.data_ptr(),
+                           d_tie_all=g_tie.data_ptr(), stream=sh)
+            if ev is not None:
+                ev[1].record(stream)
+                ev[2].record(stream)
+            return
+        score_shard()
         if ev is not None:
             ev[1].record(stream)
-        rc = L.pars_dev_priority_order(ctx.h, d_scores.data_ptr(), None, d_tie.data_ptr(), n,
-                                       d_order.data_ptr(), sh)
-        if rc != 0:
-            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+        check(L.pars_dev_priority_order(ctx.h, d_scores.data_ptr(), None, d_tie.data_ptr(), n,
+                                        d_order.data_ptr(), sh))
         if world > 1:
-            gather_into(g_scores, d_scores)
+            gather_into(g_pad, d_scores)
             gather_into(g_orders, d_order)
             if rank == 0:
-                rc = L.pars_dev_merge_orders(ctx.h, g_scores.data_ptr(), None, g_tie.data_ptr(),
-                                             g_orders.data_ptr(), run_offs.ctypes.data, world,
-                                             g_order.data_ptr(), sh)
-                if rc != 0:
-                    raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+                check(L.pars_dev_merge_orders(ctx.h, g_pad.data_ptr(), None, g_tie.data_ptr(),
+                                              g_orders.data_ptr(), run_offs.ctypes.data, world,
+                                              g_order.data_ptr(), sh))
         if ev is not None:
             ev[2].record(stream)
 
@@ -360,9 +370,13 @@ def run_ours(args):
     from oracle.bind import Oracle
     o = Oracle()
     t_par = time.perf_counter()
-    got = d_scores[:n].cpu().numpy()
+    got = (g_scores[b:e] if world > 1 and dp is not None else d_scores[:n]).cpu().numpy()
     so = o.score_batch(OEx.make(), wl.text, wl.offsets[b:e + 1], w, 0.0, threads=host_threads())
     parity_ok = bool((got.view(np.uint64) == so.view(np.uint64)).all())
+    if world > 1 and dp is not None:  # this rank's shard order, for the shard check
+        check(L.pars_dev_priority_order(ctx.h, g_scores[b:].data_ptr(), None, d_tie.data_ptr(), n,
+                                        d_order.data_ptr(), sh))
+        torch.cuda.synchronize()
     got_order = d_order[:n].cpu().numpy().astype(np.int64)
     oorder = o.select_order(np.zeros(n), ["p%06d" % i for i in range(b, e)], so,
                             np.zeros(n, np.uint8), 0.0)
@@ -376,7 +390,8 @@ def run_ours(args):
     if world > 1 and rank == 0:
         # the merged global order equals one sort of all N gathered scores
         full = torch.empty(N_PROMPTS, dtype=torch.int32, device=dev)
-        L.pars_dev_priority_order(ctx.h, g_scores.data_ptr(), None, g_tie.data_ptr(), N_PROMPTS,
+        gs = g_scores if dp is not None else g_pad
+        L.pars_dev_priority_order(ctx.h, gs.data_ptr(), None, g_tie.data_ptr(), N_PROMPTS,
                                   full.data_ptr(), sh)
         torch.cuda.synchronize()
         global_order_ok = bool(torch.equal(full, g_order))
@@ -402,9 +417,20 @@ def run_ours(args):
     value = N_PROMPTS / (ms_step / 1e3) if world > 1 else n / (ms_step / 1e3)
     feat_ms = float(np.mean([a.elapsed_time(b_) for a, b_, _ in evs]))
     sort_ms = float(np.mean([b_.elapsed_time(c) for _, b_, c in evs]))
+    if world > 1 and dp is not None:  # the fused dp step has no split: time the kernels alone
+        feat_ms = timed_ms(torch, stream, 1, score_shard, args.steps)
+        sort_ms = timed_ms(torch, stream, 1, lambda: check(L.pars_dev_priority_order(
+            ctx.h, d_scores.data_ptr(), None, d_tie.data_ptr(), n, d_order.data_ptr(), sh)), args.steps)
 
     # roofline of the dominant kernel (fused featurize+score): algorithmic bytes
     alg_bytes = text_bytes + 8 * (n + 1) + 8 * n + 8 * DIM
+    # ... and its integer-issue roofline: int ops counted on the
+    # host from the text, sum over tokens of 4(l+1) + 12 max(0, l-2) + 8 per
+    # emitted feature (one word + max(0, l-2) char trigrams per token), over
+    # the measured integer issue peak (tools/micro/int_issue.cu)
+    ntok, sum_len, sum_tri, _ = wl.token_stats(b, e)
+    int_ops = 4 * (sum_len + ntok) + 12 * sum_tri + 8 * (ntok + sum_tri)
+    spec_issue, meas_issue = issue_peaks()
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (feat_ms / 1e3) / 1e9
     # traffic and pipe utilisation from the committed ncu capture of this
@@ -442,6 +468,12 @@ def run_ours(args):
     e2e_s = float(np.median(e2e_vals)) if e2e_vals else float("nan")
     e2e_vals_ok = bool(e2e_vals)
     e2e_value = (N_PROMPTS if world > 1 else n) / e2e_s
+    # the same step through the reference's public C++ API (Scorer::score_batch
+    # over pageable std::string records + select_batch), linked with the
+    # drop-in: a program written against proj/include only (tools/c4api_main.cpp)
+    api_e2e = None
+    if world == 1 and not args.no_e2e and n == N_PROMPTS:
+        api_e2e = bench_reference_api(w, got, got_order)
     h2d = text_bytes + 8 * (n + 1) + 8 * DIM + 4 * n  # text, offsets, weights, tie ranks
     d2h = 8 * n + 4 * n  # scores, order
 
@@ -451,10 +483,10 @@ def run_ours(args):
         configs = bench_configs(P, ctx, args)
     pairs = None
     if not args.no_pairs:
-        pairs = bench_pairs(P, ctx, torch, dev, stream, world, rank, args)
+        pairs = bench_pairs(P, ctx, torch, dev, stream, world, rank, args, dp)
     tau = None
     if not args.no_pairs:
-        tau = bench_tau(P, ctx, torch, dev, stream, world, rank, args)
+        tau = bench_tau(P, ctx, torch, dev, stream, world, rank, args, dp)
     embed = None
     if world == 1 and not args.no_configs:
         embed = bench_embeddings(P, ctx, torch, dev, stream, args)
@@ -490,10 +522,25 @@ def run_ours(args):
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_kind": peak_kind, "traffic": traffic, "issue_bound_evidence": issue,
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": feat_ms,
-                         "sort_ms": sort_ms},
+                         "sort_ms": sort_ms,
+                         "issue": {"bound": "int issue", "int_ops_per_launch": int_ops,
+                                   "ops_model": "sum over tokens of 4(l+1) + 12 max(0,l-2) + 8 per "
+                                                "emitted feature (SURVEY 8(d)), counted on the host "
+                                                "from the text: %d tokens, %d token bytes, %d "
+                                                "trigrams" % (ntok, sum_len, sum_tri),
+                                   "achieved": int_ops / (feat_ms / 1e3) / 1e12,
+                                   "peak": (meas_issue or spec_issue) / 1e12,
+                                   "unit": "T int-ops/s",
+                                   "frac": int_ops / (feat_ms / 1e3) / (meas_issue or spec_issue),
+                                   "peak_kind": "measured: tools/micro/int_issue.cu fnv_step "
+                                                "(LOP3+IMAD) mix, profiles/r2_int_issue.json"
+                                                if meas_issue else "spec issue rate",
+                                   "spec_peak": spec_issue / 1e12}},
+            "sort": sort_roofline(n, sort_ms, hbm),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "prompts/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
+            "e2e_reference_api": api_e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
             "parity": {"c4_scores_all": parity_ok, "c4_order_all": order_ok, "prompts_checked": n,
@@ -513,59 +560,155 @@ def run_ours(args):
                               "unit": "pairs/s", "n_gpus": world,
                               "ms_per_step": pairs["ms_per_step"], "config": "C5"}))
         print(json.dumps(line))
+    if dp is not None:
+        dp.close()
     ctx.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
 
-def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
-    """C5: one full-batch data-parallel training step over 65,536 prompts:
-    score this rank's prompt shard (exact CSR dot), all-gather the scores,
-    this rank's slice of the all-pairs tiles (Eq. 1 mask + hinge + integer
-    coefficients), all-reduce the coefficients, X^T c on the row shard,
-    all-reduce the gradient, w -= (lr / kept) * grad. Metric: kept pairs per
+def make_dp(P, ctx, world, rank):
+    """The C ABI's NCCL data-parallel layer (pars_dp_*): one communicator per
+    rank, its unique id broadcast from rank 0. None in the gloo test mode
+    (several ranks on one GPU, which NCCL refuses)."""
+    if os.environ.get("PARS_DIST_BACKEND", "nccl") != "nccl":
+        return None
+    uid = P.nccl_unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    return P.DataParallel(ctx, uid, world, rank)
+
+
+def timed_ms(torch, stream, world, fn, k):
+    """Mean device time of fn() over k calls on `stream` (CUDA events),
+    max over ranks."""
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(k):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return barrier_max(world, a.elapsed_time(b)) / k
+
+
+def sort_roofline(n, sort_ms, hbm):
+    """The priority sort's HBM roofline: LSD radix traffic of the passes it
+    runs (8 B key + 4 B tie rank + 4 B index read and written per key per
+    pass; C4's burst tie ranks are already in input order, so only the score's
+    varying digit positions run) and, beside it, the one-pass I/O floor (read
+    score + tie rank, write the order)."""
+    floor = n * (8 + 4 + 4)
+    return {"kernel": "radix sort (pars_dev_priority_order)", "ms": sort_ms, "bound": "hbm",
+            "floor_bytes": floor, "bytes_model": "one-pass I/O floor: 8 B score + 4 B tie rank "
+            "read, 4 B order written per key",
+            "achieved": floor / (sort_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": floor / (sort_ms / 1e3) / 1e9 / hbm}
+
+
+def issue_peaks():
+    """Lane-op issue peaks: the spec rate (one warp-instruction per cycle per
+    SM sub-partition at the max SM clock) and the measured integer mix of the
+    featurize hash (tools/micro/int_issue.cu -> profiles/r2_int_issue.json)."""
+    mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    clk = float(mp.get("sm_max_mhz", 1965.0)) * 1e6
+    spec = 148 * 4 * 32 * clk
+    meas = None
+    p = ROOT / "profiles" / "r2_int_issue.json"
+    if p.exists():
+        try:
+            meas = float(json.loads(p.read_text())["kinds"]["fnv_step (LOP3+IMAD)"]["lane_ops_per_s"])
+        except Exception:
+            meas = None
+    return spec, meas
+
+
+def bench_pairs(P, ctx, torch, dev, stream, world, rank, args, dp=None):
+    """C5: one full-batch data-parallel training step over 65,536 prompts
+    through pars_dp_train_step: score this rank's prompt shard (exact CSR
+    dot), all-gather the scores, this rank's cost-balanced slice of the
+    all-pairs tiles (Eq. 1 mask + hinge + integer coefficients), all-reduce
+    the coefficients and counts, X^T c on the row shard, all-reduce the
+    gradient, w -= (lr / kept) * grad (a kernel). Metric: kept pairs per
     second of step time (max over ranks)."""
     wl = P.Workload.synthesize(C5_N, C5_SEED)
     ex = P.Extractor.make()
     feats = ctx.extract(ex, wl.text, wl.offsets)  # once, like train()'s extract_all
-    lens = wl.output_len.astype(np.int32)
-    max_len = int(lens.max())
-    d_L = torch.from_numpy(lens).to(dev)
+    n = C5_N
     w0 = np.random.default_rng(99).normal(size=DIM) * 0.05
     d_w = torch.from_numpy(w0).to(dev)
-    per = (C5_N + world - 1) // world
-    scores_pad = torch.zeros(per * world, dtype=torch.float64, device=dev)
-    from paper_2510_03243_b200 import distributed as D
     sh = stream.cuda_stream
     plan = ctx.pair_plan(wl.output_len, DELTA)  # per dataset: lengths are fixed
     kept = plan.kept
     lr = 0.1
-    res = {}
+    d_s = torch.empty(n, dtype=torch.float64, device=dev)
+    d_c = torch.zeros(n, dtype=torch.int32, device=dev)
+    d_cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    d_loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    if dp is not None:
+        def step():
+            dp.train_step(feats, plan, d_w.data_ptr(), MARGIN, lr, d_c.data_ptr(), d_s.data_ptr(),
+                          d_cnt.data_ptr(), d_loss.data_ptr(), stream=sh)
+    else:  # gloo test mode: the torch.distributed restatement (distributed.py)
+        from paper_2510_03243_b200 import distributed as D
+        lens = wl.output_len.astype(np.int32)
+        d_L = torch.from_numpy(lens).to(dev)
+        per = (n + world - 1) // world
+        scores_pad = torch.zeros(per * world, dtype=torch.float64, device=dev)
 
-    def step():
-        res["out"] = D.train_step_gpu(ctx, feats, d_w, scores_pad, d_L, C5_N, DELTA, MARGIN,
-                                      max_len, lr / kept, stream=sh, plan=plan)
+        def step():
+            cnt, part = D.train_step_gpu(ctx, feats, d_w, scores_pad, d_L, n, DELTA, MARGIN,
+                                         int(lens.max()), lr / kept, stream=sh, plan=plan)
+            d_cnt.copy_(cnt)
+            d_s.copy_(scores_pad[:n])
 
-    # parity of the first step (untimed, from w0): scores, coefficients and
-    # counts against the oracle
+    # parity of the first step (untimed, from w0) against the oracle: scores
+    # and integer coefficients bit-exact, counts exact, the loss and the
+    # updated weights within the stated tolerances (fp64 sums in another order)
+    from oracle.bind import Extractor as OEx
     from oracle.bind import Oracle
+    o = Oracle()
     step()
     torch.cuda.synchronize()
-    s0 = feats.score(w0)
-    oc, okept, oact, oloss = Oracle().allpairs(s0, wl.output_len, DELTA, MARGIN)
-    cnt0, part0 = res["out"]
-    first_ok = bool(int(cnt0[0]) == okept == 1920977782 and int(cnt0[1]) == oact)
+    so = o.score_batch(OEx.make(), wl.text, wl.offsets, w0, 0.0, threads=host_threads())
+    oc, okept, oact, oloss = o.allpairs(so, wl.output_len, DELTA, MARGIN, threads=host_threads())
+    par = {"c5_scores": bool((d_s.cpu().numpy().view(np.uint64) == so.view(np.uint64)).all()),
+           "c5_kept": int(d_cnt[0]) == okept == 1920977782, "c5_active": int(d_cnt[1]) == oact}
+    if dp is not None:
+        rp, idx, val = feats.download()
+        g = o.xt_c(rp, idx, val, oc, DIM)
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        mag = np.zeros(DIM)
+        np.add.at(mag, idx, np.abs(val * oc[rows]))
+        w1 = w0 - (lr / okept) * g
+        dw = np.abs(d_w.cpu().numpy() - w1)
+        scale = (lr / okept) * mag
+        grad_rel = float(np.max(np.where(scale > 0, dw / np.where(scale > 0, scale, 1), 0.0)))
+        loss_rel = abs(float(d_loss[0]) - oloss) / abs(oloss)
+        par.update({"c5_coeff": bool((d_c.cpu().numpy() == oc).all()),
+                    "c5_loss_rel": loss_rel, "c5_grad_rel": grad_rel,
+                    "tolerance": "loss <= 1e-12 relative; weights |w - w_oracle| <= 1e-12 * "
+                                 "(lr/kept) * sum_i |c_i x_i[d]| per component (X^T c summed "
+                                 "in another order)",
+                    "c5_ok": bool(loss_rel <= 1e-12 and grad_rel <= 1e-12)})
+        del rp, idx, val, rows
+    first_ok = all(v for k, v in par.items() if isinstance(v, bool))
     d_w.copy_(torch.from_numpy(w0).to(dev))
     for _ in range(3):
         step()
     torch.cuda.synchronize()
-    # the whole step (kernels, the torch update, NCCL collectives) as one CUDA
-    # graph replayed per step: the host launches nothing per kernel. Falls
-    # back to eager launches if capture is refused (e.g. a collective backend
-    # that cannot be captured).
+    # the whole step (kernels and NCCL collectives) as one CUDA graph replayed
+    # per step: the host launches nothing per kernel. Falls back to eager
+    # launches if capture is refused.
     graph = None
-    if world == 1 or os.environ.get("PARS_DIST_BACKEND", "nccl") == "nccl":
+    if dp is not None:
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
@@ -577,19 +720,8 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
             graph = None
             torch.cuda.synchronize()
     run = graph.replay if graph is not None else step
-    for _ in range(2):
-        run()
-    torch.cuda.synchronize()
-    barrier(world)
-    a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(3, args.steps)
-    a.record(stream)
-    for _ in range(k):
-        run()
-    bb.record(stream)
-    torch.cuda.synchronize()
-    ms = barrier_max(world, a.elapsed_time(bb)) / k
-    cnt, part = res["out"]
+    ms = timed_ms(torch, stream, world, run, k)
     graph_ok = None
     if graph is not None:
         # replaying the graph trains exactly like launching the steps
@@ -603,21 +735,56 @@ def bench_pairs(P, ctx, torch, dev, stream, world, rank, args):
             step()
         torch.cuda.synchronize()
         graph_ok = bool(torch.equal(w_graph.view(torch.int64), d_w.view(torch.int64)))
+    active = int(d_cnt[1])
+    # the dominant kernel alone, over every tile (prep + allpairs + scatter),
+    # and X^T c over every row, each timed with events on the launch stream
+    tiles = int(P.lib().pars_allpairs_tiles(n))
+    part = torch.zeros(tiles, dtype=torch.float64, device=dev)
+    ms_pairs = timed_ms(torch, stream, world, lambda: plan.run(
+        d_s.data_ptr(), MARGIN, 0, tiles, d_c.data_ptr(), d_cnt.data_ptr(), part.data_ptr(), sh), k)
+    d_g = torch.zeros(DIM, dtype=torch.float64, device=dev)
+    L = P.lib()
+    ms_xtc = timed_ms(torch, stream, world, lambda: L.pars_dev_xt_c(
+        ctx.h, __import__("ctypes").c_void_p(feats.h), d_c.data_ptr(), 0, n, d_g.data_ptr(), sh), k)
+    nnz = feats.nnz
+    spec, meas = issue_peaks()
+    all_pairs = n * (n - 1) // 2
+    ach = all_pairs * 11 / (ms_pairs / 1e3)
+    hbm, peak_kind = peaks()
+    xtc_bytes = nnz * 12 + (DIM + 1) * 8 + n * 4 + DIM * 8
     feats.free()
     return {"metric": "filtered pairs/s", "value": kept / (ms / 1e3), "unit": "pairs/s",
             "ms_per_step": ms, "kept": kept, "kept_expected": 1920977782,
-            "active_last_step": int(cnt[1]), "first_step_matches_oracle": first_ok,
+            "active_last_step": active, "first_step_matches_oracle": first_ok, "parity": par,
             "plan_sorted": plan.sorted, "cuda_graph": graph is not None,
             "cuda_graph_matches_eager": graph_ok,
+            "api": "pars_dp_train_step (NCCL world %d)" % world if dp is not None else
+                   "distributed.train_step_gpu (gloo test mode)",
             "workload": "C5: full-batch DP training step over all 2,147,450,880 unordered pairs "
                         "of 65,536 prompts (seed 25): CSR scoring of the rank's shard + score "
                         "all-gather, Eq.1 mask delta=0.2 + hinge + integer coefficients on the "
                         "rank's tiles + all-reduce, X^T c + gradient all-reduce, SGD update",
             "bound": "issue (int/fp64 ALU); inputs 0.5 MB are L2-resident",
-            "roofline": pairs_roofline(ms)}
+            "roofline": {"bound": "issue", "kernel": "allpairs_sorted_kernel (+ prep, scatter), "
+                         "all tiles on one GPU", "kernel_ms": ms_pairs,
+                         "achieved": ach / 1e12, "peak": spec / 1e12, "unit": "T lane-ops/s",
+                         "frac": ach / spec,
+                         "algorithmic": "11 lane-ops per unordered pair (SURVEY 8(d): sub, abs, "
+                                        "max, dmin lookup, compare, label, sign, add-margin, max, "
+                                        "2 accumulates) x all 2,147,450,880 pairs; the sorted "
+                                        "plan executes fewer (empty tiles skipped, one compare "
+                                        "per pair), so frac can exceed 1",
+                         "peak_kind": "spec: 148 SMs x 4 SMSPs x 32 lanes x max SM clock",
+                         "measured_int_mix_peak": meas / 1e12 if meas else None,
+                         "pairs_per_s_kernel": all_pairs / (ms_pairs / 1e3)},
+            "xtc": {"kernel": "xtc_csc_kernel + xtc_task_reduce (grad = X^T c, all 65,536 rows)",
+                    "ms": ms_xtc, "bound": "hbm", "algorithmic_bytes": xtc_bytes,
+                    "bytes_model": "nnz x (4 B row + 8 B value) + column pointers + c + grad",
+                    "achieved": xtc_bytes / (ms_xtc / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": xtc_bytes / (ms_xtc / 1e3) / 1e9 / hbm, "peak_kind": peak_kind}}
 
 
-def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
+def bench_tau(P, ctx, torch, dev, stream, world, rank, args, dp=None):
     """Kendall tau-b counts (metrics.cpp:42-64) at compare_policies scale: the
     PARS scores vs output lengths of 100,000 requests (C3-sized trace). The
     default path counts by sorting (tau_sorted.cu, O(n log n), exact; every
@@ -648,7 +815,10 @@ def bench_tau(P, ctx, torch, dev, stream, world, rank, args):
         return barrier_max(world, a.elapsed_time(b)) / k, r
 
     ms, (tau, c) = timed(lambda: ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), n, stream=sh))
-    ms_pairs, (tau_p, c_p) = timed(lambda: D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh))
+    if dp is not None:  # pars_dp_kendall_tau: tiles split over ranks, one u64 all-reduce
+        ms_pairs, (tau_p, c_p) = timed(lambda: dp.kendall_tau(dx.data_ptr(), dy.data_ptr(), n, stream=sh))
+    else:
+        ms_pairs, (tau_p, c_p) = timed(lambda: D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh))
     pairs = n * (n - 1) // 2
     out = {"metric": "pairs/s", "value": pairs / (ms / 1e3), "ms_per_call": ms, "tau_b": tau,
            "algorithm": "sorted counts (two radix sorts + merge inversion count), exact",
@@ -823,6 +993,34 @@ def bench_ingest(P, ctx, torch, dev, stream, wl, w, args):
                                   % (sample, host_threads())})
     P.lib().pars_host_free(hb)
     return out
+
+
+def bench_reference_api(w, scores, order):
+    """C4 end to end through the reference API: oracle/_ref/c4api_b200 (the
+    program tools/c4api_main.cpp — reference headers only — built against the
+    drop-in libpars_b200.so; the reference's own generator makes the records).
+    Its step is the reference arm's step; its outputs must equal ours."""
+    import tempfile
+    exe = ROOT / "oracle" / "_ref" / "c4api_b200"
+    if not exe.exists():
+        return {"unavailable": "oracle/_ref/c4api_b200 not built"}
+    with tempfile.TemporaryDirectory() as td:
+        wf = Path(td) / "w.bin"
+        np.ascontiguousarray(w, np.float64).tofile(wf)
+        pre = Path(td) / "out"
+        r = subprocess.run([str(exe), str(N_PROMPTS), str(wf), "3", str(pre)], capture_output=True,
+                           text=True, timeout=900)
+        if r.returncode != 0:
+            return {"error": (r.stderr or r.stdout)[-400:]}
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+        s2 = np.fromfile(str(pre) + ".scores", np.float64)
+        o2 = np.fromfile(str(pre) + ".order", np.int64)
+    j["scores_equal_c_abi"] = bool(len(s2) == len(scores) and
+                                   (s2.view(np.uint64) == scores.view(np.uint64)).all())
+    j["order_equal_c_abi"] = bool(len(o2) == len(order) and (o2 == order).all())
+    j["api"] = ("LinearScorer::score_batch(Dataset) + select_batch (proj/include/pars) "
+                "through libpars_b200.so; records are pageable std::string")
+    return j
 
 
 def fnv64(a: np.ndarray) -> str:

@@ -82,6 +82,15 @@ void pars_host_free(void* p);
 int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
                     const int64_t* offsets, int64_t n, const double* weights,
                     double bias, int mode, double* scores);
+/* Scorer::score_batch over records held as separate host strings (the
+ * reference's Dataset of std::string, scorer.cpp:9-24): texts[i] points at
+ * lens[i] bytes. Host threads gather ~64 MB chunks straight into pinned
+ * staging (no packing pass), overlapped with the uploads and the kernels.
+ * Bit-identical to pars_score_text over the concatenation. */
+int pars_score_records(pars_ctx* ctx, const pars_extractor* ex,
+                       const char* const* texts, const int64_t* lens, int64_t n,
+                       const double* weights, double bias, int mode,
+                       double* scores);
 int pars_dev_score_text(pars_ctx* ctx, const pars_extractor* ex,
                         const char* d_text, const int64_t* d_offsets,
                         int64_t n, const double* d_weights, double bias,
@@ -147,6 +156,7 @@ int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows,
                          const double* val, pars_features** out);
 int64_t pars_features_rows(const pars_features* f);
 int64_t pars_features_nnz(const pars_features* f);
+int64_t pars_features_dim(const pars_features* f);
 /* Copies the CSR back to the host: row_ptr[rows+1], idx[nnz], val[nnz]. */
 int pars_features_download(pars_ctx* ctx, const pars_features* f,
                            int64_t* row_ptr, uint32_t* idx, double* val);
@@ -311,12 +321,23 @@ int pars_dev_priority_order(pars_ctx* ctx, const double* d_scores,
  * pars_dev_priority_order result (indices relative to the shard start),
  * concatenated; d_scores / d_boosted / d_tie cover all n = run_offsets[nruns]
  * prompts. d_order[n] receives what pars_dev_priority_order over all n would
- * (bit-identical), by merging the runs. run_offsets is a host array. Returns
- * after the merge completes on `stream`. */
+ * (bit-identical), by merging the runs (one level: each element's place is
+ * its position in its run plus one binary search per other run; at most 64
+ * runs). run_offsets is a host array (read before the call returns); the
+ * merge is asynchronous on `stream`. */
 int pars_dev_merge_orders(pars_ctx* ctx, const double* d_scores,
                           const uint8_t* d_boosted, const uint32_t* d_tie,
                           const uint32_t* d_run_orders, const int64_t* run_offsets,
                           int nruns, uint32_t* d_order, void* stream);
+/* The same placement for the elements of ONE run only (run in [0, nruns)):
+ * d_order[p] is written for exactly the positions p that run's elements take
+ * in the merged order; other positions are untouched. Disjoint across runs,
+ * so data-parallel ranks each place their own shard and combine by a sum
+ * (pars_dp_score_order). */
+int pars_dev_merge_rank(pars_ctx* ctx, const double* d_scores,
+                        const uint8_t* d_boosted, const uint32_t* d_tie,
+                        const uint32_t* d_run_orders, const int64_t* run_offsets,
+                        int nruns, int run, uint32_t* d_order, void* stream);
 /* Host helper: dense ranks of (arrival, id) with equal keys sharing a rank.
  * ids: arena + offsets[n+1] (raw bytes, compared unsigned). */
 int pars_tie_ranks(const double* arrival, const char* ids,
@@ -354,6 +375,72 @@ int pars_dev_kendall_counts(pars_ctx* ctx, const double* d_x, const double* d_y,
 /* finish_tau (metrics.cpp:13-32): counts5 = {n_c, n_d, n0, n1, n2}. */
 int pars_kendall_finish(const uint64_t* counts4, int64_t n, uint64_t* counts5,
                         double* tau_b);
+
+
+/* ---- data-parallel ranks over NCCL ---------------------
+ * One process per GPU. A pars_dp binds a pars_ctx to an NCCL communicator
+ * (libnccl is bound at run time; an already-loaded copy, e.g. torch's, is
+ * reused; PARS_NCCL_LIB overrides the path). Prompt shards are contiguous:
+ * rank r owns [r*per, min(n, (r+1)*per)), per = ceil(n / world)
+ * (pars_dp_shard). All pars_dp_* calls are collective: every rank calls them
+ * in the same order. They are asynchronous on `stream` unless noted. */
+typedef struct pars_dp pars_dp;
+#define PARS_NCCL_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId on one rank; the caller broadcasts the 128 bytes. */
+int pars_nccl_get_unique_id(uint8_t* id);
+/* ncclCommInitRank(world, id, rank) on ctx's device (owned by the dp). */
+int pars_dp_create(pars_ctx* ctx, const uint8_t* id, int world, int rank,
+                   pars_dp** out);
+/* Wrap a caller-owned ncclComm_t (passed as void*; not destroyed). */
+int pars_dp_create_from_comm(pars_ctx* ctx, void* nccl_comm, pars_dp** out);
+int pars_dp_rank(const pars_dp* dp);
+int pars_dp_world(const pars_dp* dp);
+void pars_dp_destroy(pars_dp* dp);
+void pars_dp_shard(int64_t n, int world, int rank, int64_t* begin,
+                   int64_t* end);
+/* Sharded Scorer::score_batch (scorer.cpp:9-24) + select_batch
+ * (scheduler.cpp:33-60) of all n_total prompts: d_text/d_offsets hold THIS
+ * rank's shard (offsets[m+1], relative to d_text); d_boosted_all/d_tie_all
+ * (optional) cover all n_total prompts. Every rank receives all n_total
+ * scores and the global order (indices into all prompts), bit-identical to
+ * pars_dev_score_text + pars_dev_priority_order on one GPU: shard scores and
+ * shard orders are all-gathered, each rank places its own run
+ * (pars_dev_merge_rank) and the placements are summed (uint32 all-reduce). */
+int pars_dp_score_order(pars_dp* dp, const pars_extractor* ex,
+                        const char* d_text, const int64_t* d_offsets,
+                        int64_t n_total, const double* d_w, double bias,
+                        int mode, const uint8_t* d_boosted_all,
+                        const uint32_t* d_tie_all, double* d_scores_all,
+                        uint32_t* d_order_all, void* stream);
+/* One full-batch data-parallel step of all-pairs margin-ranking training
+ * over the plan's n prompts (pairs.hpp:21-31; train.cpp:34-44 in
+ * coefficient form; apply train.cpp:141-151 with batch_n = kept pairs):
+ * scores of this rank's rows (exact CSR dot), all-gathered; this rank's
+ * cost-balanced slice of the pair tiles (pars_pair_plan_tile_split);
+ * int32 coefficients and u64 {kept, active} all-reduced (exact for any rank
+ * count); grad = X^T c over the row shard, fp64 all-reduce;
+ * w -= (lr / kept) * grad where grad != 0. f holds all n rows on every rank.
+ * Outputs (device): d_scores_all[n] (optional), d_coeff[n],
+ * d_counters[2] (optional), d_loss (optional: the loss sum, per-tile partials
+ * summed in tile order — identical for every rank count). */
+int pars_dp_train_step(pars_dp* dp, const pars_features* f,
+                       const pars_pair_plan* plan, double* d_w, double margin,
+                       double lr, double* d_scores_all, int32_t* d_coeff,
+                       unsigned long long* d_counters, double* d_loss,
+                       void* stream);
+/* kendall_tau_b (metrics.cpp:42-64) with the pair tiles split evenly across
+ * ranks and one exact all-reduce of the integer counts; counts[5] and tau on
+ * the host of every rank (synchronises `stream`). */
+int pars_dp_kendall_tau(pars_dp* dp, const double* d_x, const double* d_y,
+                        int64_t n, uint64_t* counts, double* tau_b,
+                        void* stream);
+/* Host-only helpers (no device): a contiguous split of weighted items with
+ * equal weight per rank (bounds[world+1]); the tile weights of a pair plan
+ * (fully or partly kept tiles cost 64, empty ones 1) split that way. */
+int pars_split_weighted(const int64_t* weights, int64_t n, int world,
+                        int64_t* bounds);
+int pars_pair_plan_tile_split(const pars_pair_plan* plan, int world,
+                              int64_t* bounds);
 
 #ifdef __cplusplus
 }

@@ -9,11 +9,15 @@ from ._lib import (  # noqa: F401
     MODE_EXACT,
     MODE_FAST,
     Context,
+    DataParallel,
     Extractor,
     Features,
     ParsError,
     Workload,
     build_pairs,
+    dp_shard,
+    nccl_unique_id,
+    split_weighted,
     device_count,
     ids_arena,
     length_gap_table,
@@ -24,7 +28,8 @@ from ._lib import (  # noqa: F401
 )
 
 __all__ = [
-    "MODE_EXACT", "MODE_FAST", "Context", "Extractor", "Features", "ParsError", "Workload",
+    "MODE_EXACT", "MODE_FAST", "Context", "DataParallel", "dp_shard", "nccl_unique_id",
+    "split_weighted", "Extractor", "Features", "ParsError", "Workload",
     "build_pairs", "device_count", "ids_arena", "length_gap_table", "lib", "pack_texts",
     "pinned_empty", "tie_ranks",
 ]

@@ -136,6 +136,22 @@ def _load() -> C.CDLL:
         "pars_kendall_tau_algo": (C.c_int, [vp, vp, vp, i64, vp, vp, C.c_int]),
         "pars_dev_merge_orders": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
         "pars_dev_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+        "pars_features_dim": (i64, [vp]),
+        "pars_score_records": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp]),
+        "pars_dev_merge_rank": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp]),
+        "pars_nccl_get_unique_id": (C.c_int, [vp]),
+        "pars_dp_create": (C.c_int, [vp, vp, C.c_int, C.c_int, vp]),
+        "pars_dp_create_from_comm": (C.c_int, [vp, vp, vp]),
+        "pars_dp_rank": (C.c_int, [vp]),
+        "pars_dp_world": (C.c_int, [vp]),
+        "pars_dp_destroy": (None, [vp]),
+        "pars_dp_shard": (None, [i64, C.c_int, C.c_int, vp, vp]),
+        "pars_dp_score_order": (C.c_int, [vp, vp, vp, vp, i64, vp, dbl, C.c_int, vp, vp, vp, vp,
+                                          vp]),
+        "pars_dp_train_step": (C.c_int, [vp, vp, vp, vp, dbl, dbl, vp, vp, vp, vp, vp]),
+        "pars_dp_kendall_tau": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+        "pars_split_weighted": (C.c_int, [vp, i64, C.c_int, vp]),
+        "pars_pair_plan_tile_split": (C.c_int, [vp, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -255,7 +271,8 @@ def workload_lib():
                 ("pars_workload_count", i64, [vp]), ("pars_workload_text_bytes", i64, [vp]),
                 ("pars_workload_text", vp, [vp]), ("pars_workload_offsets", vp, [vp]),
                 ("pars_workload_output_len", vp, [vp]), ("pars_workload_prompt_len", vp, [vp]),
-                ("pars_workload_free", None, [vp]), ("pars_workload_last_error", C.c_char_p, [])):
+                ("pars_workload_free", None, [vp]), ("pars_workload_last_error", C.c_char_p, []),
+                ("pars_workload_token_stats", C.c_int, [vp, vp, i64, vp])):
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
         _WL = L
@@ -295,6 +312,17 @@ class Workload:
 
     def __len__(self):
         return len(self.output_len)
+
+    def token_stats(self, b: int = 0, e: Optional[int] = None):
+        """(tokens, sum of token lengths, sum of max(0, len - 2), text bytes)
+        of prompts [b, e) — the host-side count behind the featurize
+        kernel's integer-issue roofline."""
+        e = len(self) if e is None else e
+        out = np.zeros(4, np.uint64)
+        offs = np.ascontiguousarray(self.offsets[b:e + 1])
+        workload_lib().pars_workload_token_stats(self.text.ctypes.data, offs.ctypes.data, e - b,
+                                                 out.ctypes.data)
+        return tuple(int(x) for x in out)
 
     def prompt(self, i) -> bytes:
         return self.text[self.offsets[i]:self.offsets[i + 1]].tobytes()
@@ -436,6 +464,13 @@ class PairPlan:
             d_partials: int, stream: int = 0):
         _check(lib().pars_dev_allpairs_plan(self.ctx.h, C.c_void_p(self.h), d_scores, margin, t0,
                                             t1, d_coeff, d_counters, d_partials, stream or None))
+
+    def tile_split(self, world: int) -> np.ndarray:
+        """Cost-balanced contiguous split of the tile list over `world` ranks
+        (pars_pair_plan_tile_split): bounds[world + 1]."""
+        b = np.zeros(world + 1, np.int64)
+        _check(lib().pars_pair_plan_tile_split(C.c_void_p(self.h), world, _p(b)))
+        return b
 
     def free(self):
         if self.h:
@@ -660,6 +695,18 @@ class Context:
         _check(lib().pars_priority_order(self.h, _p(s), _p(bst), _p(t), len(s), _p(out)))
         return out
 
+    def score_records(self, ex: Extractor, texts, weights, bias: float = 0.0,
+                      mode: int = MODE_EXACT) -> np.ndarray:
+        """Scorer::score_batch over separate host strings (pars_score_records)."""
+        bufs = [t if isinstance(t, bytes) else bytes(t) for t in texts]
+        ptrs = (C.c_char_p * max(1, len(bufs)))(*bufs)
+        lens = np.array([len(t) for t in bufs], np.int64)
+        w = _c(weights, np.float64)
+        out = np.zeros(len(bufs), np.float64)
+        _check(lib().pars_score_records(self.h, C.byref(ex), ptrs, _p(lens), len(bufs), _p(w), bias,
+                                        mode, _p(out)))
+        return out
+
     def kendall_tau(self, x, y, algo: str = "auto"):
         """kendall_tau_b (metrics.cpp:42-64): (tau_b, counts[n_c,n_d,n0,n1,n2]).
         algo: "auto" (sorted unless an input is inf/NaN), "sorted" (O(n log n))
@@ -678,3 +725,88 @@ class Context:
         tau = C.c_double()
         _check(lib().pars_dev_kendall_tau(self.h, d_x, d_y, n, _p(counts), C.byref(tau), stream))
         return tau.value, counts
+
+
+def split_weighted(weights, world: int) -> np.ndarray:
+    """pars_split_weighted (host only): bounds[world + 1] of a contiguous
+    split with equal weight per rank."""
+    w = _c(weights, np.int64)
+    b = np.zeros(world + 1, np.int64)
+    _check(lib().pars_split_weighted(_p(w), len(w), world, _p(b)))
+    return b
+
+
+def dp_shard(n: int, world: int, rank: int):
+    b, e = C.c_int64(), C.c_int64()
+    lib().pars_dp_shard(n, world, rank, C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().pars_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+class DataParallel:
+    """One rank of the NCCL data-parallel layer (pars_dp*).
+
+    Create on every rank with the same 128-byte unique id (from
+    nccl_unique_id() on rank 0, broadcast by the caller) — or wrap an
+    existing ncclComm_t with from_comm. Every method is collective."""
+
+    def __init__(self, ctx: "Context", uid: bytes, world: int, rank: int):
+        h = C.c_void_p()
+        idb = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().pars_dp_create(ctx.h, idb, world, rank, C.byref(h)))
+        self.ctx, self.h = ctx, h
+
+    @classmethod
+    def from_comm(cls, ctx: "Context", comm_ptr: int) -> "DataParallel":
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        _check(lib().pars_dp_create_from_comm(ctx.h, C.c_void_p(comm_ptr), C.byref(h)))
+        self.ctx, self.h = ctx, h
+        return self
+
+    @property
+    def rank(self) -> int:
+        return lib().pars_dp_rank(self.h)
+
+    @property
+    def world(self) -> int:
+        return lib().pars_dp_world(self.h)
+
+    def score_order(self, ex: Extractor, d_text: int, d_offsets: int, n_total: int, d_w: int,
+                    bias: float, mode: int, d_scores_all: int, d_order_all: int,
+                    d_boosted_all: int = 0, d_tie_all: int = 0, stream: int = 0):
+        """pars_dp_score_order on device pointers (this rank's shard text)."""
+        _check(lib().pars_dp_score_order(self.h, C.byref(ex), d_text, d_offsets, n_total, d_w, bias,
+                                         mode, d_boosted_all or None, d_tie_all or None,
+                                         d_scores_all or None, d_order_all or None, stream or None))
+
+    def train_step(self, feats: "Features", plan: "PairPlan", d_w: int, margin: float, lr: float,
+                   d_coeff: int, d_scores_all: int = 0, d_counters: int = 0, d_loss: int = 0,
+                   stream: int = 0):
+        """pars_dp_train_step: one full-batch all-pairs step, w updated in place."""
+        _check(lib().pars_dp_train_step(self.h, C.c_void_p(feats.h), C.c_void_p(plan.h), d_w, margin,
+                                        lr, d_scores_all or None, d_coeff, d_counters or None,
+                                        d_loss or None, stream or None))
+
+    def kendall_tau(self, d_x: int, d_y: int, n: int, stream: int = 0):
+        counts = np.zeros(5, np.uint64)
+        tau = C.c_double()
+        _check(lib().pars_dp_kendall_tau(self.h, d_x, d_y, n, _p(counts), C.byref(tau),
+                                         stream or None))
+        return tau.value, counts
+
+    def close(self):
+        if self.h:
+            lib().pars_dp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

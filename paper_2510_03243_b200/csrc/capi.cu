@@ -9,8 +9,12 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -19,6 +23,7 @@
 #include "ingest.cuh"
 #include "ingest_host.hpp"
 #include "sgd_cluster.cuh"
+#include "tiles.cuh"
 
 namespace pars_b200 {
 
@@ -52,6 +57,64 @@ struct HostBuf {
   size_t cap = 0;
 };
 
+// Fork-join pool of host threads for the gathering copy of pageable records
+// into pinned staging (pars_score_records): workers wait on a generation
+// counter; run(k, fn) calls fn(0..k-1) across them and the caller.
+class CopyPool {
+ public:
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this, i] { loop(i + 1); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        f = fn_;
+      }
+      (*f)(id);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
 struct pars_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -61,7 +124,8 @@ struct pars_ctx {
   // grow-only scratch
   DevBuf text[2], offs[2], scores[2], w64, w32, misc, misc2, longl, sort, sgd, pairs_in, dmin_buf,
       gscratch, lists, plan_buf, baseline, tau;
-  HostBuf h_offs[2], h_scores;
+  HostBuf h_offs[2], h_scores, h_text[2];
+  std::unique_ptr<CopyPool> pool;  // created on the first pars_score_records
   std::vector<cudaEvent_t> ev_chunk;  // per-chunk score hand-off (grow-only)
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
@@ -440,8 +504,9 @@ void pars_ctx_destroy(pars_ctx* c) {
                     &c->baseline, &c->tau};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
-  for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores})
+  for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores, &c->h_text[0], &c->h_text[1]})
     if (b->p) cudaFreeHost(b->p);
+  c->pool.reset();
   for (cudaEvent_t e : c->ev_chunk) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(c->ev_copy[k]);
@@ -591,6 +656,105 @@ int pars_score_text(pars_ctx* ctx, const pars_extractor* ex, const char* text,
   PARS_TRY(score_text_pipeline(ctx, cfg, text, offsets, n, weights, bias, mode, nullptr, h_sc, &chunks));
   if (!pin) PARS_TRY(drain_scores(ctx, chunks, h_sc, scores));
   PARS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return PARS_OK;
+}
+
+// Scorer::score_batch over records that live in separate (pageable) host
+// strings — the reference's Dataset of std::string (scorer.cpp:9-24). Each
+// ~64 MB chunk of records is gathered by a pool of host threads straight
+// into pinned staging (one host copy, no packing pass), then streams to the
+// device while the next chunk is gathered and the previous one is scored.
+int pars_score_records(pars_ctx* ctx, const pars_extractor* ex, const char* const* texts,
+                       const int64_t* lens, int64_t n, const double* weights, double bias, int mode,
+                       double* scores) {
+  PARS_TRY(check_ctx(ctx));
+  PARS_TRY(check_mode(mode));
+  FeatConfig cfg;
+  PARS_TRY(check_text_call(ex, n, &cfg, "pars_score_records"));
+  if (n == 0) return PARS_OK;
+  for (int64_t i = 0; i < n; ++i)
+    if (lens[i] < 0 || (lens[i] > 0 && !texts[i])) {
+      set_error("pars_score_records: record %lld has no text", (long long)i);
+      return PARS_ERR_INVALID;
+    }
+  Guard g(ctx);
+  if (!ctx->pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    ctx->pool.reset(new CopyPool((int)std::max(1u, std::min(hc ? hc : 1u, 16u)) - 1));
+  }
+  cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+  PARS_TRY(upload_weights(ctx, cfg, weights, mode, st));
+  const bool pin = is_pinned(scores);
+  double* h_sc = scores;
+  if (!pin) {
+    PARS_TRY(ensure_host(ctx->h_scores, (size_t)n * 8));
+    h_sc = static_cast<double*>(ctx->h_scores.p);
+  }
+  // chunks: <= 2^18 records and <= 64 MB (ramping from 4 MB)
+  const int64_t kChunkPrompts = 1 << 18;
+  int64_t chunk_bytes = 4ll << 20;
+  std::vector<int64_t> starts;
+  int64_t max_bytes = 0, max_n = 0;
+  for (int64_t i = 0; i < n;) {
+    starts.push_back(i);
+    int64_t j = i, bytes = 0;
+    while (j < n && j - i < kChunkPrompts && (j == i || bytes + lens[j] <= chunk_bytes)) bytes += lens[j++];
+    max_bytes = std::max(max_bytes, bytes);
+    max_n = std::max(max_n, j - i);
+    i = j;
+    chunk_bytes = std::min<int64_t>(chunk_bytes * 2, 64ll << 20);
+  }
+  starts.push_back(n);
+  const int nchunks = (int)starts.size() - 1;
+  while ((int)ctx->ev_chunk.size() < nchunks) {
+    cudaEvent_t e;
+    PARS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ev_chunk.push_back(e);
+  }
+  for (int b = 0; b < 2; ++b) {
+    PARS_TRY(ensure(ctx->text[b], (size_t)max_bytes + 16));
+    PARS_TRY(ensure(ctx->offs[b], (size_t)(max_n + 1) * 8));
+    PARS_TRY(ensure(ctx->scores[b], (size_t)max_n * 8));
+    PARS_TRY(ensure_host(ctx->h_offs[b], (size_t)(max_n + 1) * 8));
+    PARS_TRY(ensure_host(ctx->h_text[b], (size_t)max_bytes + 16));
+  }
+  CopyPool& pool = *ctx->pool;
+  const int workers = pool.size();
+  for (int k = 0; k < nchunks; ++k) {
+    const int b = k & 1;
+    const int64_t i0 = starts[k], i1 = starts[k + 1], m = i1 - i0;
+    if (k >= 2) PARS_CUDA_CHECK(cudaEventSynchronize(ctx->ev_copy[b]));  // staging b is free again
+    int64_t* ho = static_cast<int64_t*>(ctx->h_offs[b].p);
+    ho[0] = 0;
+    for (int64_t i = 0; i < m; ++i) ho[i + 1] = ho[i] + lens[i0 + i];
+    char* ht = static_cast<char*>(ctx->h_text[b].p);
+    // byte-balanced split of the chunk's records over the pool
+    const int64_t tb = ho[m];
+    pool.run([&](int w) {
+      int64_t a = 0, e = m;
+      {  // first record whose start is >= w/workers of the bytes
+        const int64_t lo = tb * w / workers, hi = tb * (w + 1) / workers;
+        a = std::lower_bound(ho, ho + m, lo) - ho;
+        e = std::lower_bound(ho, ho + m, hi) - ho;
+        if (w == workers - 1) e = m;
+      }
+      for (int64_t i = a; i < e; ++i)
+        if (lens[i0 + i]) std::memcpy(ht + ho[i], texts[i0 + i], (size_t)lens[i0 + i]);
+    });
+    if (k >= 2) PARS_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->text[b].p, ht, (size_t)tb, cudaMemcpyHostToDevice, cs));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(ctx->offs[b].p, ho, (size_t)(m + 1) * 8, cudaMemcpyHostToDevice, cs));
+    PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_copy[b], cs));
+    PARS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copy[b], 0));
+    double* dst = (double*)ctx->scores[b].p;
+    PARS_TRY(score_chunk(ctx, cfg, mode, static_cast<const uint8_t*>(ctx->text[b].p),
+                         (const int64_t*)ctx->offs[b].p, m, bias, dst, st));
+    PARS_CUDA_CHECK(cudaMemcpyAsync(h_sc + i0, dst, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+    PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_chunk[k], st));
+    PARS_CUDA_CHECK(cudaEventRecord(ctx->ev_done[b], st));
+  }
+  if (!pin) PARS_TRY(drain_scores(ctx, starts, h_sc, scores));
+  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
   return PARS_OK;
 }
 
@@ -902,6 +1066,7 @@ int pars_features_upload(pars_ctx* ctx, uint32_t dim, int64_t rows, const int64_
 
 int64_t pars_features_rows(const pars_features* f) { return f ? f->rows : -1; }
 int64_t pars_features_nnz(const pars_features* f) { return f ? f->nnz : -1; }
+int64_t pars_features_dim(const pars_features* f) { return f ? (int64_t)f->dim : -1; }
 
 int pars_features_download(pars_ctx* ctx, const pars_features* f, int64_t* row_ptr, uint32_t* idx,
                            double* val) {
@@ -1186,6 +1351,49 @@ int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
   return launch_xtc_csc(ctx, f->d_csc_tasks, f->csc_ntasks, f->d_csc_col_task, f->d_csc_row,
                         f->d_csc_val, d_coeff, row_begin, row_end, f->dim, f->d_csc_part, d_grad, st);
 }
+
+}  // extern "C"
+
+// ---- accessors for the data-parallel layer (dp.cu) -------------------------
+namespace pars_b200 {
+int ctx_device(pars_ctx* ctx) { return ctx->device; }
+cudaStream_t ctx_stream(pars_ctx* ctx, void* s) { return capi_detail::pick(ctx, s); }
+void* ctx_sort_scratch(pars_ctx* ctx, size_t bytes) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  return capi_detail::ensure(ctx->sort, bytes + 4096) == PARS_OK ? ctx->sort.p : nullptr;
+}
+int64_t plan_size(const pars_pair_plan* p) { return p ? p->dev.n : 0; }
+// Relative cost of each upper-triangle tile for a cost-balanced split: on a
+// length-sorted plan a tile whose rows keep no column of it costs a load
+// and a reduction (weight 1), any other tile the full column loop (weight
+// 64, the measured ratio of instructions); the general kernel's tiles all
+// cost the same.
+int plan_tile_weights(const pars_pair_plan* p, std::vector<int64_t>* w) {
+  if (!p) {
+    set_error("null pair plan");
+    return PARS_ERR_INVALID;
+  }
+  const int64_t n = p->dev.n;
+  const int64_t T = kPairTile, nt = ceil_div(std::max<int64_t>(n, 0), T);
+  w->assign((size_t)(nt * (nt + 1) / 2), 1);
+  if (!p->dev.monotone || n == 0) return PARS_OK;
+  std::vector<int32_t> f((size_t)n);
+  cudaSetDevice(p->device);
+  PARS_CUDA_CHECK(cudaMemcpy(f.data(), p->dev.f, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  size_t t = 0;
+  for (int64_t I = 0; I < nt; ++I) {
+    const int64_t fmin = f[(size_t)(I * T)];
+    for (int64_t J = I; J < nt; ++J, ++t) {
+      const int64_t J0 = J * T, jn = std::min<int64_t>(T, n - J0);
+      (*w)[t] = (I == J || fmin < J0 + jn) ? 64 : 1;
+    }
+  }
+  return PARS_OK;
+}
+}  // namespace pars_b200
+
+extern "C" {
 
 // ---- training ------------------------------------------------------------
 

@@ -1011,12 +1011,115 @@ __host__ inline size_t lane_slot_bytes(int64_t n) {
   return (size_t)n * kSlotCap * 4 + (size_t)n * 8 + (size_t)n * 4 + 256;
 }
 
-template <int MODE>
+// Exact mode, fused (default): the CTA is kFuseH hashing warps plus one
+// chain warp. A hashing warp walks each prompt's touched buckets in
+// ascending order into a ring slot (kFuseD slots per hashing warp, in global
+// memory that stays L2-resident: 148 x 16 x 8 x 2 KB = 38 MB, rewritten every
+// few microseconds) and publishes it through a shared-memory sequence
+// counter; the chain warp runs the sequential fp64 dots of 32 prompts at a
+// time, one per lane (two generations of every hashing warp), with the
+// weights in shared memory, and hands the slots back. The (idx, count) lists
+// never travel to DRAM and no second kernel runs.
+constexpr int kFuseH = 16;  // hashing warps per CTA (the chain warp maps lane -> (lane & 15, lane >> 4))
+constexpr int kFuseD = 8;   // ring slots per hashing warp
+struct FuseMeta {
+  double inv;
+  int64_t prompt;
+  int32_t nnz;  // entries in the slot; -1: nothing to chain (scored elsewhere)
+  int32_t pad;
+};
+__host__ inline size_t fused_cta_bytes(uint32_t dim) {
+  return (size_t)dim * 2 /* table alignment slack */ + (size_t)kFuseH * lane_warp_bytes(dim) +
+         (size_t)dim * 8 /* fp64 weights */ + (size_t)kFuseH * kFuseD * sizeof(FuseMeta) +
+         2 * kFuseH * sizeof(int) + 64;
+}
+__host__ inline size_t fused_ring_bytes(int64_t grid) {
+  return (size_t)grid * kFuseH * kFuseD * kSlotCap * 4;
+}
+
+// Products of one 4-entry chunk (entries past the list's end give +0.0,
+// which leaves a sum that started at +0.0 unchanged under round-to-nearest).
+__device__ __forceinline__ void chain_products(const FeatConfig& c, const double* sw, uint4 q4,
+                                               int lim, double inv, double p[4]) {
+  const uint32_t ev[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int cn = (int)(ev[t] & 0xffffu) - 0x8000;
+    const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+    const double pr = __dmul_rn(sw[(ev[t] >> 16) & c.mask], v);
+    p[t] = (t < lim && cn != 0) ? pr : 0.0;
+  }
+}
+
+// The chain warp: lane = (hashing warp h, generation parity); 32 prompts'
+// sequential dots per round (features.hpp:31-35, scorer.cpp:40-42).
+__device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const FeatArgs& a,
+                                                 const double* sw, const FuseMeta* meta,
+                                                 volatile int* produced, volatile int* consumed,
+                                                 const uint32_t* ring, int64_t nw, int lane) {
+  const int h = lane & (kFuseH - 1), par = lane >> 4;
+  const int64_t rem = a.n - a.first - ((int64_t)blockIdx.x * kFuseH + h);
+  const int cnt = rem > 0 ? (int)((rem + nw - 1) / nw) : 0;
+  const int maxcnt = __reduce_max_sync(kFull, (unsigned)cnt);
+  for (int T = 0; T < maxcnt; T += 2) {
+    const int t = T + par;
+    const bool valid = t < cnt;
+    if (valid)
+      while (produced[h] <= t) __nanosleep(64);
+    __syncwarp();
+    __threadfence_block();
+    int m = -1;
+    double inv = 1.0;
+    int64_t prompt = 0;
+    const int slot = t % kFuseD;
+    if (valid) {
+      const FuseMeta& f = meta[h * kFuseD + slot];
+      m = f.nnz;
+      inv = f.inv;
+      prompt = f.prompt;
+    }
+    const uint4* L = reinterpret_cast<const uint4*>(ring + ((size_t)h * kFuseD + slot) * kSlotCap);
+    const int nq = m > 0 ? (m + 3) >> 2 : 0;
+    // software pipeline as in chain_slots_thread_kernel; loads bypass L1 (the
+    // slot was rewritten by another warp since this SM last read it)
+    constexpr int kAhead = 4;
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    uint4 r[kAhead];
+#pragma unroll
+    for (int j = 0; j < kAhead; ++j) r[j] = j < nq ? __ldcg(L + j) : z4;
+    double pa[4];
+    chain_products(c, sw, r[0], m, inv, pa);
+    double s = 0.0;
+    for (int q0 = 0; q0 < nq; q0 += kAhead) {
+#pragma unroll
+      for (int j = 0; j < kAhead; ++j) {
+        const int q = q0 + j;
+        if (q < nq) {
+          r[j] = q + kAhead < nq ? __ldcg(L + q + kAhead) : z4;
+          double pb[4];
+          chain_products(c, sw, r[(j + 1) % kAhead], m - 4 * (q + 1), inv, pb);
+          s = __dadd_rn(s, pa[0]);
+          s = __dadd_rn(s, pa[1]);
+          s = __dadd_rn(s, pa[2]);
+          s = __dadd_rn(s, pa[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pa[u] = pb[u];
+        }
+      }
+    }
+    if (m >= 0) a.scores[prompt] = __dadd_rn(s, a.bias);
+    __threadfence_block();
+    __syncwarp();
+    if (par == 0) consumed[h] = T + 2;  // generations <= T + 1 are free again
+  }
+}
+
+template <int MODE, bool FUSED>
 __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool kChain = MODE == kFeatScoreExact;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwc = blockDim.x >> 5;  // hashing warps per CTA
+  const int nwc = FUSED ? kFuseH : (int)(blockDim.x >> 5);  // hashing warps per CTA
   const int64_t gw = (int64_t)blockIdx.x * nwc + warp;
   const int64_t nw = (int64_t)gridDim.x * nwc;
   // tables aligned to their size, so a counter address is base | offset
@@ -1031,6 +1134,43 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
     for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw32[k] = a.w32[k];
     __syncthreads();
   }
+  // fused exact mode: fp64 weights, slot metadata and sequence counters
+  double* sw64 = reinterpret_cast<double*>(sw32);
+  FuseMeta* meta = reinterpret_cast<FuseMeta*>(sw64 + c.dim);
+  volatile int* produced = reinterpret_cast<volatile int*>(meta + kFuseH * kFuseD);
+  volatile int* consumed = produced + kFuseH;
+  uint32_t* ring = a.slots + (size_t)blockIdx.x * kFuseH * kFuseD * kSlotCap;
+  if (FUSED) {
+    for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw64[k] = a.w64[k];
+    if (threadIdx.x < 2 * kFuseH) produced[threadIdx.x] = 0;
+    __syncthreads();
+    if (warp == kFuseH) {
+      fused_chain_warp(c, a, sw64, meta, produced, consumed, ring, (int64_t)gridDim.x * kFuseH, lane);
+      return;
+    }
+  }
+  int gen = 0;  // this warp's prompt count so far (its ring sequence number)
+  // fused: wait until the chain warp has released slot gen % kFuseD
+  auto wait_slot = [&]() {
+    if (lane == 0)
+      while (consumed[warp] < gen - kFuseD + 1) __nanosleep(32);
+    __syncwarp();
+  };
+  // fused: publish generation gen (its slot's entries written by the lanes)
+  auto publish = [&](int nnz, double inv, int64_t prompt) {
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      FuseMeta& f = meta[warp * kFuseD + gen % kFuseD];
+      f.inv = inv;
+      f.prompt = prompt;
+      f.nnz = nnz;
+      __threadfence_block();
+      produced[warp] = gen + 1;
+    }
+    __syncwarp();
+    ++gen;
+  };
   const uint32_t cbase = tb + (uint32_t)warp * tsz;
   const uint32_t bbase = tb + (uint32_t)nwc * tsz + (uint32_t)warp * (c.dim / 8);
   // increments by (ev bit, half, sign): 0 x4, then -1, +1, -1 << 16, +1 << 16
@@ -1089,16 +1229,26 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
       const int64_t nb2 = a.offsets[i + nw], nl = a.offsets[i + nw + 1] - nb2;
       if (fits(nb2, nl)) st_lo = lane_stage(buf, a.text, nb2, nb2 + nl, text_lo, text_hi, lane, pol);
     }
-    if (((len + 1) / 2) + len > kNarrowMaxFeatures) continue;
+    if (((len + 1) / 2) + len > kNarrowMaxFeatures) {
+      if (FUSED) {
+        wait_slot();
+        publish(-1, 1.0, i);
+      }
+      continue;
+    }
     // pass 1: this lane's entries (bitmap popcount)
     uint32_t mine = 0;
     for (uint32_t j = 0; j < nb; ++j) mine += __popc(bm[j]);
     int tot;
     const uint32_t off = (uint32_t)warp_excl_scan((int)mine, lane, &tot);
     long long sq = 0;
-    // exact: the prompt's own slot, or (long lists) the warp's arena
+    // exact: the prompt's own slot (fused: the warp's next ring slot), or
+    // (long lists) the warp's arena
     const bool in_slot = kChain && (uint32_t)tot <= kSlotCap;
-    uint32_t* L = in_slot ? a.slots + (size_t)(i - a.first) * kSlotCap : lists;
+    if (FUSED) wait_slot();
+    uint32_t* L = !in_slot ? lists
+                  : FUSED  ? ring + ((size_t)warp * kFuseD + gen % kFuseD) * kSlotCap
+                           : a.slots + (size_t)(i - a.first) * kSlotCap;
     // pass 2: ascending entries (lane-major = bucket order); resets the table
     uint32_t pos = off;
     float facc = 0.f;
@@ -1120,7 +1270,13 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
       }
     }
     const double inv = inv_norm(c, warp_sum_i64(sq));
-    if (kChain) {
+    if (FUSED) {
+      if (!in_slot) {
+        __syncwarp();
+        chain_group(c, a, lists, true, lane, 1, i, 0, (uint32_t)tot, inv);
+      }
+      publish(in_slot ? tot : -1, inv, i);
+    } else if (kChain) {
       if (lane == 0) {
         a.slot_nnz[i - a.first] = in_slot ? tot : -1;
         a.slot_inv[i - a.first] = inv;
@@ -1144,20 +1300,6 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
 // 16-byte entry loads issued four ahead and the weights in shared memory.
 // It runs right after the hashing kernel on the same chunk of prompts, so
 // the slots it reads were written moments ago and are still in L2.
-// Products of one 4-entry chunk (entries past the list's end give +0.0,
-// which leaves a sum that started at +0.0 unchanged under round-to-nearest).
-__device__ __forceinline__ void chain_products(const FeatConfig& c, const double* sw, uint4 q4,
-                                               int lim, double inv, double p[4]) {
-  const uint32_t ev[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int cn = (int)(ev[t] & 0xffffu) - 0x8000;
-    const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
-    const double pr = __dmul_rn(sw[(ev[t] >> 16) & c.mask], v);
-    p[t] = (t < lim && cn != 0) ? pr : 0.0;
-  }
-}
-
 __global__ void __launch_bounds__(256) chain_slots_thread_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char csm[];
   double* sw = reinterpret_cast<double*>(csm);
@@ -1300,7 +1442,7 @@ int plan_seq(const FeatConfig& c, int64_t items, Plan* p) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto kern = lane ? featurize_lane_kernel<MODE> : featurize_seq_kernel<MODE>;
+  auto kern = lane ? featurize_lane_kernel<MODE, false> : featurize_seq_kernel<MODE>;
   int warps = 1, per_sm = 1, best = 0;
   for (int w : {18, 16, 12, 9, 8, 6, 4, 2, 1}) {
     if (!lane && w > 8) continue;
@@ -1348,8 +1490,58 @@ static int64_t chain_chunk() {
   return v;
 }
 
+// Exact mode runs the fused lane kernel (hashing warps + chain warp) when
+// its shared memory fits; PARS_FEAT_UNFUSED=1 selects the two-kernel form
+// (lane kernel writing per-prompt slots + chain_slots_thread_kernel) for A/B.
+__host__ inline bool use_fused(const FeatConfig& c) {
+  static const bool off = [] {
+    const char* e = std::getenv("PARS_FEAT_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return !off && fused_cta_bytes(c.dim) <= kMaxLaneSmem;
+}
+
+__host__ inline int64_t fused_grid(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div(std::max<int64_t>(n, 1), kFuseH)));
+}
+
+__host__ inline size_t fused_scratch_bytes(const FeatConfig& c, int64_t n) {
+  const int64_t g = fused_grid(n);
+  return (((size_t)list_cap_words(c) * 4 * (size_t)g * kFuseH + 255) & ~(size_t)255) + fused_ring_bytes(g);
+}
+
+int launch_fused(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStream_t st) {
+  auto kern = featurize_lane_kernel<kFeatScoreExact, true>;
+  const size_t bytes = fused_cta_bytes(c.dim);
+  PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int threads = (kFuseH + 1) * 32;
+  int b = 0;
+  PARS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, bytes));
+  if (b < 1) {
+    set_error("featurize: fused kernel does not fit an SM (dimension %u)", c.dim);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  const int64_t grid = fused_grid(a0.n);
+  const size_t arenas = (((size_t)a0.list_cap * 4 * (size_t)grid * kFuseH) + 255) & ~(size_t)255;
+  if (a0.lists_bytes < arenas + fused_ring_bytes(grid)) {
+    set_error("featurize: list scratch too small (fused)");
+    return PARS_ERR_INVALID;
+  }
+  FeatArgs a = a0;
+  a.slots = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a0.lists) + arenas);
+  a.first = 0;
+  kern<<<(unsigned)grid, threads, bytes, st>>>(c, a);
+  count_launch(ctx);
+  PARS_CUDA_CHECK(cudaGetLastError());
+  return PARS_OK;
+}
+
 template <int MODE>
 int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStream_t st) {
+  if (MODE == kFeatScoreExact && use_lane(MODE) && use_fused(c)) return launch_fused(ctx, c, a0, st);
   Plan p;
   PARS_TRY(plan_seq<MODE>(c, a0.n, &p));
   const size_t arenas = (((size_t)a0.list_cap * 4 * (size_t)p.grid * p.warps) + 255) & ~(size_t)255;
@@ -1359,7 +1551,7 @@ int launch_seq(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStrea
     set_error("featurize: list scratch too small");
     return PARS_ERR_INVALID;
   }
-  auto kern = use_lane(MODE) ? featurize_lane_kernel<MODE> : featurize_seq_kernel<MODE>;
+  auto kern = use_lane(MODE) ? featurize_lane_kernel<MODE, false> : featurize_seq_kernel<MODE>;
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   if (!slots) {
     kern<<<(unsigned)p.grid, p.warps * 32, p.smem, st>>>(c, a0);
@@ -1417,9 +1609,11 @@ int scratch_pair(const FeatConfig& c, int64_t n, size_t* gs, size_t* ls) {
   if (POW2 && DEF && use_seq(c)) {
     Plan p;
     PARS_TRY(plan_seq<MODE>(c, n, &p));
-    if (MODE == kFeatScoreExact)
+    if (MODE == kFeatScoreExact) {
       *ls = std::max(*ls, (((size_t)list_cap_words(c) * 4 * (size_t)p.grid * p.warps + 255) & ~(size_t)255) +
                               (use_lane(MODE) ? lane_slot_bytes(std::min<int64_t>(n, chain_chunk())) : 0));
+      if (use_lane(MODE) && use_fused(c)) *ls = std::max(*ls, fused_scratch_bytes(c, n));
+    }
   }
   return PARS_OK;
 }

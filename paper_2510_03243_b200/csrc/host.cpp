@@ -147,14 +147,27 @@ int pars_length_gap_table(double delta, int64_t max_len, int32_t* dmin) {
 
 int pars_tie_ranks(const double* arrival, const char* ids, const int64_t* offs, int64_t n,
                    uint32_t* rank) {
-  std::vector<int64_t> o(n);
-  std::iota(o.begin(), o.end(), 0);
   auto cmp_id = [&](int64_t a, int64_t b) {
     const int64_t la = offs[a + 1] - offs[a], lb = offs[b + 1] - offs[b];
     int r = std::memcmp(ids + offs[a], ids + offs[b], (size_t)std::min(la, lb));
     if (r != 0) return r;
     return la < lb ? -1 : (la > lb ? 1 : 0);
   };
+  // common case (a trace in arrival order, a burst with ascending ids): the
+  // keys are already non-decreasing in input order -> one linear pass
+  bool sorted = true;
+  for (int64_t k = 1; k < n && sorted; ++k)
+    sorted = arrival[k - 1] < arrival[k] || (arrival[k - 1] == arrival[k] && cmp_id(k - 1, k) <= 0);
+  if (sorted) {
+    uint32_t r = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      if (k > 0 && (arrival[k - 1] != arrival[k] || cmp_id(k - 1, k) != 0)) ++r;
+      rank[k] = r;
+    }
+    return PARS_OK;
+  }
+  std::vector<int64_t> o(n);
+  std::iota(o.begin(), o.end(), 0);
   std::stable_sort(o.begin(), o.end(), [&](int64_t a, int64_t b) {
     if (arrival[a] != arrival[b]) return arrival[a] < arrival[b];
     return cmp_id(a, b) < 0;

@@ -77,7 +77,17 @@ int launch_sgd_epoch(pars_ctx* ctx, const int64_t* rp, const uint32_t* idx, cons
                      cudaStream_t st);
 
 // Merge of per-shard select_batch orders into the global one (sort.cu).
+constexpr int kMaxRuns = 64;  // shards (ranks) a merge accepts
+struct RunOffsets {  // by value in kernel parameters: no upload, capturable
+  int64_t off[kMaxRuns + 1];
+  int nruns;
+};
 size_t merge_runs_scratch_bytes(int64_t n, int nruns);
+// Places the elements of run `run` (all runs when run < 0) at their merged
+// positions in order[] (other positions untouched). h_off: host [nruns+1].
+int launch_merge_rank(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
+                      const uint32_t* run_order, const int64_t* h_off, int nruns, int run,
+                      uint32_t* order, void* scratch, cudaStream_t st);
 int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
                       const uint32_t* run_order, const int64_t* h_off, int nruns, int64_t n,
                       uint32_t* order, void* scratch, cudaStream_t st);

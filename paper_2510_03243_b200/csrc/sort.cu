@@ -50,84 +50,133 @@ __device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint32_t lo, int pos) 
   return pos < 4 ? (lo >> (8 * pos)) & 0xffu : (uint32_t)(hi >> (8 * (pos - 4))) & 0xffu;
 }
 
+// All 12 digit histograms in one pass over the inputs (keys formed on the
+// fly), plus whether the tie ranks are already non-decreasing in input
+// order (then the stable sort by score alone is the (score, tie, index)
+// order and the tie digits are skipped).
 __global__ void radix_init(const double* __restrict__ score, const uint8_t* __restrict__ boosted,
-                           const uint32_t* __restrict__ tie, int64_t n, uint64_t* __restrict__ khi,
-                           uint32_t* __restrict__ klo, uint32_t* __restrict__ val,
-                           uint32_t* __restrict__ dh) {
+                           const uint32_t* __restrict__ tie, int64_t n, uint32_t* __restrict__ dh) {
   __shared__ uint32_t h[12 * 256];
   for (int k = threadIdx.x; k < 12 * 256; k += blockDim.x) h[k] = 0;
   __syncthreads();
+  bool unsorted = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool bst = boosted && boosted[i];
     const uint64_t hi = bst ? 0ull : ordered_bits(score[i]);
     const uint32_t lo = tie ? tie[i] : 0u;  // no tie ranks: order by score, then index
-    khi[i] = hi;
-    klo[i] = lo;
-    val[i] = (uint32_t)i;
-    // tie ranks already non-decreasing in input order -> the stable sort
-    // by score alone yields the (score, tie, index) order: skip tie digits
-    if (tie && i > 0 && tie[i] < tie[i - 1]) dh[12 * 256] = 1u;
+    if (tie && i > 0 && lo < tie[i - 1]) unsorted = true;
 #pragma unroll
     for (int p = 0; p < 12; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, p)], 1u);
   }
+  if (__any_sync(kFull, unsorted) && (threadIdx.x & 31) == 0) dh[12 * 256] = 1u;
   __syncthreads();
   for (int k = threadIdx.x; k < 12 * 256; k += blockDim.x)
     if (h[k]) atomicAdd(&dh[k], h[k]);
 }
 
-__global__ void __launch_bounds__(kThreads) radix_hist(const uint64_t* __restrict__ khi,
-                                                       const uint32_t* __restrict__ klo,
-                                                       int64_t n, int pos, int nblocks,
-                                                       uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kTileKeys;
-  for (int k = threadIdx.x; k < kTileKeys; k += kThreads) {
-    const int64_t i = base + k;
-    if (i < n) atomicAdd(&h[digit_of(khi[i], klo[i], pos)], 1u);
-  }
-  __syncthreads();
-  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
-}
+// The per-position pass plan, decided on the device (no host round trip, so
+// the whole sort is stream-ordered and capturable): a position runs when its
+// digits are not all equal (and, for tie digits, when the tie ranks are not
+// already in input order). For every position: active, which ping-pong
+// buffer it reads (or the raw inputs for the first active pass), whether it
+// carries the tie ranks (only while tie passes remain), whether it is the
+// last (writes the order), and the exclusive digit bases.
+struct PassPlan {
+  int active, first, last, src, carry_lo, none;
+};
 
-// Exclusive offsets of one digit position: block d (one warp) scans digit
-// d's per-CTA counts in CTA order, starting from the digit's global base
-// (sum of the all-digit histogram's counts of smaller digits).
-__global__ void __launch_bounds__(32) radix_scan_digits(uint32_t* __restrict__ hist, int nblocks,
-                                                        const uint32_t* __restrict__ dh_pos) {
-  const int d = blockIdx.x, lane = threadIdx.x;
-  uint32_t base = 0;
-  for (int k = lane; k < d; k += 32) base += dh_pos[k];
-  base = __reduce_add_sync(0xffffffffu, base);
-  uint32_t* row = hist + (int64_t)d * nblocks;
-  for (int b0 = 0; b0 < nblocks; b0 += 32) {
-    const int b = b0 + lane;
-    const uint32_t v = b < nblocks ? row[b] : 0u;
-    uint32_t x = v;
+__global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ dh, int64_t n,
+                                                  PassPlan* __restrict__ plan,
+                                                  uint32_t* __restrict__ dbase) {
+  __shared__ int act[12];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool tie_sorted = dh[12 * 256] == 0u;
+  if (t < 12) {
+    bool trivial = false;
+    for (int d = 0; d < 256; ++d)
+      if (dh[t * 256 + d] == (uint32_t)n) trivial = true;
+    act[t] = !trivial && !(t < 4 && tie_sorted);
+  }
+  // exclusive bases of every position, warp w scanning positions w, w+8
+  for (int p = warp; p < 12; p += 8) {
+    uint32_t base = 0;
+    for (int d0 = 0; d0 < 256; d0 += 32) {
+      const uint32_t v = dh[p * 256 + d0 + lane];
+      uint32_t x = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      dbase[p * 256 + d0 + lane] = base + x - v;
+      base += __shfl_sync(kFull, x, 31);
     }
-    if (b < nblocks) row[b] = base + x - v;
-    base += __shfl_sync(0xffffffffu, x, 31);
+  }
+  __syncthreads();
+  if (t == 0) {
+    int last = -1, last_tie = -1, cnt = 0;
+    for (int p = 0; p < 12; ++p)
+      if (act[p]) {
+        last = p;
+        if (p < 4) last_tie = p;
+      }
+    for (int p = 0; p < 12; ++p) {
+      PassPlan q;
+      q.active = act[p];
+      q.first = act[p] && cnt == 0;
+      q.src = cnt & 1;
+      q.last = p == last;
+      q.carry_lo = p < last_tie;  // a later tie pass still needs the ranks
+      q.none = last < 0;
+      plan[p] = q;
+      cnt += act[p];
+    }
   }
 }
 
-__global__ void __launch_bounds__(kThreads) radix_scatter(
-    const uint64_t* __restrict__ khi_in, const uint32_t* __restrict__ klo_in,
-    const uint32_t* __restrict__ val_in, uint64_t* __restrict__ khi_out,
-    uint32_t* __restrict__ klo_out, uint32_t* __restrict__ val_out, int64_t n, int pos,
-    int nblocks, const uint32_t* __restrict__ offsets) {
+// One onesweep LSD pass: dynamic tile ids (launch order), per-tile digit
+// counts by warp match_any ranking, the tile's global digit offsets by
+// decoupled look-back over the previous tiles' (aggregate | inclusive
+// prefix) status words, then the tile laid out in digit order in shared
+// memory and written run by run (coalesced).
+constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kThreads) radix_onesweep(
+    const double* __restrict__ score, const uint8_t* __restrict__ boosted,
+    const uint32_t* __restrict__ tie, uint64_t* __restrict__ khi0, uint64_t* __restrict__ khi1,
+    uint32_t* __restrict__ klo0, uint32_t* __restrict__ klo1, uint32_t* __restrict__ val0,
+    uint32_t* __restrict__ val1, uint32_t* __restrict__ order, int64_t n, int pos,
+    const PassPlan* __restrict__ plans, const uint32_t* __restrict__ dbase,
+    unsigned long long* __restrict__ status, unsigned* __restrict__ tile_ctr) {
+  const PassPlan pl = plans[pos];
+  if (!pl.active) {
+    if (pos == 11 && pl.none)  // every key equal: the stable order is the input order
+      for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+           i += (int64_t)gridDim.x * kThreads)
+        order[i] = (uint32_t)i;
+    return;
+  }
   __shared__ uint32_t wcnt[kThreads / 32][256];
   __shared__ uint32_t gbase[256];
+  __shared__ uint32_t tstart[256];
+  __shared__ uint32_t wsum[kThreads / 32];
+  __shared__ unsigned s_tile;
+  __shared__ uint64_t s_hi[kTileKeys];
+  __shared__ uint32_t s_lo[kTileKeys], s_val[kTileKeys];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   for (int k = threadIdx.x; k < (kThreads / 32) * 256; k += kThreads) (&wcnt[0][0])[k] = 0;
-  gbase[threadIdx.x] = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
   __syncthreads();
-  const int64_t sub = (int64_t)blockIdx.x * kTileKeys + warp * (32 * kItems);
+  const unsigned tile = s_tile;
+  const uint64_t* khi_in = pl.src ? khi1 : khi0;
+  const uint32_t* klo_in = pl.src ? klo1 : klo0;
+  const uint32_t* val_in = pl.src ? val1 : val0;
+  uint64_t* khi_out = pl.src ? khi0 : khi1;
+  uint32_t* klo_out = pl.src ? klo0 : klo1;
+  uint32_t* val_out = pl.src ? val0 : val1;
+  const bool need_lo = pos < 4 || pl.carry_lo;  // this pass reads the tie digits or carries them
+  const int64_t sub = (int64_t)tile * kTileKeys + warp * (32 * kItems);
   const unsigned lt = (1u << lane) - 1u;
   uint64_t hi[kItems];
   uint32_t lo[kItems], vv[kItems], dg[kItems], rk[kItems];
@@ -135,9 +184,15 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
   for (int r = 0; r < kItems; ++r) {
     const int64_t i = sub + r * 32 + lane;
     const bool ok = i < n;
-    hi[r] = ok ? khi_in[i] : 0ull;
-    lo[r] = ok ? klo_in[i] : 0u;
-    vv[r] = ok ? val_in[i] : 0u;
+    if (pl.first) {
+      hi[r] = ok ? ((boosted && boosted[i]) ? 0ull : ordered_bits(score[i])) : 0ull;
+      lo[r] = (ok && tie) ? tie[i] : 0u;
+      vv[r] = (uint32_t)i;
+    } else {
+      hi[r] = ok ? khi_in[i] : 0ull;
+      lo[r] = (ok && need_lo) ? klo_in[i] : 0u;
+      vv[r] = ok ? val_in[i] : 0u;
+    }
     const uint32_t d = ok ? digit_of(hi[r], lo[r], pos) : 256u;
     dg[r] = d;
     const unsigned peers = __match_any_sync(kFull, d);
@@ -148,9 +203,7 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
     __syncwarp();
   }
   __syncthreads();
-  __shared__ uint32_t tstart[256];  // the tile's digit runs, exclusive prefix
-  __shared__ uint32_t wsum[kThreads / 32];
-  {  // thread = digit: each warp's offset inside the digit's run, the run length
+  {  // thread = digit: warp offsets inside the digit's run, the tile's count
     const int d = threadIdx.x;
     uint32_t run = 0;
     for (int w = 0; w < kThreads / 32; ++w) {
@@ -158,7 +211,27 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
       wcnt[w][d] = run;
       run += c;
     }
-    // exclusive scan of the run lengths over the 256 digits
+    // decoupled look-back: publish the aggregate, add predecessors' counts
+    // until one has its inclusive prefix, publish ours
+    unsigned long long* st = status + (size_t)tile * 256 + d;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      __stcg(st, kStPre | run);
+    } else {
+      __stcg(st, kStAgg | run);
+      for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
+        unsigned long long v;
+        const unsigned long long* q = status + (size_t)j * 256 + d;
+        do {
+          v = *reinterpret_cast<const volatile unsigned long long*>(q);
+        } while ((v & ~kStMask) == 0);
+        excl += (uint32_t)(v & kStMask);
+        if ((v & ~kStMask) == kStPre) break;
+      }
+      __stcg(st, kStPre | (excl + run));
+    }
+    gbase[d] = dbase[pos * 256 + d] + excl;
+    // the tile's digit runs: exclusive scan of the run lengths
     uint32_t x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -172,11 +245,6 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
     tstart[d] = wb + x - run;
   }
   __syncthreads();
-  // the tile in digit order in shared memory, then written out run by run:
-  // consecutive threads store consecutive addresses of a digit's run instead
-  // of every key landing in its own sector
-  __shared__ uint64_t s_hi[kTileKeys];
-  __shared__ uint32_t s_lo[kTileKeys], s_val[kTileKeys];
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     if (dg[r] < 256u) {
@@ -187,19 +255,26 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(
     }
   }
   __syncthreads();
-  const int64_t t0 = (int64_t)blockIdx.x * kTileKeys;
+  const int64_t t0 = (int64_t)tile * kTileKeys;
   const int cnt = (int)(n - t0 < kTileKeys ? n - t0 : (int64_t)kTileKeys);
   for (int k = threadIdx.x; k < cnt; k += kThreads) {
     const uint64_t h = s_hi[k];
     const uint32_t l = s_lo[k];
     const uint32_t d = digit_of(h, l, pos);
     const uint32_t p = gbase[d] + (uint32_t)k - tstart[d];
-    khi_out[p] = h;
-    klo_out[p] = l;
-    val_out[p] = s_val[k];
+    if (pl.last) {
+      order[p] = s_val[k];
+    } else {
+      khi_out[p] = h;
+      if (pl.carry_lo) klo_out[p] = l;
+      val_out[p] = s_val[k];
+    }
   }
 }
 
+}  // namespace
+
+namespace {
 // Small queues (n <= kSmallSort): one CTA, one launch, no host round trip.
 // The key (ordered score bits or 0 if boosted, tie rank, input index) is
 // unique, so ANY correct sort of it yields the stable order the radix path
@@ -250,19 +325,23 @@ __global__ void __launch_bounds__(kSmallThreads) small_sort_kernel(
 // Runs [off[r], off[r+1]) are each in select_batch order (run-local orders
 // from launch_priority_sort on the shard). Every element becomes the 128-bit
 // key (hi = boosted ? 0 : ordered_bits(score), lo = tie << 32 | index), a
-// total order equal to the global sort's (key, tie, then input index), and
-// adjacent runs are merged level by level: each element finds its place in
-// the sibling run by binary search (keys are unique, so no tie rule is needed).
+// total order equal to the global sort's (key, tie, then input index) with
+// no two keys equal. An element's place in the merged order is then its
+// position in its own run plus, for every other run, the number of that
+// run's keys below it (one binary search per run): one level, any run count,
+// and each element's place is independent of every other's — so a data-
+// parallel rank can place only its own run's elements (launch_merge_rank
+// with run >= 0) and the ranks' disjoint outputs combine by a sum.
 namespace {
 __global__ void merge_keys_kernel(const double* __restrict__ score, const uint8_t* __restrict__ boosted,
                                   const uint32_t* __restrict__ tie, const uint32_t* __restrict__ run_order,
-                                  const int64_t* __restrict__ off, int nruns, int64_t n,
-                                  uint64_t* __restrict__ hi, uint64_t* __restrict__ lo) {
+                                  const RunOffsets off, int64_t n, uint64_t* __restrict__ hi,
+                                  uint64_t* __restrict__ lo) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int r = 0;
-  while (r + 1 < nruns && off[r + 1] <= k) ++r;  // nruns is the rank count: small
-  const uint32_t i = (uint32_t)(off[r] + run_order[k]);
+  while (r + 1 < off.nruns && off.off[r + 1] <= k) ++r;  // nruns is the rank count: small
+  const uint32_t i = (uint32_t)(off.off[r] + run_order[k]);
   hi[k] = (boosted && boosted[i]) ? 0ull : ordered_bits(score[i]);
   lo[k] = ((uint64_t)(tie ? tie[i] : 0u) << 32) | i;
 }
@@ -271,96 +350,81 @@ __device__ __forceinline__ bool key_less(uint64_t ah, uint64_t al, uint64_t bh, 
   return ah < bh || (ah == bh && al < bl);
 }
 
-// one level: runs (a, b) = (2m, 2m+1) of the current boundaries merge into
-// [off[2m], off[2m+2]); boundaries for the next level are every other one
-__global__ void merge_level_kernel(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo,
-                                   const int64_t* __restrict__ off, int nruns, int64_t n,
-                                   uint64_t* __restrict__ ohi, uint64_t* __restrict__ olo) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+// Elements [k0, k1) (one run, or all): order[place] = input index.
+__global__ void merge_rank_kernel(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo,
+                                  const RunOffsets off, int64_t k0, int64_t k1,
+                                  uint32_t* __restrict__ order) {
+  const int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   int r = 0;
-  while (r + 1 < nruns && off[r + 1] <= k) ++r;
+  while (r + 1 < off.nruns && off.off[r + 1] <= k) ++r;
   const uint64_t h = hi[k], l = lo[k];
-  const int sib = r ^ 1;
-  if (sib >= nruns) {  // odd run out: copied through
-    ohi[k] = h;
-    olo[k] = l;
-    return;
+  int64_t pos = k - off.off[r];
+  for (int j = 0; j < off.nruns; ++j) {
+    if (j == r) continue;
+    int64_t a = off.off[j], b = off.off[j + 1];  // first element of run j above (h, l)
+    const int64_t s0 = a;
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if (key_less(hi[m], lo[m], h, l)) a = m + 1; else b = m;
+    }
+    pos += a - s0;
   }
-  const int64_t s0 = off[sib], s1 = off[sib + 1];
-  int64_t a = s0, b = s1;  // first sibling element greater than (h, l)
-  while (a < b) {
-    const int64_t m = (a + b) >> 1;
-    if (key_less(hi[m], lo[m], h, l)) a = m + 1; else b = m;
-  }
-  const int64_t base = off[r & ~1];
-  const int64_t pos = base + (k - off[r]) + (a - s0);
-  ohi[pos] = h;
-  olo[pos] = l;
-}
-
-__global__ void merge_out_kernel(const uint64_t* __restrict__ lo, int64_t n, uint32_t* __restrict__ order) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) order[k] = (uint32_t)lo[k];
+  order[pos] = (uint32_t)l;
 }
 
 }  // namespace
 
 size_t merge_runs_scratch_bytes(int64_t n, int nruns) {
-  return 4 * ((size_t)n * 8 + 256) + 2 * ((size_t)(nruns + 1) * 8 + 256);
+  (void)nruns;
+  return 2 * ((size_t)n * 8 + 256);
 }
 
-int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
-                      const uint32_t* run_order, const int64_t* h_off, int nruns, int64_t n,
+int launch_merge_rank(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
+                      const uint32_t* run_order, const int64_t* h_off, int nruns, int run,
                       uint32_t* order, void* scratch, cudaStream_t st) {
+  if (nruns < 1 || nruns > kMaxRuns) {
+    set_error("merge_orders: %d runs (supported: 1..%d)", nruns, kMaxRuns);
+    return PARS_ERR_UNSUPPORTED;
+  }
+  const int64_t n = h_off[nruns];
   if (n == 0) return PARS_OK;
   if (n > 0x7fffffffLL) {
     set_error("priority order: n=%lld exceeds 2^31-1", (long long)n);
     return PARS_ERR_UNSUPPORTED;
   }
+  RunOffsets off{};
+  off.nruns = nruns;
+  for (int r = 0; r <= nruns; ++r) off.off[r] = h_off[r];
   char* p = static_cast<char*>(scratch);
-  auto take = [&](size_t bytes) {
-    char* r = p;
-    p += (bytes + 255) & ~(size_t)255;
-    return r;
-  };
-  uint64_t* hi[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
-  uint64_t* lo[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
-  int64_t* d_off[2] = {(int64_t*)take((nruns + 1) * 8), (int64_t*)take((nruns + 1) * 8)};
-  const unsigned g = (unsigned)ceil_div(n, 256);
-  std::vector<int64_t> off(h_off, h_off + nruns + 1);
-  PARS_CUDA_CHECK(cudaMemcpyAsync(d_off[0], off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
-  merge_keys_kernel<<<g, 256, 0, st>>>(score, boosted, tie, run_order, d_off[0], nruns, n, hi[0], lo[0]);
+  uint64_t* hi = (uint64_t*)p;
+  uint64_t* lo = (uint64_t*)(p + (((size_t)n * 8 + 255) & ~(size_t)255));
+  const int64_t k0 = run < 0 ? 0 : h_off[run], k1 = run < 0 ? n : h_off[run + 1];
+  merge_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(score, boosted, tie, run_order, off, n,
+                                                                 hi, lo);
   count_launch(ctx);
-  int cur = 0, cb = 0;
-  int runs = nruns;
-  while (runs > 1) {
-    merge_level_kernel<<<g, 256, 0, st>>>(hi[cur], lo[cur], d_off[cb], runs, n, hi[cur ^ 1],
-                                          lo[cur ^ 1]);
+  if (k1 > k0) {
+    merge_rank_kernel<<<(unsigned)ceil_div(k1 - k0, 256), 256, 0, st>>>(hi, lo, off, k0, k1, order);
     count_launch(ctx);
-    cur ^= 1;
-    std::vector<int64_t> next;
-    for (int r = 0; r < runs; r += 2) next.push_back(off[r]);
-    next.push_back(off[runs]);
-    off.swap(next);
-    runs = (int)off.size() - 1;
-    cb ^= 1;
-    PARS_CUDA_CHECK(cudaMemcpyAsync(d_off[cb], off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
   }
-  merge_out_kernel<<<g, 256, 0, st>>>(lo[cur], n, order);
-  count_launch(ctx);
   PARS_CUDA_CHECK(cudaGetLastError());
-  // the boundary vectors are pageable host memory read by async copies
-  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
   return PARS_OK;
+}
+
+int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted, const uint32_t* tie,
+                      const uint32_t* run_order, const int64_t* h_off, int nruns, int64_t n,
+                      uint32_t* order, void* scratch, cudaStream_t st) {
+  (void)n;
+  return launch_merge_rank(ctx, score, boosted, tie, run_order, h_off, nruns, -1, order, scratch, st);
 }
 
 size_t sort_scratch_bytes(int64_t n) {
   const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kTileKeys);
   size_t b = 0;
-  b += 2 * (size_t)n * 8 + 2 * (size_t)n * 4 + 2 * (size_t)n * 4;
-  b += (size_t)nb * 256 * 4 + 12 * 256 * 4 + 1024;
-  return b;
+  b += 2 * ((size_t)n * 8 + 256) + 2 * ((size_t)n * 4 + 256) * 2;  // khi, klo, val ping-pong
+  b += (size_t)nb * 256 * 8 * 12 + 256;                            // look-back status per pass
+  b += 12 * 256 * 4 * 2 + 1024 + 12 * sizeof(PassPlan) + 64 * 4;  // histograms, bases, plan, tile ids
+  return b + 4096;
 }
 
 int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boosted,
@@ -393,35 +457,32 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   uint64_t* khi[2] = {(uint64_t*)take(n * 8), (uint64_t*)take(n * 8)};
   uint32_t* klo[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
   uint32_t* val[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
-  uint32_t* hist = (uint32_t*)take((size_t)nb * 256 * 4);
-  uint32_t* dh = (uint32_t*)take(12 * 256 * 4 + 16);
-  PARS_CUDA_CHECK(cudaMemsetAsync(dh, 0, 12 * 256 * 4 + 16, st));
+  // zeroed together: status words, tile counters, histograms + tie flag
+  const size_t status_bytes = (size_t)nb * 256 * 8 * 12;
+  char* zero0 = p;
+  auto* status = (unsigned long long*)take(status_bytes);
+  auto* tile_ctr = (unsigned*)take(64 * 4);
+  auto* dh = (uint32_t*)take(12 * 256 * 4 + 16);
+  const size_t zero_bytes = (size_t)(p - zero0);
+  auto* dbase = (uint32_t*)take(12 * 256 * 4);
+  auto* plan = (PassPlan*)take(12 * sizeof(PassPlan));
+  PARS_CUDA_CHECK(cudaMemsetAsync(zero0, 0, zero_bytes, st));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t ig = std::min<int64_t>(ceil_div(n, 256), (int64_t)sms * 4);
-  radix_init<<<(unsigned)ig, 256, 0, st>>>(score, boosted, tie, n, khi[0], klo[0], val[0], dh);
-  count_launch(ctx);
-  PARS_CUDA_CHECK(cudaGetLastError());
-  std::vector<uint32_t> hh(12 * 256 + 1);
-  PARS_CUDA_CHECK(cudaMemcpyAsync(hh.data(), dh, hh.size() * 4, cudaMemcpyDeviceToHost, st));
-  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
-  const bool tie_sorted = hh[12 * 256] == 0;
-  int cur = 0;
-  for (int pos = tie_sorted ? 4 : 0; pos < 12; ++pos) {
-    bool trivial = false;
-    for (int d = 0; d < 256; ++d)
-      if (hh[pos * 256 + d] == (uint32_t)n) trivial = true;
-    if (trivial) continue;
-    radix_hist<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], n, pos, nb, hist);
-    radix_scan_digits<<<256, 32, 0, st>>>(hist, nb, dh + pos * 256);
-    radix_scatter<<<nb, kThreads, 0, st>>>(khi[cur], klo[cur], val[cur], khi[cur ^ 1],
-                                           klo[cur ^ 1], val[cur ^ 1], n, pos, nb, hist);
-    count_launch(ctx, 3);
-    PARS_CUDA_CHECK(cudaGetLastError());
-    cur ^= 1;
+  radix_init<<<(unsigned)ig, 256, 0, st>>>(score, boosted, tie, n, dh);
+  radix_plan<<<1, 256, 0, st>>>(dh, n, plan, dbase);
+  count_launch(ctx, 2);
+  // without tie ranks the tie digits are all zero: those passes are known
+  // trivial on the host and not launched at all
+  for (int pos = tie ? 0 : 4; pos < 12; ++pos) {
+    radix_onesweep<<<nb, kThreads, 0, st>>>(score, boosted, tie, khi[0], khi[1], klo[0], klo[1], val[0],
+                                            val[1], order, n, pos, plan, dbase,
+                                            status + (size_t)nb * 256 * pos, tile_ctr + pos);
+    count_launch(ctx);
   }
-  PARS_CUDA_CHECK(cudaMemcpyAsync(order, val[cur], (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  PARS_CUDA_CHECK(cudaGetLastError());
   return PARS_OK;
 }
 

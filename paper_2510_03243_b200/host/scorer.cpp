@@ -35,10 +35,17 @@ std::vector<double> linear_scores(const LinearScorer& s, const Dataset& ds) {
                                       s.bias(), PARS_MODE_EXACT_F64, out.data()));
     return out;
   }
-  b200::Packed p = b200::pack(ds);
-  b200::check(pars_score_text(b200::ctx(), &ce, p.text.data(), p.offsets.data(),
-                              static_cast<int64_t>(ds.records.size()), s.weights().data(), s.bias(),
-                              PARS_MODE_EXACT_F64, out.data()));
+  // the records' own strings, gathered by the library into pinned staging
+  // (no packing pass over the dataset)
+  const size_t n = ds.records.size();
+  std::vector<const char*> texts(n);
+  std::vector<int64_t> lens(n);
+  for (size_t i = 0; i < n; ++i) {
+    texts[i] = ds.records[i].prompt_text.data();
+    lens[i] = static_cast<int64_t>(ds.records[i].prompt_text.size());
+  }
+  b200::check(pars_score_records(b200::ctx(), &ce, texts.data(), lens.data(), static_cast<int64_t>(n),
+                                 s.weights().data(), s.bias(), PARS_MODE_EXACT_F64, out.data()));
   return out;
 }
 

@@ -121,3 +121,22 @@ def test_baseline_samplers_match_reference(ref):
         assert lib().pars_listmle_lists(lens.ctypes.data, arena.ctypes.data, offs.ctypes.data, n,
                                         nlists, k, C.c_uint64(seed), got.ctypes.data) == 0
         assert got.tolist() == ref.listmle_lists(ds, nlists, k, seed).tolist()
+
+
+def test_tie_ranks_sorted_fast_path_equals_general_path():
+    """Inputs already in (arrival, id) order take a linear pass; a shuffle of
+    the same requests takes the sort. Every request must get the same dense
+    rank either way (equal keys share one)."""
+    from paper_2510_03243_b200 import tie_ranks
+    rng = np.random.default_rng(11)
+    n = 5000
+    arrival = np.sort(np.round(rng.random(n) * 50, 1))
+    ids = ["p%04d" % rng.integers(0, 3000) for _ in range(n)]
+    key = sorted(range(n), key=lambda i: (arrival[i], ids[i].encode()))
+    arrival, ids = arrival[key], [ids[i] for i in key]
+    r_sorted = tie_ranks(arrival, ids)
+    perm = rng.permutation(n)
+    r_perm = tie_ranks(arrival[perm], [ids[i] for i in perm])
+    assert (r_perm == r_sorted[perm]).all()
+    assert r_sorted[0] == 0 and (np.diff(r_sorted.astype(np.int64)) >= 0).all()
+    assert r_sorted[-1] + 1 == len({(a, i) for a, i in zip(arrival, ids)})

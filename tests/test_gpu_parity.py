@@ -654,3 +654,24 @@ def test_dp_train_step_replays_as_a_cuda_graph(ctx):
     assert torch.equal(w_graph.view(torch.int64), d_w.view(torch.int64))
     assert not torch.equal(d_w, torch.from_numpy(w0).to(dev))
     f.free()
+
+
+@pytest.mark.gpu
+def test_score_records_gather_equals_score_text(ctx, oracle):
+    """pars_score_records (records as separate host strings, gathered into
+    pinned staging by host threads, several chunks) is bit-identical to
+    pars_score_text over the packed arena and to the oracle."""
+    from oracle.bind import Extractor as OEx
+    from paper_2510_03243_b200 import Extractor, Workload
+    wl = Workload.synthesize(40000, 22, pad_tokens=300)  # > 1 chunk of the 4 MB ramp
+    texts = [wl.prompt(i) for i in range(len(wl))]
+    texts[7] = b""  # an empty record
+    w = np.random.default_rng(4).normal(size=4096)
+    s = ctx.score_records(Extractor.make(), texts, w, 0.25)
+    arena = np.frombuffer(b"".join(texts), np.uint8)
+    offs = np.zeros(len(texts) + 1, np.int64)
+    offs[1:] = np.cumsum([len(t) for t in texts])
+    s2 = ctx.score_text(Extractor.make(), arena, offs, w, 0.25)
+    so = oracle.score_batch(OEx.make(), arena, offs, w, 0.25)
+    assert (s.view(np.uint64) == s2.view(np.uint64)).all()
+    assert (s.view(np.uint64) == so.view(np.uint64)).all()

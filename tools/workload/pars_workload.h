@@ -30,6 +30,12 @@ const int64_t* pars_workload_offsets(const pars_workload* w);
 const int64_t* pars_workload_output_len(const pars_workload* w);
 const int64_t* pars_workload_prompt_len(const pars_workload* w);
 void pars_workload_free(pars_workload* w);
+/* Token statistics of prompts [0, n) of a text arena (offsets[n+1],
+ * absolute), tokens split as features.cpp:36-49 (C-locale isspace):
+ * out[0] = tokens, out[1] = sum of token lengths, out[2] = sum of
+ * max(0, len - 2) (char trigrams), out[3] = text bytes. Measurement only
+ * (the integer-issue roofline of bench.py). */
+int pars_workload_token_stats(const char* text, const int64_t* offsets, int64_t n, uint64_t* out);
 const char* pars_workload_last_error(void);
 
 #ifdef __cplusplus

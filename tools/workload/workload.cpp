@@ -142,3 +142,35 @@ void pars_workload_free(pars_workload* w) {
 }
 
 }  // extern "C"
+
+extern "C" int pars_workload_token_stats(const char* text, const int64_t* offsets, int64_t n,
+                                         uint64_t* out) {
+  uint64_t tok = 0, sum = 0, tri = 0;
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t len = 0;
+    for (int64_t p = offsets[i]; p < offsets[i + 1]; ++p) {
+      const unsigned c = t[p];
+      if (c == 32u || (c - 9u) < 5u) {
+        if (len) {
+          ++tok;
+          sum += (uint64_t)len;
+          tri += len > 2 ? (uint64_t)(len - 2) : 0;
+          len = 0;
+        }
+      } else {
+        ++len;
+      }
+    }
+    if (len) {
+      ++tok;
+      sum += (uint64_t)len;
+      tri += len > 2 ? (uint64_t)(len - 2) : 0;
+    }
+  }
+  out[0] = tok;
+  out[1] = sum;
+  out[2] = tri;
+  out[3] = n > 0 ? (uint64_t)(offsets[n] - offsets[0]) : 0;
+  return 0;
+}
