@@ -127,6 +127,12 @@ struct pars_ctx {
   HostBuf h_offs[2], h_scores, h_text[2];
   std::unique_ptr<CopyPool> pool;  // created on the first pars_score_records
   std::vector<cudaEvent_t> ev_chunk;  // per-chunk score hand-off (grow-only)
+  // the ctx's device scratch is shared by calls on any stream: each call's
+  // work is ordered after the previous call's (event recorded on the stream
+  // it used), except inside a stream capture (one stream, ordered already)
+  cudaEvent_t scratch_ev = nullptr;
+  cudaStream_t scratch_stream = nullptr;  // where scratch_ev was last recorded
+  cudaStream_t cur_stream = nullptr;      // the stream the current call uses
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   double dmin_delta = -1.0;
@@ -234,14 +240,43 @@ void pool_release(int device, void* const* ptrs, int k) {
   cudaGetLastError();
 }
 
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Orders `st` after the previous call's use of the ctx scratch.
+void order_on(pars_ctx* ctx, cudaStream_t st) {
+  if (ctx->scratch_stream && ctx->scratch_stream != st && !capturing(st))
+    cudaStreamWaitEvent(st, ctx->scratch_ev, 0);
+  ctx->cur_stream = st;
+}
+
 struct Guard {
   pars_ctx* c;
   std::lock_guard<std::mutex> lk;
-  explicit Guard(pars_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
+  explicit Guard(pars_ctx* ctx) : c(ctx), lk(ctx->mu) {
+    cudaSetDevice(ctx->device);
+    order_on(ctx, ctx->stream);
+  }
+  ~Guard() {
+    cudaStream_t st = c->cur_stream ? c->cur_stream : c->stream;
+    if (c->scratch_ev && !capturing(st)) {
+      cudaEventRecord(c->scratch_ev, st);
+      c->scratch_stream = st;
+    }
+    c->cur_stream = nullptr;
+  }
 };
 
 cudaStream_t pick(pars_ctx* ctx, void* s) {
-  return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+  cudaStream_t st = s ? static_cast<cudaStream_t>(s) : ctx->stream;
+  order_on(ctx, st);
+  return st;
 }
 
 int check_ctx(pars_ctx* ctx) {
@@ -476,6 +511,7 @@ int pars_ctx_create(int device, pars_ctx** out) {
   c->device = device;
   PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   PARS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  PARS_CUDA_CHECK(cudaEventCreateWithFlags(&c->scratch_ev, cudaEventDisableTiming));
   {
     // keep released pool memory cached (features / plans are re-created per call)
     cudaMemPool_t pool;
@@ -508,6 +544,7 @@ void pars_ctx_destroy(pars_ctx* c) {
     if (b->p) cudaFreeHost(b->p);
   c->pool.reset();
   for (cudaEvent_t e : c->ev_chunk) cudaEventDestroy(e);
+  if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(c->ev_copy[k]);
     cudaEventDestroy(c->ev_done[k]);
@@ -1357,11 +1394,17 @@ int pars_dev_xt_c(pars_ctx* ctx, const pars_features* f, const int32_t* d_coeff,
 // ---- accessors for the data-parallel layer (dp.cu) -------------------------
 namespace pars_b200 {
 int ctx_device(pars_ctx* ctx) { return ctx->device; }
-cudaStream_t ctx_stream(pars_ctx* ctx, void* s) { return capi_detail::pick(ctx, s); }
-void* ctx_sort_scratch(pars_ctx* ctx, size_t bytes) {
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  cudaSetDevice(ctx->device);
-  return capi_detail::ensure(ctx->sort, bytes + 4096) == PARS_OK ? ctx->sort.p : nullptr;
+// (no scratch ordering: dp.cu's own kernels use dp-owned buffers; the ctx
+// calls it makes order themselves)
+cudaStream_t ctx_stream(pars_ctx* ctx, void* s) { return s ? static_cast<cudaStream_t>(s) : ctx->stream; }
+int ctx_merge_rank(pars_ctx* ctx, const double* d_scores, const uint8_t* d_boosted,
+                   const uint32_t* d_tie, const uint32_t* d_run_orders, const int64_t* run_offsets,
+                   int nruns, int run, uint32_t* d_order, void* stream) {
+  capi_detail::Guard g(ctx);
+  cudaStream_t st = capi_detail::pick(ctx, stream);
+  PARS_TRY(capi_detail::ensure(ctx->sort, merge_runs_scratch_bytes(run_offsets[nruns], nruns) + 4096));
+  return launch_merge_rank(ctx, d_scores, d_boosted, d_tie, d_run_orders, run_offsets, nruns, run,
+                           d_order, ctx->sort.p, st);
 }
 int64_t plan_size(const pars_pair_plan* p) { return p ? p->dev.n : 0; }
 // Relative cost of each upper-triangle tile for a cost-balanced split: on a

@@ -181,7 +181,9 @@ struct pars_dp {
 namespace pars_b200 {
 int ctx_device(pars_ctx* ctx);
 cudaStream_t ctx_stream(pars_ctx* ctx, void* s);
-void* ctx_sort_scratch(pars_ctx* ctx, size_t bytes);  // grow-only, under the caller's ordering
+int ctx_merge_rank(pars_ctx* ctx, const double* d_scores, const uint8_t* d_boosted,
+                   const uint32_t* d_tie, const uint32_t* d_run_orders, const int64_t* run_offsets,
+                   int nruns, int run, uint32_t* d_order, void* stream);
 int plan_tile_weights(const pars_pair_plan* plan, std::vector<int64_t>* weights);
 int64_t plan_size(const pars_pair_plan* plan);
 }  // namespace pars_b200
@@ -331,13 +333,8 @@ int pars_dev_merge_rank(pars_ctx* ctx, const double* d_scores, const uint8_t* d_
       set_error("merge_orders: run offsets must be non-decreasing");
       return PARS_ERR_INVALID;
     }
-  const int64_t n = run_offsets[nruns];
-  cudaSetDevice(ctx_device(ctx));
-  cudaStream_t st = ctx_stream(ctx, stream);
-  void* scratch = ctx_sort_scratch(ctx, merge_runs_scratch_bytes(n, nruns));
-  if (!scratch) return PARS_ERR_OOM;
-  return launch_merge_rank(ctx, d_scores, d_boosted, d_tie, d_run_orders, run_offsets, nruns, run,
-                           d_order, scratch, st);
+  return ctx_merge_rank(ctx, d_scores, d_boosted, d_tie, d_run_orders, run_offsets, nruns, run,
+                        d_order, stream);
 }
 
 int pars_dp_score_order(pars_dp* dp, const pars_extractor* ex, const char* d_text,

@@ -1011,8 +1011,8 @@ __host__ inline size_t lane_slot_bytes(int64_t n) {
   return (size_t)n * kSlotCap * 4 + (size_t)n * 8 + (size_t)n * 4 + 256;
 }
 
-// Exact mode, fused (default): the CTA is kFuseH hashing warps plus one
-// chain warp. A hashing warp walks each prompt's touched buckets in
+// Exact mode, fused (default): the CTA is kFuseH hashing warps plus kFuseC
+// chain warps. A hashing warp walks each prompt's touched buckets in
 // ascending order into a ring slot (kFuseD slots per hashing warp, in global
 // memory that stays L2-resident: 148 x 16 x 8 x 2 KB = 38 MB, rewritten every
 // few microseconds) and publishes it through a shared-memory sequence
@@ -1020,8 +1020,22 @@ __host__ inline size_t lane_slot_bytes(int64_t n) {
 // time, one per lane (two generations of every hashing warp), with the
 // weights in shared memory, and hands the slots back. The (idx, count) lists
 // never travel to DRAM and no second kernel runs.
-constexpr int kFuseH = 16;  // hashing warps per CTA (the chain warp maps lane -> (lane & 15, lane >> 4))
-constexpr int kFuseD = 8;   // ring slots per hashing warp
+#ifndef PARS_FUSE_H
+#define PARS_FUSE_H 18
+#endif
+#ifndef PARS_FUSE_D
+#define PARS_FUSE_D 8
+#endif
+#ifndef PARS_FUSE_C
+#define PARS_FUSE_C 2
+#endif
+constexpr int kFuseH = PARS_FUSE_H;  // hashing warps per CTA
+constexpr int kFuseD = PARS_FUSE_D;  // ring slots per hashing warp
+constexpr int kFuseC = PARS_FUSE_C;  // chain warps (round-robin over 32-item rounds)
+#ifndef PARS_FUSE_WSMEM
+#define PARS_FUSE_WSMEM 0
+#endif
+constexpr bool kFuseWSmem = PARS_FUSE_WSMEM;  // fp64 weights in shared memory (else through L1)
 struct FuseMeta {
   double inv;
   int64_t prompt;
@@ -1030,8 +1044,8 @@ struct FuseMeta {
 };
 __host__ inline size_t fused_cta_bytes(uint32_t dim) {
   return (size_t)dim * 2 /* table alignment slack */ + (size_t)kFuseH * lane_warp_bytes(dim) +
-         (size_t)dim * 8 /* fp64 weights */ + (size_t)kFuseH * kFuseD * sizeof(FuseMeta) +
-         2 * kFuseH * sizeof(int) + 64;
+         (kFuseWSmem ? (size_t)dim * 8 : 0) + (size_t)kFuseH * kFuseD * sizeof(FuseMeta) +
+         (kFuseH + kFuseH * kFuseD) * sizeof(int) + 64;
 }
 __host__ inline size_t fused_ring_bytes(int64_t grid) {
   return (size_t)grid * kFuseH * kFuseD * kSlotCap * 4;
@@ -1044,26 +1058,32 @@ __device__ __forceinline__ void chain_products(const FeatConfig& c, const double
   const uint32_t ev[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    const int cn = (int)(ev[t] & 0xffffu) - 0x8000;
-    const double v = c.norm ? __dmul_rn((double)cn, inv) : (double)cn;
+    // the biased 16-bit count as a double without an I2F.F64 (a slow pipe):
+    // the bits of 2^52 + (cnt + 2^15), less 2^52 + 2^15, exactly, in one DADD
+    const uint32_t cb = ev[t] & 0xffffu;
+    const double cd = __dsub_rn(__hiloint2double(0x43300000, (int)cb), 4503599627403264.0);
+    const double v = c.norm ? __dmul_rn(cd, inv) : cd;
     const double pr = __dmul_rn(sw[(ev[t] >> 16) & c.mask], v);
-    p[t] = (t < lim && cn != 0) ? pr : 0.0;
+    p[t] = (t < lim && cb != 0x8000u) ? pr : 0.0;
   }
 }
 
-// The chain warp: lane = (hashing warp h, generation parity); 32 prompts'
-// sequential dots per round (features.hpp:31-35, scorer.cpp:40-42).
+// A chain warp: 32 prompts' sequential dots per round (features.hpp:31-35,
+// scorer.cpp:40-42). Round b covers items [32b, 32b + 32) of the sequence
+// (generation t, hashing warp h), item = t * kFuseH + h; chain warp cw takes
+// rounds cw, cw + kFuseC, ...
 __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const FeatArgs& a,
                                                  const double* sw, const FuseMeta* meta,
-                                                 volatile int* produced, volatile int* consumed,
-                                                 const uint32_t* ring, int64_t nw, int lane) {
-  const int h = lane & (kFuseH - 1), par = lane >> 4;
-  const int64_t rem = a.n - a.first - ((int64_t)blockIdx.x * kFuseH + h);
-  const int cnt = rem > 0 ? (int)((rem + nw - 1) / nw) : 0;
-  const int maxcnt = __reduce_max_sync(kFull, (unsigned)cnt);
-  for (int T = 0; T < maxcnt; T += 2) {
-    const int t = T + par;
-    const bool valid = t < cnt;
+                                                 volatile int* produced, volatile int* free_gen,
+                                                 const uint32_t* ring, int64_t nw, int lane, int cw) {
+  const int64_t rem0 = a.n - a.first - (int64_t)blockIdx.x * kFuseH;
+  const int cnt0 = rem0 > 0 ? (int)((rem0 + nw - 1) / nw) : 0;  // warp 0 has the most prompts
+  const int items = cnt0 * kFuseH;
+  for (int b = cw; b * 32 < items; b += kFuseC) {
+    const int j = b * 32 + lane;
+    const int t = j / kFuseH, h = j - t * kFuseH;
+    const int64_t rem = a.n - a.first - ((int64_t)blockIdx.x * kFuseH + h);
+    const bool valid = j < items && (int64_t)t * nw < rem;
     if (valid)
       while (produced[h] <= t) __nanosleep(64);
     __syncwarp();
@@ -1082,7 +1102,7 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
     const int nq = m > 0 ? (m + 3) >> 2 : 0;
     // software pipeline as in chain_slots_thread_kernel; loads bypass L1 (the
     // slot was rewritten by another warp since this SM last read it)
-    constexpr int kAhead = 4;
+    constexpr int kAhead = 8;
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     uint4 r[kAhead];
 #pragma unroll
@@ -1110,12 +1130,13 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
     if (m >= 0) a.scores[prompt] = __dadd_rn(s, a.bias);
     __threadfence_block();
     __syncwarp();
-    if (par == 0) consumed[h] = T + 2;  // generations <= T + 1 are free again
+    if (valid) free_gen[h * kFuseD + slot] = t + kFuseD;  // the slot's next writer
   }
 }
 
 template <int MODE, bool FUSED>
-__global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig c, const FeatArgs a) {
+__global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
+    featurize_lane_kernel(const FeatConfig c, const FeatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool kChain = MODE == kFeatScoreExact;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1134,18 +1155,24 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
     for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw32[k] = a.w32[k];
     __syncthreads();
   }
-  // fused exact mode: fp64 weights, slot metadata and sequence counters
-  double* sw64 = reinterpret_cast<double*>(sw32);
-  FuseMeta* meta = reinterpret_cast<FuseMeta*>(sw64 + c.dim);
+  // fused exact mode: slot metadata and sequence counters (the chain warps
+  // gather the fp64 weights through L1: 32 KB, the rest of the SM's
+  // on-chip memory after the hashing warps' shared memory)
+  double* sw64s = reinterpret_cast<double*>(sw32);
+  const double* sw64 = kFuseWSmem ? sw64s : a.w64;
+  FuseMeta* meta = reinterpret_cast<FuseMeta*>(sw32 + (kFuseWSmem ? 2 * c.dim : 0));
   volatile int* produced = reinterpret_cast<volatile int*>(meta + kFuseH * kFuseD);
-  volatile int* consumed = produced + kFuseH;
+  volatile int* free_gen = produced + kFuseH;  // [kFuseH][kFuseD]: generation allowed to write the slot
   uint32_t* ring = a.slots + (size_t)blockIdx.x * kFuseH * kFuseD * kSlotCap;
   if (FUSED) {
-    for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw64[k] = a.w64[k];
-    if (threadIdx.x < 2 * kFuseH) produced[threadIdx.x] = 0;
+    if (kFuseWSmem)
+      for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw64s[k] = a.w64[k];
+    if (threadIdx.x < kFuseH) produced[threadIdx.x] = 0;
+    if (threadIdx.x < kFuseH * kFuseD) free_gen[threadIdx.x] = threadIdx.x % kFuseD;
     __syncthreads();
-    if (warp == kFuseH) {
-      fused_chain_warp(c, a, sw64, meta, produced, consumed, ring, (int64_t)gridDim.x * kFuseH, lane);
+    if (warp >= kFuseH) {
+      fused_chain_warp(c, a, sw64, meta, produced, free_gen, ring, (int64_t)gridDim.x * kFuseH, lane,
+                       warp - kFuseH);
       return;
     }
   }
@@ -1153,7 +1180,7 @@ __global__ void __launch_bounds__(576, 1) featurize_lane_kernel(const FeatConfig
   // fused: wait until the chain warp has released slot gen % kFuseD
   auto wait_slot = [&]() {
     if (lane == 0)
-      while (consumed[warp] < gen - kFuseD + 1) __nanosleep(32);
+      while (free_gen[warp * kFuseD + gen % kFuseD] != gen) __nanosleep(32);
     __syncwarp();
   };
   // fused: publish generation gen (its slot's entries written by the lanes)
@@ -1517,7 +1544,7 @@ int launch_fused(pars_ctx* ctx, const FeatConfig& c, const FeatArgs& a0, cudaStr
   auto kern = featurize_lane_kernel<kFeatScoreExact, true>;
   const size_t bytes = fused_cta_bytes(c.dim);
   PARS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  const int threads = (kFuseH + 1) * 32;
+  const int threads = (kFuseH + kFuseC) * 32;
   int b = 0;
   PARS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, bytes));
   if (b < 1) {

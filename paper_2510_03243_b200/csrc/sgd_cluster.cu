@@ -177,11 +177,14 @@ __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
     });
     __syncthreads();
     each([&](uint32_t E) {
+      // atomic read / reset: the bucket's other warps read the mask while its
+      // lowest warp clears it (their outcome is the same either way, but a
+      // plain load racing the store is a data race)
       const uint32_t d = E >> 16;
-      const uint32_t m = mask[d];
+      const uint32_t m = atomicOr(&mask[d], 0u);
       if (m && !(m & below)) {  // the bucket's lowest warp this round
         cur[d] += __popc(m);
-        mask[d] = 0;
+        atomicExch(&mask[d], 0u);
       }
     });
     __syncthreads();

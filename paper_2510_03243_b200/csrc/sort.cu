@@ -67,9 +67,22 @@ __global__ void radix_init(const double* __restrict__ score, const uint8_t* __re
     const uint32_t lo = tie ? tie[i] : 0u;  // no tie ranks: order by score, then index
     if (tie && i > 0 && lo < tie[i - 1]) unsorted = true;
 #pragma unroll
-    for (int p = 0; p < 12; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, p)], 1u);
+    for (int p = 0; p < 12; ++p) {
+      if (p < 4 && !tie) continue;  // all-zero tie digits: counted once below
+      const uint32_t d = digit_of(hi, lo, p);
+      // the high byte positions of each word are shared by most keys (the
+      // exponent, the high bytes of the ranks): aggregate them per warp so
+      // the shared-memory atomics do not serialise
+      if (p == 1 || p == 2 || p == 3 || p == 9 || p == 10 || p == 11) {
+        const unsigned peers = __match_any_sync(__activemask(), d);
+        if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&h[p * 256 + d], __popc(peers));
+      } else {
+        atomicAdd(&h[p * 256 + d], 1u);
+      }
+    }
   }
   if (__any_sync(kFull, unsorted) && (threadIdx.x & 31) == 0) dh[12 * 256] = 1u;
+  if (!tie && blockIdx.x == 0 && threadIdx.x < 4) h[threadIdx.x * 256] = (uint32_t)n;
   __syncthreads();
   for (int k = threadIdx.x; k < 12 * 256; k += blockDim.x)
     if (h[k]) atomicAdd(&dh[k], h[k]);
@@ -89,15 +102,16 @@ struct PassPlan {
 __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ dh, int64_t n,
                                                   PassPlan* __restrict__ plan,
                                                   uint32_t* __restrict__ dbase) {
+  __shared__ int trivial[12];
   __shared__ int act[12];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const bool tie_sorted = dh[12 * 256] == 0u;
-  if (t < 12) {
-    bool trivial = false;
-    for (int d = 0; d < 256; ++d)
-      if (dh[t * 256 + d] == (uint32_t)n) trivial = true;
-    act[t] = !trivial && !(t < 4 && tie_sorted);
-  }
+  if (t < 12) trivial[t] = 0;
+  __syncthreads();
+  for (int k = t; k < 12 * 256; k += blockDim.x)  // a digit holding every key
+    if (dh[k] == (uint32_t)n) trivial[k >> 8] = 1;
+  __syncthreads();
+  if (t < 12) act[t] = !trivial[t] && !(t < 4 && tie_sorted);
   // exclusive bases of every position, warp w scanning positions w, w+8
   for (int p = warp; p < 12; p += 8) {
     uint32_t base = 0;
@@ -142,7 +156,20 @@ __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ d
 // memory and written run by run (coalesced).
 constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(kThreads) radix_onesweep(
+// 512 threads x 14 keys = 7,168-key tiles, one CTA per SM: 1M keys are 140
+// tiles, one wave (a pass is latency-bound: two waves cost twice as much)
+constexpr int kSweepThreads = 512;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kSweepItems = 14;
+constexpr int kSweepTile = kSweepThreads * kSweepItems;
+constexpr size_t kSweepSmem = (size_t)kSweepWarps * 256 * 4 /* wcnt */ + 256 * 4 * 2 /* gbase, tstart */ +
+                              64 /* wsum, tile */ + (size_t)kSweepTile * (8 + 4 + 4);
+
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* q) {
+  return *reinterpret_cast<const volatile unsigned long long*>(q);
+}
+
+__global__ void __launch_bounds__(kSweepThreads) radix_onesweep(
     const double* __restrict__ score, const uint8_t* __restrict__ boosted,
     const uint32_t* __restrict__ tie, uint64_t* __restrict__ khi0, uint64_t* __restrict__ khi1,
     uint32_t* __restrict__ klo0, uint32_t* __restrict__ klo1, uint32_t* __restrict__ val0,
@@ -152,23 +179,25 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
   const PassPlan pl = plans[pos];
   if (!pl.active) {
     if (pos == 11 && pl.none)  // every key equal: the stable order is the input order
-      for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
-           i += (int64_t)gridDim.x * kThreads)
+      for (int64_t i = (int64_t)blockIdx.x * kSweepThreads + threadIdx.x; i < n;
+           i += (int64_t)gridDim.x * kSweepThreads)
         order[i] = (uint32_t)i;
     return;
   }
-  __shared__ uint32_t wcnt[kThreads / 32][256];
-  __shared__ uint32_t gbase[256];
-  __shared__ uint32_t tstart[256];
-  __shared__ uint32_t wsum[kThreads / 32];
-  __shared__ unsigned s_tile;
-  __shared__ uint64_t s_hi[kTileKeys];
-  __shared__ uint32_t s_lo[kTileKeys], s_val[kTileKeys];
+  extern __shared__ __align__(16) unsigned char osm[];
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(osm);
+  uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kSweepTile);
+  uint32_t* s_val = s_lo + kSweepTile;
+  uint32_t (*wcnt)[256] = reinterpret_cast<uint32_t (*)[256]>(s_val + kSweepTile);
+  uint32_t* gbase = &wcnt[kSweepWarps][0];
+  uint32_t* tstart = gbase + 256;
+  uint32_t* wsum = tstart + 256;  // [8]
+  unsigned* s_tile = wsum + 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int k = threadIdx.x; k < (kThreads / 32) * 256; k += kThreads) (&wcnt[0][0])[k] = 0;
+  if (threadIdx.x == 0) *s_tile = atomicAdd(tile_ctr, 1u);
+  for (int k = threadIdx.x; k < kSweepWarps * 256; k += kSweepThreads) (&wcnt[0][0])[k] = 0;
   __syncthreads();
-  const unsigned tile = s_tile;
+  const unsigned tile = *s_tile;
   const uint64_t* khi_in = pl.src ? khi1 : khi0;
   const uint32_t* klo_in = pl.src ? klo1 : klo0;
   const uint32_t* val_in = pl.src ? val1 : val0;
@@ -176,12 +205,12 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
   uint32_t* klo_out = pl.src ? klo0 : klo1;
   uint32_t* val_out = pl.src ? val0 : val1;
   const bool need_lo = pos < 4 || pl.carry_lo;  // this pass reads the tie digits or carries them
-  const int64_t sub = (int64_t)tile * kTileKeys + warp * (32 * kItems);
+  const int64_t sub = (int64_t)tile * kSweepTile + warp * (32 * kSweepItems);
   const unsigned lt = (1u << lane) - 1u;
-  uint64_t hi[kItems];
-  uint32_t lo[kItems], vv[kItems], dg[kItems], rk[kItems];
+  uint64_t hi[kSweepItems];
+  uint32_t lo[kSweepItems], vv[kSweepItems], dr[kSweepItems];  // dr = digit << 16 | rank
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
+  for (int r = 0; r < kSweepItems; ++r) {
     const int64_t i = sub + r * 32 + lane;
     const bool ok = i < n;
     if (pl.first) {
@@ -193,75 +222,92 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep(
       lo[r] = (ok && need_lo) ? klo_in[i] : 0u;
       vv[r] = ok ? val_in[i] : 0u;
     }
+  }
+#pragma unroll
+  for (int r = 0; r < kSweepItems; ++r) {
+    const bool ok = sub + r * 32 + lane < n;
     const uint32_t d = ok ? digit_of(hi[r], lo[r], pos) : 256u;
-    dg[r] = d;
     const unsigned peers = __match_any_sync(kFull, d);
     const uint32_t before = ok ? wcnt[warp][d] : 0u;
-    rk[r] = before + __popc(peers & lt);
+    dr[r] = (d << 16) | (before + __popc(peers & lt));
     __syncwarp();
     if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  {  // thread = digit: warp offsets inside the digit's run, the tile's count
-    const int d = threadIdx.x;
-    uint32_t run = 0;
-    for (int w = 0; w < kThreads / 32; ++w) {
+  const int d = threadIdx.x;  // threads 0..255: one digit each
+  uint32_t run = 0, x = 0;
+  if (d < 256) {
+    for (int w = 0; w < kSweepWarps; ++w) {
       const uint32_t c = wcnt[w][d];
       wcnt[w][d] = run;
       run += c;
     }
-    // decoupled look-back: publish the aggregate, add predecessors' counts
-    // until one has its inclusive prefix, publish ours
+    // decoupled look-back, four predecessors per step: publish the
+    // aggregate, add predecessors' counts back to the first inclusive prefix
     unsigned long long* st = status + (size_t)tile * 256 + d;
     uint32_t excl = 0;
     if (tile == 0) {
       __stcg(st, kStPre | run);
     } else {
       __stcg(st, kStAgg | run);
-      for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
-        unsigned long long v;
+      // kLook predecessors per step, loaded together: the inclusive-prefix
+      // front advances kLook tiles per L2 round trip even when every tile
+      // starts at once
+      constexpr int kLook = 8;
+      for (int64_t j = (int64_t)tile - 1;; j -= kLook) {
         const unsigned long long* q = status + (size_t)j * 256 + d;
-        do {
-          v = *reinterpret_cast<const volatile unsigned long long*>(q);
-        } while ((v & ~kStMask) == 0);
-        excl += (uint32_t)(v & kStMask);
-        if ((v & ~kStMask) == kStPre) break;
+        unsigned long long v[kLook];
+#pragma unroll
+        for (int k = 0; k < kLook; ++k) v[k] = j >= k ? ld_status(q - (size_t)k * 256) : kStPre;
+        bool done = false;
+#pragma unroll
+        for (int k = 0; k < kLook; ++k) {
+          if (!done) {
+            while ((v[k] & ~kStMask) == 0) v[k] = ld_status(q - (size_t)k * 256);
+            excl += (uint32_t)(v[k] & kStMask);
+            done = (v[k] & ~kStMask) == kStPre;
+          }
+        }
+        if (done) break;
       }
       __stcg(st, kStPre | (excl + run));
     }
     gbase[d] = dbase[pos * 256 + d] + excl;
     // the tile's digit runs: exclusive scan of the run lengths
-    uint32_t x = run;
+    x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
     if (lane == 31) wsum[warp] = x;
-    __syncthreads();
+  }
+  __syncthreads();
+  if (d < 256) {
     uint32_t wb = 0;
     for (int w = 0; w < warp; ++w) wb += wsum[w];
     tstart[d] = wb + x - run;
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    if (dg[r] < 256u) {
-      const uint32_t lp = tstart[dg[r]] + wcnt[warp][dg[r]] + rk[r];
+  for (int r = 0; r < kSweepItems; ++r) {
+    const uint32_t dg = dr[r] >> 16;
+    if (dg < 256u) {
+      const uint32_t lp = tstart[dg] + wcnt[warp][dg] + (dr[r] & 0xffffu);
       s_hi[lp] = hi[r];
       s_lo[lp] = lo[r];
       s_val[lp] = vv[r];
     }
   }
   __syncthreads();
-  const int64_t t0 = (int64_t)tile * kTileKeys;
-  const int cnt = (int)(n - t0 < kTileKeys ? n - t0 : (int64_t)kTileKeys);
-  for (int k = threadIdx.x; k < cnt; k += kThreads) {
+  const int64_t t0 = (int64_t)tile * kSweepTile;
+  const int cnt = (int)(n - t0 < kSweepTile ? n - t0 : (int64_t)kSweepTile);
+  for (int k = threadIdx.x; k < cnt; k += kSweepThreads) {
     const uint64_t h = s_hi[k];
     const uint32_t l = s_lo[k];
-    const uint32_t d = digit_of(h, l, pos);
-    const uint32_t p = gbase[d] + (uint32_t)k - tstart[d];
+    const uint32_t dd = digit_of(h, l, pos);
+    const uint32_t p = gbase[dd] + (uint32_t)k - tstart[dd];
     if (pl.last) {
       order[p] = s_val[k];
     } else {
@@ -419,7 +465,7 @@ int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted
 }
 
 size_t sort_scratch_bytes(int64_t n) {
-  const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kTileKeys);
+  const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kSweepTile);
   size_t b = 0;
   b += 2 * ((size_t)n * 8 + 256) + 2 * ((size_t)n * 4 + 256) * 2;  // khi, klo, val ping-pong
   b += (size_t)nb * 256 * 8 * 12 + 256;                            // look-back status per pass
@@ -447,7 +493,7 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
     PARS_CUDA_CHECK(cudaGetLastError());
     return PARS_OK;
   }
-  const int nb = (int)ceil_div(n, kTileKeys);
+  const int nb = (int)ceil_div(n, kSweepTile);
   char* p = static_cast<char*>(scratch);
   auto take = [&](size_t bytes) {
     char* r = p;
@@ -470,14 +516,22 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t ig = std::min<int64_t>(ceil_div(n, 256), (int64_t)sms * 4);
+  const int64_t ig = std::min<int64_t>(ceil_div(n, 256), (int64_t)sms * 2);
   radix_init<<<(unsigned)ig, 256, 0, st>>>(score, boosted, tie, n, dh);
+  static bool attr = [] {
+    return cudaFuncSetAttribute(radix_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSweepSmem) == cudaSuccess;
+  }();
+  if (!attr) {
+    set_error("priority order: cannot configure the sort kernel's shared memory");
+    return PARS_ERR_CUDA;
+  }
   radix_plan<<<1, 256, 0, st>>>(dh, n, plan, dbase);
   count_launch(ctx, 2);
   // without tie ranks the tie digits are all zero: those passes are known
   // trivial on the host and not launched at all
   for (int pos = tie ? 0 : 4; pos < 12; ++pos) {
-    radix_onesweep<<<nb, kThreads, 0, st>>>(score, boosted, tie, khi[0], khi[1], klo[0], klo[1], val[0],
+    radix_onesweep<<<nb, kSweepThreads, kSweepSmem, st>>>(score, boosted, tie, khi[0], khi[1], klo[0], klo[1], val[0],
                                             val[1], order, n, pos, plan, dbase,
                                             status + (size_t)nb * 256 * pos, tile_ctr + pos);
     count_launch(ctx);

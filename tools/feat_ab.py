@@ -34,7 +34,7 @@ d_s = torch.empty(n, dtype=torch.float64, device=dev)
 L = P.lib()
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)
-out = {"kernel": "v1" if os.environ.get("PARS_FEAT_V1") == "1" else "lane", "prompts": n}
+out = {"kernel": "v1" if os.environ.get("PARS_FEAT_V1") == "1" else ("lane-unfused" if os.environ.get("PARS_FEAT_UNFUSED") == "1" else "lane-fused"), "prompts": n}
 for mode, name in ((P.MODE_EXACT, "exact"), (P.MODE_FAST, "fast")):
     def run():
         rc = L.pars_dev_score_text(ctx.h, C.byref(ex), d_text.data_ptr(), d_offs.data_ptr(), n,
