@@ -386,6 +386,26 @@ def run_ours(args):
     if world == 1:
         outputs = {"scores_sha256": hashlib.sha256(got.tobytes()).hexdigest()[:32],
                    "order_sha256": hashlib.sha256(got_order.tobytes()).hexdigest()[:32]}
+    # the fast mode on the same prompts (fp32 products, tree reduction): its
+    # kernel time and its order quality as Kendall tau_b against the exact
+    # fp64 scores (GPU tau, metrics.cpp:42-64)
+    fast = None
+    if world == 1 and not args.no_configs:
+        d_fast = torch.empty(n, dtype=torch.float64, device=dev)
+
+        def score_fast():
+            check(L.pars_dev_score_text(ctx.h, __import__("ctypes").byref(ex), d_text.data_ptr(),
+                                        d_offs.data_ptr(), n, d_w.data_ptr(), 0.0, P.MODE_FAST,
+                                        d_fast.data_ptr(), sh))
+        fast_ms = timed_ms(torch, stream, 1, score_fast, args.steps)
+        d_ex = torch.from_numpy(got).to(dev)
+        tau_fe, _ = ctx.dev_kendall_tau(d_ex.data_ptr(), d_fast.data_ptr(), n, stream=sh)
+        fs = d_fast.cpu().numpy()
+        fast = {"kernel_ms": fast_ms, "prompts_per_s": n / (fast_ms / 1e3),
+                "tau_b_vs_exact": tau_fe,
+                "max_abs_diff_vs_exact": float(np.abs(fs - got).max()),
+                "mode": "PARS_MODE_FAST_F32 (fp32 weights and products, tree reduction)"}
+        del d_fast, d_ex
     global_order_ok = None
     if world > 1 and rank == 0:
         # the merged global order equals one sort of all N gathered scores
@@ -541,6 +561,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "prompts/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
             "e2e_reference_api": api_e2e,
+            "fast_mode": fast,
             "gpu_launches": int(launches),
             "clocks": clk,
             "parity": {"c4_scores_all": parity_ok, "c4_order_all": order_ok, "prompts_checked": n,
@@ -906,12 +927,35 @@ def bench_embeddings(P, ctx, torch, dev, stream, args):
     alg = n * dim * 8 + dim * 8 + n * 8
     hbm, _ = peaks()
     ach = alg / (ms / 1e3) / 1e9
+    exact = out.clone()
+    # fast mode (fp32 products, tree reductions, one pass over the rows)
+    w32_rel = None
+
+    def step_fast():
+        rc = L.pars_dev_score_embeddings(ctx.h, C.byref(ex), X.data_ptr(), n, w.data_ptr(), 0.0,
+                                         P.MODE_FAST, out.data_ptr(), sh)
+        if rc != 0:
+            raise P.ParsError(rc, L.pars_last_error().decode("utf-8", "replace"))
+    ms_fast = timed_ms(torch, stream, 1, step_fast, k)
+    # tolerance: |fast - exact| <= 1e-5 * sum_i |w_i v_i|
+    Xn = X / X.norm(dim=1, keepdim=True)
+    mag = (Xn.abs() * w.abs()).sum(dim=1)
+    w32_rel = float(((out - exact).abs() / mag).max())
+    tau_fe, _ = ctx.dev_kendall_tau(exact.data_ptr(), out.data_ptr(), n, stream=sh)
+    del Xn
+    ach_fast = alg / (ms_fast / 1e3) / 1e9
     return {"metric": "prompts scored/s", "value": n / (ms / 1e3), "unit": "prompts/s",
             "ms_per_step": ms, "parity_bitexact_sample": ok, "sample": chk,
             "workload": "PrecomputedEmbedding: 65,536 prompts x 4,096 fp64 dims, L2 norm, exact",
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "algorithmic_bytes_per_launch": alg,
-                         "note": "exact mode reads the rows twice (norm chain, then dot chain)"}}
+                         "note": "exact mode reads the rows twice (norm chain, then dot chain): "
+                                 "its ceiling is 0.5 of this roofline"},
+            "fast": {"ms_per_step": ms_fast, "value": n / (ms_fast / 1e3),
+                     "roofline": {"bound": "hbm", "achieved": ach_fast, "peak": hbm, "unit": "GB/s",
+                                  "frac": ach_fast / hbm},
+                     "max_err_over_sum_abs_wv": w32_rel, "tolerance": 1e-5,
+                     "tau_b_vs_exact": tau_fe}}
 
 
 def bench_ingest(P, ctx, torch, dev, stream, wl, w, args):

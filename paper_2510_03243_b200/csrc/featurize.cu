@@ -1818,26 +1818,154 @@ __global__ void dense_exact_simple_kernel(const double* __restrict__ X, int64_t 
   out[i] = __dadd_rn(s, bias);
 }
 
-// Fast: one warp per prompt, coalesced row reads, fp32 tree reductions.
-__global__ void dense_fast_kernel(const double* __restrict__ X, int64_t n, uint32_t dim,
-                                  int norm, const float* __restrict__ w, double bias,
-                                  double* __restrict__ out) {
+// Fast: one warp per prompt, 16-byte row loads eight deep per lane (4 KB
+// of the row in flight per warp), fp32 products, tree reductions.
+__global__ void __launch_bounds__(256) dense_fast_kernel(const double* __restrict__ X, int64_t n,
+                                                         uint32_t dim, int norm,
+                                                         const float* __restrict__ w, double bias,
+                                                         double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   const double* x = X + i * (int64_t)dim;
   float sq = 0.f, dot = 0.f;
-  for (uint32_t k = lane; k < dim; k += 32) {
-    float v = (float)x[k];
-    sq += v * v;
-    dot += w[k] * v;
+  if ((dim & 1) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const uint32_t n2 = dim >> 1;
+    constexpr int kU = 8;
+    uint32_t k = lane;
+    for (; k + 32 * (kU - 1) < n2; k += 32 * kU) {
+      double2 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = __ldcs(x2 + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const float a = (float)v[u].x, b = (float)v[u].y;
+        const uint32_t e = 2 * (k + 32 * u);
+        sq = fmaf(a, a, fmaf(b, b, sq));
+        dot = fmaf(__ldg(w + e), a, fmaf(__ldg(w + e + 1), b, dot));
+      }
+    }
+    for (; k < n2; k += 32) {
+      const double2 v = __ldcs(x2 + k);
+      const float a = (float)v.x, b = (float)v.y;
+      sq = fmaf(a, a, fmaf(b, b, sq));
+      dot = fmaf(__ldg(w + 2 * k), a, fmaf(__ldg(w + 2 * k + 1), b, dot));
+    }
+  } else {
+    for (uint32_t k = lane; k < dim; k += 32) {
+      const float v = (float)x[k];
+      sq = fmaf(v, v, sq);
+      dot = fmaf(w[k], v, dot);
+    }
   }
   sq = warp_sum_f32(sq);
   dot = warp_sum_f32(dot);
   if (lane == 0) {
-    float inv = (norm && sq > 0.f) ? rsqrtf(sq) : 1.f;
+    const float inv = (norm && sq > 0.f) ? rsqrtf(sq) : 1.f;
     out[i] = (double)(dot * inv) + bias;
   }
+}
+
+// Exact, cooperative staging: a CTA owns blocks of kCoopRows prompts, one
+// thread per prompt running the reference's sequential chains (sum of
+// squares in index order, features.cpp:113-116, then the dot in index order,
+// features.hpp:31-35). All 256 threads stream each 32-column tile of the
+// block's rows into shared memory with 16-byte cp.async copies (a warp
+// covers two 256-byte row segments: full sectors), kCoopStages tiles in
+// flight, the weights' tile alongside; the chains then read their row from
+// shared memory (272-byte pitch: conflict-free 16-byte reads). With L2
+// normalisation the block is streamed twice (the dot needs the norm first).
+constexpr int kCoopRows = 256, kCoopCols = 32, kCoopStages = 3;
+constexpr int kCoopPitch = kCoopCols * 8 + 16;
+constexpr size_t kCoopStageBytes = (size_t)kCoopRows * kCoopPitch + kCoopCols * 8;
+constexpr size_t kCoopSmem = kCoopStages * kCoopStageBytes;
+
+__global__ void __launch_bounds__(kCoopRows, 1) dense_coop_kernel(
+    const double* __restrict__ X, int64_t n, uint32_t dim, int norm, const double* __restrict__ w,
+    double bias, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char csm2[];
+  const int t = threadIdx.x;
+  const uint32_t ntiles = (dim + kCoopCols - 1) / kCoopCols;
+  const int npass = norm ? 2 : 1;
+  const int64_t nblocks = (n + kCoopRows - 1) / kCoopRows;
+  const int64_t my_blocks = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t njobs = my_blocks * npass * ntiles;
+  // job j -> (block, pass, tile): every thread copies 16 of the stage's
+  // 16-byte chunks (+ one weight chunk for threads < 16)
+  auto issue = [&](int64_t j) {
+    const int64_t b = blockIdx.x + (j / (npass * ntiles)) * (int64_t)gridDim.x;
+    const uint32_t kt = (uint32_t)(j % ntiles);
+    const int64_t r0 = b * kCoopRows;
+    const uint32_t c0 = kt * kCoopCols;
+    unsigned char* st = csm2 + (size_t)(j % kCoopStages) * kCoopStageBytes;
+#pragma unroll
+    for (int q = 0; q < (kCoopRows * kCoopCols / 2) / kCoopRows; ++q) {
+      const int c = t + kCoopRows * q;  // chunk: row c / 16, column pair c % 16
+      const int r = c >> 4, cp = c & 15;
+      const uint32_t col = c0 + 2 * cp;
+      const bool ok = r0 + r < n && col < dim;
+      const double* src = ok ? X + (r0 + r) * (int64_t)dim + col : X;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(st + (size_t)r * kCoopPitch + 16 * cp);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                   "r"(ok ? 16 : 0));
+    }
+    if (t < kCoopCols / 2) {
+      const uint32_t col = c0 + 2 * t;
+      const uint32_t dst =
+          (uint32_t)__cvta_generic_to_shared(st + (size_t)kCoopRows * kCoopPitch + 16 * t);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                   "l"(col < dim ? w + col : w), "r"(col < dim ? 16 : 0));
+    }
+  };
+  for (int64_t j = 0; j < kCoopStages - 1; ++j) {
+    if (j < njobs) issue(j);
+    asm volatile("cp.async.commit_group;");
+  }
+  double acc = 0.0, inv = 1.0;
+  bool scale = false;
+  for (int64_t j = 0; j < njobs; ++j) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kCoopStages - 2));
+    __syncthreads();  // stage j % S landed for every thread; stage (j-1) % S is free
+    if (j + kCoopStages - 1 < njobs) issue(j + kCoopStages - 1);
+    asm volatile("cp.async.commit_group;");
+    const int64_t b = blockIdx.x + (j / (npass * ntiles)) * (int64_t)gridDim.x;
+    const int pass = (int)((j / ntiles) % npass);
+    const uint32_t kt = (uint32_t)(j % ntiles);
+    const unsigned char* st = csm2 + (size_t)(j % kCoopStages) * kCoopStageBytes;
+    const double2* row = reinterpret_cast<const double2*>(st + (size_t)t * kCoopPitch);
+    const double2* wt = reinterpret_cast<const double2*>(st + (size_t)kCoopRows * kCoopPitch);
+    const uint32_t cols = min((uint32_t)kCoopCols, dim - kt * kCoopCols);
+    if (kt == 0) acc = 0.0;
+    if (pass == 0 && norm) {
+#pragma unroll 4
+      for (uint32_t k = 0; k < cols / 2; ++k) {
+        const double2 v = row[k];
+        acc = __dadd_rn(acc, __dmul_rn(v.x, v.x));
+        acc = __dadd_rn(acc, __dmul_rn(v.y, v.y));
+      }
+      if (kt == ntiles - 1) {
+        scale = acc > 0.0;
+        inv = scale ? __ddiv_rn(1.0, __dsqrt_rn(acc)) : 1.0;
+      }
+    } else {
+#pragma unroll 4
+      for (uint32_t k = 0; k < cols / 2; ++k) {
+        const double2 v = row[k], ww = wt[k];
+        const double a = scale ? __dmul_rn(v.x, inv) : v.x;
+        const double bq = scale ? __dmul_rn(v.y, inv) : v.y;
+        acc = __dadd_rn(acc, __dmul_rn(ww.x, a));
+        acc = __dadd_rn(acc, __dmul_rn(ww.y, bq));
+      }
+      if (kt == ntiles - 1) {
+        const int64_t i = b * kCoopRows + t;
+        if (i < n) out[i] = __dadd_rn(acc, bias);
+        scale = false;
+        inv = 1.0;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace
@@ -1914,6 +2042,15 @@ int launch_featurize(pars_ctx* ctx, const FeatConfig& c, int mode, const FeatArg
   return PARS_ERR_INVALID;
 }
 
+// PARS_DENSE_TMA=1 selects the round-1 TMA bulk-copy kernel (A/B)
+__host__ inline bool use_dense_tma() {
+  static const bool v = [] {
+    const char* e = std::getenv("PARS_DENSE_TMA");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 int launch_score_dense(pars_ctx* ctx, const FeatConfig& c, int mode, const double* X, int64_t n,
                        const double* w64, const float* w32, double bias, double* scores,
                        cudaStream_t st) {
@@ -1924,6 +2061,15 @@ int launch_score_dense(pars_ctx* ctx, const FeatConfig& c, int mode, const doubl
     if (!aligned) {
       dense_exact_simple_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(X, n, c.dim, c.norm, w64,
                                                                            bias, scores);
+    } else if (!use_dense_tma()) {
+      PARS_CUDA_CHECK(cudaFuncSetAttribute(dense_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kCoopSmem));
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kCoopRows), sms));
+      dense_coop_kernel<<<(unsigned)grid, kCoopRows, kCoopSmem, st>>>(X, n, c.dim, c.norm, w64, bias,
+                                                                    scores);
     } else {
       PARS_CUDA_CHECK(cudaFuncSetAttribute(dense_exact_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem));

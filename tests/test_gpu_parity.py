@@ -319,9 +319,10 @@ def test_c2_epoch_bit_identical(ctx):
     assert fnv64_array(w) == m["c2"]["weights_fnv"] == "f97c96a353829ee2"
 
 
-@pytest.mark.parametrize("n,dim", [(300, 64), (1000, 100), (129, 7), (1, 4096)])
+@pytest.mark.parametrize("n,dim", [(300, 64), (1000, 100), (129, 7), (1, 4096), (600, 4096), (513, 34), (300, 2)])
 def test_embedding_scores_exact(ctx, oracle, n, dim):
-    """Tiled dense kernel: row tails (n % 128), column tails (dim % 16)."""
+    """Cooperative dense kernel: row-block tails (n % 256), column-tile tails
+    (dim % 32), odd dims (the simple kernel), fast mode within 1e-5."""
     from paper_2510_03243_b200 import MODE_EXACT, MODE_FAST, Extractor
     rng = np.random.default_rng(4)
     for norm in ("l2", "none"):
