@@ -676,3 +676,21 @@ def test_score_records_gather_equals_score_text(ctx, oracle):
     so = oracle.score_batch(OEx.make(), arena, offs, w, 0.25)
     assert (s.view(np.uint64) == s2.view(np.uint64)).all()
     assert (s.view(np.uint64) == so.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("n", [4097, 5000, 65536, 100_003, 1 << 20])
+def test_priority_order_radix_sizes(ctx, n):
+    """The onesweep radix path from just above the bitonic switch to 2^20
+    keys (one to 147 tiles of look-back): ties in score and tie rank, +-0.0,
+    boosts, against numpy's lexsort of the same keys."""
+    rng = np.random.default_rng(n)
+    score = rng.choice(np.concatenate([rng.normal(size=300), [0.0, -0.0]]), size=n)
+    tie = rng.integers(0, 50, size=n).astype(np.uint32)
+    boosted = (rng.random(n) < 0.05).astype(np.uint8)
+    got = ctx.priority_order(score, tie, boosted)
+    # select_batch's order: boosted first, then (score, tie), then index; -0.0 == +0.0
+    s = np.where(score == 0, 0.0, score)
+    # boosted keys compare by (tie, index) only
+    want = np.lexsort((np.arange(n), tie, np.where(boosted == 1, 0.0, s), 1 - boosted.astype(np.int64)))
+    assert (got == want).all()
+
