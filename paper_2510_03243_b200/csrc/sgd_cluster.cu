@@ -37,7 +37,10 @@ namespace {
 
 constexpr int kCL = kSgdCluster;  // CTAs per cluster
 constexpr int kThreads = 256;
-constexpr int kChainWarps = 2;  // warps running the step's score chains
+#ifndef PARS_SGD_CHAIN_WARPS
+#define PARS_SGD_CHAIN_WARPS 2
+#endif
+constexpr int kChainWarps = PARS_SGD_CHAIN_WARPS;  // warps running the step's score chains
 constexpr int kChainThreads = kChainWarps * 32;
 constexpr int kBuildThreads = 1024;  // one warp per slot of a placement round
 constexpr int kBuildWarps = kBuildThreads / 32;
@@ -290,7 +293,7 @@ struct Layout {
   uint32_t dim, B, spc, ppc;  // slots / pairs per CTA
   uint32_t rowcap, csccap, runcap;
   size_t w, rowbuf, slotptr, slotsrc, slotlen, slotinv, pairy, cscbuf, runbuf, desc, sinv,
-      loss_all, score, total;
+      loss_all, score, mbar, total;
 };
 
 struct StepDesc {
@@ -301,7 +304,26 @@ struct StepDesc {
   uint32_t ent_end;   // batch-relative end of this CTA's entries
   uint32_t pad;
   uint32_t cshift;    // staged CSC: entry ent_base sits at cscbuf[cshift] (16-byte copies)
+  uint32_t rshift;    // staged runs: run pad sits at runbuf[rshift] (16-byte aligned copy)
 };
+
+// TMA bulk copy global -> this CTA's shared memory, completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tSTAGE_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra STAGE_WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -343,6 +365,8 @@ __host__ __device__ inline Layout make_layout(uint32_t dim, uint32_t B, uint32_t
   o = al16(o + (size_t)B * 8);
   L.score = o;
   o = al16(o + (size_t)L.spc * 8);
+  L.mbar = o;
+  o = al16(o + 2 * 8);
   L.total = o;
   return L;
 }
@@ -372,7 +396,11 @@ struct EpochArgs {
 
 // Stage step q's data for CTA `rank` into buffer `buf`; run by the staging
 // warps (t = thread index within them, nt = their thread count) while the
-// chain warps score step q-1.
+// chain warps score step q-1. The rows, the CTA's CSC entries and its runs
+// are TMA bulk copies (one per slot row, one for the CSC range, one for the
+// runs) completing on the buffer's mbarrier, whose two arrivals (staging
+// warp 0's lane 0 and thread 32, each with the bytes its copies carry) are
+// made here; stage_wait() waits for the phase.
 __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* sm, int64_t q,
                            int buf, int rank, int t, int nt) {
   const int64_t p0 = q * L.B;
@@ -386,10 +414,13 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
   uint32_t* cscbuf = reinterpret_cast<uint32_t*>(sm + L.cscbuf) + (size_t)buf * L.csccap;
   uint2* runbuf = reinterpret_cast<uint2*>(sm + L.runbuf) + (size_t)buf * L.runcap;
   StepDesc* desc = reinterpret_cast<StepDesc*>(sm + L.desc) + buf;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sm + L.mbar) + 8u * (uint32_t)buf;
   const int w = t >> 5, lane = t & 31;
+  // the buffer's previous contents were read through the generic proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (w == 0) {
     // slot metadata, 32 slots at a time; buffer offsets by a warp scan
-    uint32_t off = 0;
+    uint32_t off = 0, bytes = 0;
     for (uint32_t k0 = 0; k0 < L.spc; k0 += 32) {
       const uint32_t k = k0 + lane;
       const int s = rank * (int)L.spc + (int)k;
@@ -410,12 +441,19 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
       const uint32_t my_off = off + x - padded;
       if (k < L.spc) {
         const uint32_t* src = ok ? a.cpk + st.x : nullptr;
+        const bool staged = ok && my_off + padded <= L.rowcap;
         slotlen[k] = len;
         slotsrc[k] = src;
-        slotptr[k] = !ok ? nullptr : (my_off + padded <= L.rowcap ? rowbuf + my_off : src);
+        slotptr[k] = !ok ? nullptr : (staged ? rowbuf + my_off : src);
+        if (staged && padded) {
+          bulk_g2s((uint32_t)__cvta_generic_to_shared(rowbuf + my_off), src, padded * 4, bar);
+          bytes += padded * 4;
+        }
       }
       off += __shfl_sync(0xffffffffu, x, 31);
     }
+    bytes = __reduce_add_sync(0xffffffffu, bytes);
+    if (lane == 0) bar_expect(bar, bytes);
   } else if (t == 32) {
     // this CTA's runs [r0, r1) and batch entries [e0, e1)
     const uint4 q4 = a.desc4[q * kCL + rank];
@@ -424,37 +462,36 @@ __device__ void stage_step(const Layout& L, const EpochArgs& a, unsigned char* s
     d.ent_base = q4.z;
     d.ent_end = q4.w;
     const uint2* rq = a.runs + q * (int64_t)L.dim;
-    d.runs = (d.nruns <= L.runcap) ? runbuf : rq + q4.x;
+    // runs from the 16-byte aligned entry at or before the first (the runs
+    // array has slack after it): run q4.x lands at runbuf[rshift]
+    d.rshift = (uint32_t)((reinterpret_cast<uintptr_t>(rq + q4.x) >> 3) & 1u);
+    const uint32_t rbytes = ((d.nruns + d.rshift) * 8 + 15) & ~15u;
+    const bool runs_staged = d.nruns > 0 && rbytes <= L.runcap * 8;
+    d.runs = runs_staged ? runbuf + d.rshift : rq + q4.x;
     const uint32_t* g0 = a.ent + a.ent_off[q] + d.ent_base;
     d.cshift = (uint32_t)((reinterpret_cast<uintptr_t>(g0) >> 2) & 3u);
-    d.csc = (d.ent_end - d.ent_base + d.cshift + 3 <= L.csccap) ? cscbuf : g0;
+    const uint32_t cbytes = ((d.ent_end - d.ent_base + d.cshift) * 4 + 15) & ~15u;
+    const bool csc_staged = d.ent_end > d.ent_base && d.ent_end - d.ent_base + d.cshift + 3 <= L.csccap;
+    d.csc = csc_staged ? cscbuf : g0;
     d.pad = q4.x;
     *desc = d;
+    uint32_t bytes = 0;
+    if (runs_staged) {
+      bulk_g2s((uint32_t)__cvta_generic_to_shared(runbuf), rq + q4.x - d.rshift, rbytes, bar);
+      bytes += rbytes;
+    }
+    if (csc_staged) {
+      bulk_g2s((uint32_t)__cvta_generic_to_shared(cscbuf), g0 - d.cshift, cbytes, bar);
+      bytes += cbytes;
+    }
+    bar_expect(bar, bytes);
   }
-  asm volatile("bar.sync 1, %0;" ::"r"(nt));  // staging warps only
-  const StepDesc d = *desc;
-  const int nw = nt >> 5;
-  for (uint32_t k = w; k < L.spc; k += nw) {  // one slot per staging warp at a time
-    const uint32_t* dst = slotptr[k];
-    if (dst < rowbuf || dst >= rowbuf + L.rowcap) continue;  // empty or read from global
-    const uint32_t* g = slotsrc[k];
-    const uint32_t n16 = (slotlen[k] + 3) / 4;
-    for (uint32_t c = lane; c < n16; c += 32)
-      __pipeline_memcpy_async(const_cast<uint32_t*>(dst) + 4 * c, g + 4 * c, 16);
-  }
-  if (d.runs == runbuf) {
-    const uint2* g = a.runs + q * (int64_t)L.dim + d.pad;
-    for (uint32_t c = t; c < d.nruns; c += nt) __pipeline_memcpy_async(runbuf + c, g + c, 8);
-  }
-  if (d.csc == cscbuf) {
-    // 16-byte copies from the aligned word at or before the first entry (the
-    // ent array is 256-byte aligned with slack after it, so the up to 3 words
-    // on either side are readable); entry ent_base lands at cscbuf[cshift]
-    const uint32_t* g = a.ent + a.ent_off[q] + d.ent_base - d.cshift;
-    const uint32_t n16 = (d.ent_end - d.ent_base + d.cshift + 3) / 4;
-    for (uint32_t c = t; c < n16; c += nt) __pipeline_memcpy_async(cscbuf + 4 * c, g + 4 * c, 16);
-  }
-  __pipeline_commit();
+  (void)nt;
+}
+
+// Wait until buffer buf's bulk copies have landed (its u-th use, parity u & 1).
+__device__ __forceinline__ void stage_wait(const Layout& L, unsigned char* sm, int buf, int64_t use) {
+  bar_wait((uint32_t)__cvta_generic_to_shared(sm + L.mbar) + 8u * (uint32_t)buf, (uint32_t)(use & 1));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L, const EpochArgs a) {
@@ -475,10 +512,13 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
   for (uint32_t d = tid; d < L.dim; d += kThreads) W[d] = a.w_io[d];
   const int64_t nb = (a.npairs + L.B - 1) / L.B;
   // stage step 0 with every warp but 0, wait, start
-  if (warp >= kChainWarps) {
-    stage_step(L, a, sm, 0, 0, rank, tid - kChainThreads, kThreads - kChainThreads);
-    __pipeline_wait_prior(0);
-  }
+  if (tid < 2)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"((uint32_t)__cvta_generic_to_shared(sm + L.mbar) +
+                                                                  8u * tid));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (warp >= kChainWarps) stage_step(L, a, sm, 0, 0, rank, tid - kChainThreads, kThreads - kChainThreads);
+  if (tid == 0) stage_wait(L, sm, 0, 0);
   __syncthreads();
   cluster.sync();
   double epoch_loss = 0.0;
@@ -564,8 +604,9 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     const double scale = __ddiv_rn(a.lr, (double)bn);
     const uint32_t* cbuf = reinterpret_cast<const uint32_t*>(sm + L.cscbuf) + (size_t)buf * L.csccap;
     const bool csc_staged = d.csc == cbuf;
-    const bool runs_staged = d.runs == reinterpret_cast<const uint2*>(sm + L.runbuf) + (size_t)buf * L.runcap;
-    const uint2* runs_s = reinterpret_cast<const uint2*>(smw + (L.runbuf >> 2)) + (size_t)buf * L.runcap;
+    const bool runs_staged =
+        d.runs == reinterpret_cast<const uint2*>(sm + L.runbuf) + (size_t)buf * L.runcap + d.rshift;
+    const uint2* runs_s = reinterpret_cast<const uint2*>(smw + (L.runbuf >> 2)) + (size_t)buf * L.runcap + d.rshift;
     for (uint32_t r = tid; r < d.nruns; r += kThreads) {
       const uint2 run = runs_staged ? runs_s[r] : d.runs[r];
       const uint32_t e1 =
@@ -599,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #ifdef PARS_SGD_TIMING
     long long c3 = clock64();
 #endif
-    if (warp >= kChainWarps) __pipeline_wait_prior(0);  // next step's staged data
+    if (tid == 0 && q + 1 < nb) stage_wait(L, sm, buf ^ 1, (q + 1) >> 1);  // next step's staged data
 #ifdef PARS_SGD_TIMING
     long long c4 = clock64();
 #endif
