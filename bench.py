@@ -843,6 +843,12 @@ def bench_tau(P, ctx, torch, dev, stream, world, rank, args, dp=None):
     pairs = n * (n - 1) // 2
     out = {"metric": "pairs/s", "value": pairs / (ms / 1e3), "ms_per_call": ms, "tau_b": tau,
            "algorithm": "sorted counts (two radix sorts + merge inversion count), exact",
+           "roofline": {"bound": "latency", "floor_bytes": 16 * n + 32,
+                        "bytes_model": "one-pass I/O floor: x and y (8 B each) read once, 4 counts written",
+                        "achieved": (16 * n + 32) / (ms / 1e3) / 1e9, "peak": peaks()[0], "unit": "GB/s",
+                        "frac": (16 * n + 32) / (ms / 1e3) / 1e9 / peaks()[0],
+                        "note": "the two stable radix sorts (sort roofline) and log2(n) merge levels are "
+                                "dependent launches on 0.8 MB of L2-resident data"},
            "pairs_path_ms": ms_pairs, "pairs_path_pairs_per_s": pairs / (ms_pairs / 1e3),
            "paths_agree": bool((c == c_p).all()) and tau == tau_p,
            "workload": "kendall_tau_b(scores, output_len) over 100,000 requests "
@@ -1131,6 +1137,31 @@ def bench_configs(P, ctx, args):
           "loss0": float(lt2[0]).hex(), "weights_fnv": fnv64(w2),
           "parity_bitexact": fnv64(w2) == "f97c96a353829ee2"
           and float(lt2[0]).hex() == "0x1.1b1e92d7700cap-1"}
+    # the SGD epoch alone against its latency floor: every step's score
+    # chains run in parallel, so a step is at least its longest chain of
+    # dependent __dadd_rn (8 cycles each, tools/micro/fp64_latency.cu)
+    f2 = ctx.extract(ex, d2.text, d2.offsets)
+    a2, b2, y2, _ = P.build_pairs(d2.output_len, 0.2, 100000, 12345)
+    nnz2 = np.diff(f2.download()[0])
+    bt = 128
+    longest = [int(max(nnz2[a2[q:q + bt]].max(), nnz2[b2[q:q + bt]].max())) for q in range(0, len(a2), bt)]
+    clk_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0)) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 1965.0
+    floor_ms = 8.0 * sum(longest) / (clk_mhz * 1e3)
+    w0 = np.zeros(4096)
+    st2 = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        ctx.sgd_epoch(f2, a2, b2, y2, bt, 0.1, 1.0, w0)
+        st2.append(time.perf_counter() - t0)
+    sgd_ms = 1e3 * float(np.median(st2[1:]))
+    c2["sgd_epoch"] = {"ms": sgd_ms, "steps": len(longest), "floor_ms": floor_ms, "frac": floor_ms / sgd_ms,
+                       "bound": "latency",
+                       "floor_model": "sum over the %d steps of the step's longest score chain (%d entries) "
+                                      "x 8 cycles (DADD latency) at the max SM clock; the gradient folds and "
+                                      "barriers are not in the floor" % (len(longest), sum(longest)),
+                       "api": "pars_sgd_epoch (cluster kernel; host weights in/out)"}
+    f2.free()
     if have_ref:
         rd2 = R.synthesize(8192, 21)
         t0 = time.perf_counter()
