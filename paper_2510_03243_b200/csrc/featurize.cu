@@ -1268,7 +1268,7 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
     for (uint32_t j = 0; j < nb; ++j) mine += __popc(bm[j]);
     int tot;
     const uint32_t off = (uint32_t)warp_excl_scan((int)mine, lane, &tot);
-    long long sq = 0;
+    uint32_t sq = 0;  // sum of count^2 <= features^2 <= 32767^2: exact in 32 bits
     // exact: the prompt's own slot (fused: the warp's next ring slot), or
     // (long lists) the warp's arena
     const bool in_slot = kChain && (uint32_t)tot <= kSlotCap;
@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
         const uint32_t idx = b0 + __ffs(t) - 1;
         const int cnt = (int)c16[idx] - 0x8000;
         c16[idx] = 0x8000;
-        sq += (long long)cnt * cnt;
+        sq += (uint32_t)(cnt * cnt);
         if (kChain) {
           L[pos++] = (idx << 16) | (uint32_t)(cnt + 0x8000);
         } else {
@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
         }
       }
     }
-    const double inv = inv_norm(c, warp_sum_i64(sq));
+    const double inv = inv_norm(c, (long long)__reduce_add_sync(kFull, sq));
     if (FUSED) {
       if (!in_slot) {
         __syncwarp();
