@@ -268,6 +268,8 @@ def workload_lib():
         for name, res, args in (
                 ("pars_workload_synthesize", C.c_int,
                  [C.c_uint64, C.c_double, C.c_double, C.c_uint64, i64, C.c_uint64, vp]),
+                ("pars_workload_synthesize_pad", C.c_int,
+                 [C.c_uint64, C.c_double, C.c_double, C.c_uint64, i64, C.c_uint64, C.c_int, vp]),
                 ("pars_workload_count", i64, [vp]), ("pars_workload_text_bytes", i64, [vp]),
                 ("pars_workload_text", vp, [vp]), ("pars_workload_offsets", vp, [vp]),
                 ("pars_workload_output_len", vp, [vp]), ("pars_workload_prompt_len", vp, [vp]),
@@ -292,10 +294,12 @@ class Workload:
 
     @classmethod
     def synthesize(cls, n: int, seed: int, mu: float = 5.0, sigma: float = 1.2,
-                   pad_tokens: int = 0, pad_seed: int = 5) -> "Workload":
+                   pad_tokens: int = 0, pad_seed: int = 5, pad_words: str = "filler") -> "Workload":
+        """pad_words: "filler" (C4: " w<k>") or "random6" (the C4 hard variant)."""
         L = workload_lib()
         h = C.c_void_p()
-        rc = L.pars_workload_synthesize(n, mu, sigma, seed, pad_tokens, pad_seed, C.byref(h))
+        kind = {"filler": 0, "random6": 1}[pad_words]
+        rc = L.pars_workload_synthesize_pad(n, mu, sigma, seed, pad_tokens, pad_seed, kind, C.byref(h))
         if rc != 0:
             raise ParsError(rc, L.pars_workload_last_error().decode("utf-8", "replace"))
         cnt = L.pars_workload_count(h)

@@ -1032,6 +1032,12 @@ __host__ inline size_t lane_slot_bytes(int64_t n) {
 constexpr int kFuseH = PARS_FUSE_H;  // hashing warps per CTA
 constexpr int kFuseD = PARS_FUSE_D;  // ring slots per hashing warp
 constexpr int kFuseC = PARS_FUSE_C;  // chain warps (round-robin over 32-item rounds)
+// Ring slot capacity (entries): a prompt with more touched buckets is chained
+// by its hashing warp itself (one lane). 2,048 covers the C4 hard variant
+// (random 6-letter words: ~1,520 touched buckets, at most ~1,690); only the
+// entries written are touched, so the slot stride costs no L2 for short
+// lists (148 CTAs x 18 warps x 8 slots x 8 KB = 170 MB of scratch).
+constexpr uint32_t kRingCap = 2048;
 #ifndef PARS_FUSE_WSMEM
 #define PARS_FUSE_WSMEM 0
 #endif
@@ -1048,7 +1054,7 @@ __host__ inline size_t fused_cta_bytes(uint32_t dim) {
          (kFuseH + kFuseH * kFuseD) * sizeof(int) + 64;
 }
 __host__ inline size_t fused_ring_bytes(int64_t grid) {
-  return (size_t)grid * kFuseH * kFuseD * kSlotCap * 4;
+  return (size_t)grid * kFuseH * kFuseD * kRingCap * 4;
 }
 
 // Products of one 4-entry chunk (entries past the list's end give +0.0,
@@ -1098,7 +1104,7 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
       inv = f.inv;
       prompt = f.prompt;
     }
-    const uint4* L = reinterpret_cast<const uint4*>(ring + ((size_t)h * kFuseD + slot) * kSlotCap);
+    const uint4* L = reinterpret_cast<const uint4*>(ring + ((size_t)h * kFuseD + slot) * kRingCap);
     const int nq = m > 0 ? (m + 3) >> 2 : 0;
     // software pipeline as in chain_slots_thread_kernel; loads bypass L1 (the
     // slot was rewritten by another warp since this SM last read it)
@@ -1163,7 +1169,7 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
   FuseMeta* meta = reinterpret_cast<FuseMeta*>(sw32 + (kFuseWSmem ? 2 * c.dim : 0));
   volatile int* produced = reinterpret_cast<volatile int*>(meta + kFuseH * kFuseD);
   volatile int* free_gen = produced + kFuseH;  // [kFuseH][kFuseD]: generation allowed to write the slot
-  uint32_t* ring = a.slots + (size_t)blockIdx.x * kFuseH * kFuseD * kSlotCap;
+  uint32_t* ring = a.slots + (size_t)blockIdx.x * kFuseH * kFuseD * kRingCap;
   if (FUSED) {
     if (kFuseWSmem)
       for (uint32_t k = threadIdx.x; k < c.dim; k += blockDim.x) sw64s[k] = a.w64[k];
@@ -1271,10 +1277,10 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
     uint32_t sq = 0;  // sum of count^2 <= features^2 <= 32767^2: exact in 32 bits
     // exact: the prompt's own slot (fused: the warp's next ring slot), or
     // (long lists) the warp's arena
-    const bool in_slot = kChain && (uint32_t)tot <= kSlotCap;
+    const bool in_slot = kChain && (uint32_t)tot <= (FUSED ? kRingCap : kSlotCap);
     if (FUSED) wait_slot();
     uint32_t* L = !in_slot ? lists
-                  : FUSED  ? ring + ((size_t)warp * kFuseD + gen % kFuseD) * kSlotCap
+                  : FUSED  ? ring + ((size_t)warp * kFuseD + gen % kFuseD) * kRingCap
                            : a.slots + (size_t)(i - a.first) * kSlotCap;
     // pass 2: ascending entries (lane-major = bucket order); resets the table
     uint32_t pos = off;

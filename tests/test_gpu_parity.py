@@ -694,3 +694,18 @@ def test_priority_order_radix_sizes(ctx, n):
     want = np.lexsort((np.arange(n), tie, np.where(boosted == 1, 0.0, s), 1 - boosted.astype(np.int64)))
     assert (got == want).all()
 
+
+
+def test_c4_hard_variant_scores_bit_identical(ctx, oracle):
+    """SURVEY 8(d)'s hard C4 variant (prompts padded to 512 tokens with random
+    6-letter words: ~3.4 KB, ~1,520 touched buckets per prompt, every list
+    longer than the old 512-entry ring slot): exact scores bit-identical to
+    the oracle, fast scores within the fp32 tolerance."""
+    from paper_2510_03243_b200 import MODE_FAST, Extractor, Workload
+    wl = Workload.synthesize(3000, 31, pad_tokens=512, pad_seed=5, pad_words="random6")
+    w = np.random.default_rng(9).normal(size=4096) * 0.05
+    got = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w, 0.0)
+    want = oracle.score_batch(OEx.make(), wl.text, wl.offsets, w, 0.0, threads=os.cpu_count())
+    assert (got.view(np.uint64) == want.view(np.uint64)).all()
+    fast = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w, 0.0, mode=MODE_FAST)
+    assert np.abs(fast - want).max() < 1e-5 * np.abs(w).sum()

@@ -1,4 +1,4 @@
-"""A/B timing + exactness of the featurize kernels on C4-shaped prompts.
+"""A/B timing (argv: n_prompts [filler|random6]) + exactness of the featurize kernels on C4-shaped prompts.
 
 Runs in one process per kernel (PARS_FEAT_V1=1 selects the round-1 kernel):
   python tools/feat_ab.py [n_prompts]
@@ -22,7 +22,8 @@ from oracle.bind import Extractor as OEx  # noqa: E402
 from oracle.bind import Oracle  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
-wl = P.Workload.synthesize(n, 31, pad_tokens=512, pad_seed=5)
+pad_words = sys.argv[2] if len(sys.argv) > 2 else "filler"  # "random6": the C4 hard variant
+wl = P.Workload.synthesize(n, 31, pad_tokens=512, pad_seed=5, pad_words=pad_words)
 w = np.random.default_rng(1234).normal(size=4096) * 0.05
 ctx = P.Context(0)
 ex = P.Extractor.make()
@@ -34,7 +35,7 @@ d_s = torch.empty(n, dtype=torch.float64, device=dev)
 L = P.lib()
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)
-out = {"kernel": "v1" if os.environ.get("PARS_FEAT_V1") == "1" else ("lane-unfused" if os.environ.get("PARS_FEAT_UNFUSED") == "1" else "lane-fused"), "prompts": n}
+out = {"pad_words": pad_words, "bytes_per_prompt": float(wl.offsets[-1]) / n, "kernel": "v1" if os.environ.get("PARS_FEAT_V1") == "1" else ("lane-unfused" if os.environ.get("PARS_FEAT_UNFUSED") == "1" else "lane-fused"), "prompts": n}
 for mode, name in ((P.MODE_EXACT, "exact"), (P.MODE_FAST, "fast")):
     def run():
         rc = L.pars_dev_score_text(ctx.h, C.byref(ex), d_text.data_ptr(), d_offs.data_ptr(), n,

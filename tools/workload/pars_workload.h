@@ -22,6 +22,11 @@ typedef struct pars_workload pars_workload;
 
 int pars_workload_synthesize(uint64_t n, double mu, double sigma, uint64_t seed,
                              int64_t pad_tokens, uint64_t pad_seed, pars_workload** out);
+/* pad_kind 0: the C4 filler above; 1: the C4 hard variant of SURVEY §8(d),
+ * random 6-letter lowercase words (letters from Rng(pad_seed).below(26)). */
+int pars_workload_synthesize_pad(uint64_t n, double mu, double sigma, uint64_t seed,
+                                 int64_t pad_tokens, uint64_t pad_seed, int pad_kind,
+                                 pars_workload** out);
 int64_t pars_workload_count(const pars_workload* w);
 int64_t pars_workload_text_bytes(const pars_workload* w);
 /* Pointers stay valid until pars_workload_free. */

@@ -36,6 +36,11 @@ const char* pars_workload_last_error(void) { return g_err.c_str(); }
 
 int pars_workload_synthesize(uint64_t n, double mu, double sigma, uint64_t seed, int64_t pad_tokens,
                              uint64_t pad_seed, pars_workload** out) {
+  return pars_workload_synthesize_pad(n, mu, sigma, seed, pad_tokens, pad_seed, 0, out);
+}
+
+int pars_workload_synthesize_pad(uint64_t n, double mu, double sigma, uint64_t seed, int64_t pad_tokens,
+                                 uint64_t pad_seed, int pad_kind, pars_workload** out) {
   *out = nullptr;
   if (n < 1) {
     g_err = "synthesize: n must be >= 1";
@@ -91,12 +96,17 @@ int pars_workload_synthesize(uint64_t n, double mu, double sigma, uint64_t seed,
     w->prompt_len[i] = static_cast<int64_t>(tokens.size());
   }
   if (pad_tokens > 0) {  // " w<k>", k = Rng(pad_seed).below(50)
-    Rng pad(pad_seed);
+    Rng pad(pad_seed);     // (pad_kind 1, the hard variant: random 6-letter lowercase words)
     for (uint64_t i = 0; i < n; ++i) {
       std::string& text = texts[i];
       for (int64_t k = w->prompt_len[i]; k < pad_tokens; ++k) {
-        text += " w";
-        append_u64(text, pad.below(50));
+        if (pad_kind == 1) {
+          text += ' ';
+          for (int c = 0; c < 6; ++c) text += static_cast<char>('a' + pad.below(26));
+        } else {
+          text += " w";
+          append_u64(text, pad.below(50));
+        }
       }
       w->prompt_len[i] = std::max<int64_t>(w->prompt_len[i], pad_tokens);
     }
