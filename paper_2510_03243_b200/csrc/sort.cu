@@ -158,9 +158,15 @@ constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 
 
 // 512 threads x 14 keys = 7,168-key tiles, one CTA per SM: 1M keys are 140
 // tiles, one wave (a pass is latency-bound: two waves cost twice as much)
-constexpr int kSweepThreads = 512;
+#ifndef PARS_SWEEP_THREADS
+#define PARS_SWEEP_THREADS 512
+#endif
+constexpr int kSweepThreads = PARS_SWEEP_THREADS;
 constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr int kSweepItems = 14;
+#ifndef PARS_SWEEP_ITEMS
+#define PARS_SWEEP_ITEMS 14
+#endif
+constexpr int kSweepItems = PARS_SWEEP_ITEMS;
 constexpr int kSweepTile = kSweepThreads * kSweepItems;
 constexpr size_t kSweepSmem = (size_t)kSweepWarps * 256 * 4 /* wcnt */ + 256 * 4 * 2 /* gbase, tstart */ +
                               64 /* wsum, tile */ + (size_t)kSweepTile * (8 + 4 + 4);
