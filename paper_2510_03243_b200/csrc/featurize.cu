@@ -836,7 +836,7 @@ constexpr int kLaneTextCap = 2560;   // prompt bytes staged in shared memory per
 constexpr int kLaneBuf = kLaneTextCap + 64;  // + 16-byte alignment slack and space padding
 
 __host__ __device__ inline size_t lane_warp_bytes(uint32_t dim) {
-  return (size_t)dim * 2 + dim / 8 + 32 /* increment table */ + kLaneBuf;
+  return (size_t)dim * 2 + dim / 8 + 48 /* increment table + staging mbarrier */ + kLaneBuf;
 }
 // + (fast mode) the fp32 weights in shared memory: the walk gathers w[idx]
 // for every entry, and an L2 round trip per gather would serialise it
@@ -991,6 +991,47 @@ __device__ __forceinline__ int lane_stage(uint32_t buf, const uint8_t* text, int
   }
   asm volatile("cp.async.commit_group;");
   return lo;
+}
+
+// The same staging as one TMA bulk copy of the 16-byte-aligned chunks
+// covering the prompt (lane 0 issues it; completion on the warp's mbarrier),
+// when those chunks lie inside the launch's readable text; otherwise the
+// per-lane cp.async form above. Returns the prompt's offset in the buffer.
+__device__ __forceinline__ int lane_stage_bulk(uint32_t buf, const uint8_t* text, int64_t beg, int64_t end,
+                                               const uint8_t* rlo, const uint8_t* rhi, int lane,
+                                               uint64_t pol, uint32_t bar, bool& bulk) {
+  const uint8_t* p0 = text + beg;
+  const uint8_t* a0 = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p0) & ~(uintptr_t)15);
+  const int lo = (int)(p0 - a0);
+  const uint32_t nbytes = ((uint32_t)(lo + (end - beg)) + 15u) & ~15u;
+  bulk = a0 >= rlo && a0 + nbytes <= rhi && nbytes > 0;
+  if (!bulk) return lane_stage(buf, text, beg, end, rlo, rhi, lane, pol);
+  if (lane == 0) {
+    // the buffer's previous prompt was read through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(buf),
+        "l"(a0), "r"(nbytes), "r"(bar), "l"(pol)
+        : "memory");
+  }
+  return lo;
+}
+
+// Wait for a bulk-staged prompt (every lane waits on the phase) and pad it.
+__device__ __forceinline__ void lane_stage_finish_bulk(uint32_t buf, int lo, int hi, int lane, uint32_t bar,
+                                                       uint32_t& phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tLSTAGE_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra LSTAGE_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+  phase ^= 1u;
+  __syncwarp();
+  if (lane < lo) asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + lane), "r"(0x20u));
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(buf + hi + lane), "r"(0x20u));
+  __syncwarp();
 }
 
 // Wait for the staged prompt and pad it with spaces: [0, lo) and [hi, hi+32).
@@ -1207,8 +1248,15 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
   const uint32_t cbase = tb + (uint32_t)warp * tsz;
   const uint32_t bbase = tb + (uint32_t)nwc * tsz + (uint32_t)warp * (c.dim / 8);
   // increments by (ev bit, half, sign): 0 x4, then -1, +1, -1 << 16, +1 << 16
-  const uint32_t lut = tb + (uint32_t)nwc * (tsz + c.dim / 8) + (uint32_t)warp * 32u;
-  const uint32_t buf = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 32u) + (uint32_t)warp * kLaneBuf;
+  const uint32_t lut = tb + (uint32_t)nwc * (tsz + c.dim / 8) + (uint32_t)warp * 48u;
+  const uint32_t sbar = lut + 32u;  // the warp's staging mbarrier
+  const uint32_t buf = tb + (uint32_t)nwc * (tsz + c.dim / 8 + 48u) + (uint32_t)warp * kLaneBuf;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t sphase = 0;
+  bool st_bulk = false;
   if (lane < 8) {
     const uint32_t dv =
         lane < 4 ? 0u : ((lane & 1) ? 1u : 0xffffffffu) << ((lane & 2) ? 16 : 0);
@@ -1234,7 +1282,8 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
   int st_lo = -1;  // buffer offset of the staged prompt (-1: nothing staged)
   if (a.first + gw < a.n) {
     const int64_t beg = a.offsets[a.first + gw], len = a.offsets[a.first + gw + 1] - beg;
-    if (fits(beg, len)) st_lo = lane_stage(buf, a.text, beg, beg + len, text_lo, text_hi, lane, pol);
+    if (fits(beg, len))
+      st_lo = lane_stage_bulk(buf, a.text, beg, beg + len, text_lo, text_hi, lane, pol, sbar, st_bulk);
   }
   for (int64_t i = a.first + gw; i < a.n; i += nw) {
     const int64_t beg = a.offsets[i], len = a.offsets[i + 1] - beg;
@@ -1242,7 +1291,8 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
       if (lane == 0) a.long_list[atomicAdd(a.long_count, 1)] = (int32_t)i;
       st_lo = -1;
     } else if (st_lo >= 0) {
-      lane_stage_finish(buf, st_lo, st_lo + (int)len, lane);
+      if (st_bulk) lane_stage_finish_bulk(buf, st_lo, st_lo + (int)len, lane, sbar, sphase);
+      else lane_stage_finish(buf, st_lo, st_lo + (int)len, lane);
       hash_lane<true>(c, buf, nullptr, st_lo, st_lo + (int)len, 0, 0, lane, cbase, bbase, lut);
     } else if (len > 0) {
       const uint8_t* base = a.text + beg;
@@ -1260,7 +1310,8 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
     st_lo = -1;
     if (i + nw < a.n) {
       const int64_t nb2 = a.offsets[i + nw], nl = a.offsets[i + nw + 1] - nb2;
-      if (fits(nb2, nl)) st_lo = lane_stage(buf, a.text, nb2, nb2 + nl, text_lo, text_hi, lane, pol);
+      if (fits(nb2, nl))
+        st_lo = lane_stage_bulk(buf, a.text, nb2, nb2 + nl, text_lo, text_hi, lane, pol, sbar, st_bulk);
     }
     if (((len + 1) / 2) + len > kNarrowMaxFeatures) {
       if (FUSED) {
