@@ -20,7 +20,7 @@
 //                   (one warp per digit, global base from the all-digit
 //                   histogram); tie-rank digits are skipped when the ranks
 //                   are already non-decreasing in input order;
-//   radix_scatter   stable rank within the CTA via warp __match_any_sync +
+//   radix_scatter   stable rank within the CTA via warp ballots +
 //                   per-warp digit counters; the tile is laid out in digit
 //                   order in shared memory and written run by run (coalesced).
 #include <cuda_runtime.h>
@@ -74,7 +74,7 @@ __global__ void radix_init(const double* __restrict__ score, const uint8_t* __re
       // exponent, the high bytes of the ranks): aggregate them per warp so
       // the shared-memory atomics do not serialise
       if (p == 1 || p == 2 || p == 3 || p == 9 || p == 10 || p == 11) {
-        const unsigned peers = __match_any_sync(__activemask(), d);
+        const unsigned peers = __match_any_sync(__activemask(), d);  // (8 ballots measured slower here)
         if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&h[p * 256 + d], __popc(peers));
       } else {
         atomicAdd(&h[p * 256 + d], 1u);
@@ -233,7 +233,19 @@ __global__ void __launch_bounds__(kSweepThreads) radix_onesweep(
   for (int r = 0; r < kSweepItems; ++r) {
     const bool ok = sub + r * 32 + lane < n;
     const uint32_t d = ok ? digit_of(hi[r], lo[r], pos) : 256u;
+#ifndef PARS_SWEEP_MATCH_RANK
+    // the lanes holding the same digit, by 9 ballots (8 digit bits + the
+    // out-of-range sentinel bit): on this part MATCH.ANY is slower (1 M keys:
+    // 0.205 -> 0.191 ms per sort)
+    unsigned peers = kFull;
+#pragma unroll
+    for (int bit = 0; bit < 9; ++bit) {
+      const unsigned bb = __ballot_sync(kFull, (d >> bit) & 1u);
+      peers &= ((d >> bit) & 1u) ? bb : ~bb;
+    }
+#else
     const unsigned peers = __match_any_sync(kFull, d);
+#endif
     const uint32_t before = ok ? wcnt[warp][d] : 0u;
     dr[r] = (d << 16) | (before + __popc(peers & lt));
     __syncwarp();
