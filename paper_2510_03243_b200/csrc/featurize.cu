@@ -1079,6 +1079,9 @@ constexpr int kFuseC = PARS_FUSE_C;  // chain warps (round-robin over 32-item ro
 // entries written are touched, so the slot stride costs no L2 for short
 // lists (148 CTAs x 18 warps x 8 slots x 8 KB = 170 MB of scratch).
 constexpr uint32_t kRingCap = 2048;
+#ifndef PARS_FUSE_SPIN_NS
+#define PARS_FUSE_SPIN_NS 32  // back-off of a hashing warp waiting for its ring slot
+#endif
 #ifndef PARS_FUSE_WSMEM
 #define PARS_FUSE_WSMEM 0
 #endif
@@ -1227,7 +1230,7 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
   // fused: wait until the chain warp has released slot gen % kFuseD
   auto wait_slot = [&]() {
     if (lane == 0)
-      while (free_gen[warp * kFuseD + gen % kFuseD] != gen) __nanosleep(32);
+      while (free_gen[warp * kFuseD + gen % kFuseD] != gen) __nanosleep(PARS_FUSE_SPIN_NS);
     __syncwarp();
   };
   // fused: publish generation gen (its slot's entries written by the lanes)
