@@ -192,6 +192,42 @@ __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
     });
     __syncthreads();
   }
+  // Runs re-encoded as (bucket | length << 16, first entry) and, within each
+  // rank's range, put longest first (counting sort on min(length, 255)): the
+  // fold thread t takes runs t, t + 256, ... so the longest runs land on
+  // different threads and a thread's second run is a short one. The order of
+  // runs is free (each bucket's fold is independent).
+  {
+    uint2* tmp = reinterpret_cast<uint2*>(cur);  // cur + mask: dim uint2 >= runs
+    uint32_t* hist = part;                        // 256 bins
+    const uint32_t nr = nruns[q], total = (uint32_t)(ent_off[q + 1] - ent_off[q]);
+    for (uint32_t k = threadIdx.x; k < nr; k += kBuildThreads) {
+      const uint2 v = rq[k];
+      const uint32_t len = (k + 1 < nr ? rq[k + 1].y : total) - v.y;
+      tmp[k] = make_uint2(v.x | (len << 16), v.y);
+    }
+    __syncthreads();
+    for (int r = 0; r < kCL; ++r) {
+      const uint32_t r0 = rb[q * (kCL + 1) + r], r1 = rb[q * (kCL + 1) + r + 1];
+      if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+      __syncthreads();
+      for (uint32_t k = r0 + threadIdx.x; k < r1; k += kBuildThreads)
+        atomicAdd(&hist[255 - min(tmp[k].x >> 16, 255u)], 1u);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int b = 0; b < 256; ++b) {
+          const uint32_t c = hist[b];
+          hist[b] = acc;
+          acc += c;
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = r0 + threadIdx.x; k < r1; k += kBuildThreads)
+        rq[r0 + atomicAdd(&hist[255 - min(tmp[k].x >> 16, 255u)], 1u)] = tmp[k];
+      __syncthreads();
+    }
+  }
 }
 
 // Per epoch slot table: for slot g of the epoch (2 per pair, a then b):
@@ -609,8 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
     const uint2* runs_s = reinterpret_cast<const uint2*>(smw + (L.runbuf >> 2)) + (size_t)buf * L.runcap + d.rshift;
     for (uint32_t r = tid; r < d.nruns; r += kThreads) {
       const uint2 run = runs_staged ? runs_s[r] : d.runs[r];
-      const uint32_t e1 =
-          (r + 1 < d.nruns) ? (runs_staged ? runs_s[r + 1].y : d.runs[r + 1].y) : d.ent_end;
+      const uint32_t bucket = run.x & 0xffffu, e1 = run.y + (run.x >> 16);  // (bucket | len << 16, first)
       // g starts at +0.0 and is never -0.0 under round-to-nearest, so the
       // +-0.0 terms of inactive pairs leave it unchanged: branch-free fold
       double g = 0.0;
@@ -627,8 +662,8 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
         }
       }
       if (g != 0.0) {
-        const double nw = __dsub_rn(W[run.x], __dmul_rn(scale, g));
-        for (int rr = 0; rr < kCL; ++rr) cluster.map_shared_rank(W, rr)[run.x] = nw;
+        const double nw = __dsub_rn(W[bucket], __dmul_rn(scale, g));
+        for (int rr = 0; rr < kCL; ++rr) cluster.map_shared_rank(W, rr)[bucket] = nw;
       }
     }
     if (rank == 0 && tid == kThreads - 1) {
