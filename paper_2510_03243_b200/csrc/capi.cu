@@ -156,7 +156,7 @@ struct pars_features {
   // (val = count * inv exactly) — the compact form the SGD cluster kernel reads
   int32_t* d_cnt = nullptr;
   double* d_inv = nullptr;
-  uint32_t* d_cpk = nullptr;      // rows of (idx << 16 | count16), 4-entry aligned
+  uint32_t* d_cpk = nullptr;      // rows of (idx << 16 | count + 2^15), 4-entry aligned
   uint32_t* d_cpk_off = nullptr;  // row offsets into d_cpk (entries)
   std::vector<uint32_t> h_cpk_off;
   int cpk_state = 0;  // 0 not built, 1 built, -1 not representable
@@ -319,7 +319,7 @@ __global__ void csr_score_kernel(const int64_t* __restrict__ rp, const uint32_t*
   out[r] = __dadd_rn(s, bias);
 }
 
-// Same dot over the compact rows (idx << 16 | count16, 4-entry aligned):
+// Same dot over the compact rows (idx << 16 | count + 2^15, 4-entry aligned):
 // v = count * inv_row is recomputed with the very __dmul_rn that produced the
 // CSR value, so the products and the sequential sum are identical; 4 bytes
 // per entry instead of 12, read 16 bytes at a time.
@@ -339,10 +339,10 @@ __global__ void cpk_score_kernel(const int64_t* __restrict__ rp, const uint32_t*
     const uint32_t e[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      s = __dadd_rn(s, __dmul_rn(w[e[j] >> 16], __dmul_rn((double)(int16_t)(e[j] & 0xffffu), inv)));
+      s = __dadd_rn(s, __dmul_rn(w[e[j] >> 16], __dmul_rn((double)((int)(e[j] & 0xffffu) - 0x8000), inv)));
   }
   for (; k < len; ++k)
-    s = __dadd_rn(s, __dmul_rn(w[row[k] >> 16], __dmul_rn((double)(int16_t)(row[k] & 0xffffu), inv)));
+    s = __dadd_rn(s, __dmul_rn(w[row[k] >> 16], __dmul_rn((double)((int)(row[k] & 0xffffu) - 0x8000), inv)));
   out[r] = __dadd_rn(s, bias);
 }
 
@@ -423,12 +423,12 @@ __global__ void __launch_bounds__(kCpkRows) cpk_score_coop_kernel(
         const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          s = __dadd_rn(s, __dmul_rn(__ldg(w + (e[j] >> 16)), __dmul_rn((double)(int16_t)(e[j] & 0xffffu), inv)));
+          s = __dadd_rn(s, __dmul_rn(__ldg(w + (e[j] >> 16)), __dmul_rn((double)((int)(e[j] & 0xffffu) - 0x8000), inv)));
       }
     } else {
       for (int q = 0; q < n; ++q) {
         const uint32_t e = row[q];
-        s = __dadd_rn(s, __dmul_rn(__ldg(w + (e >> 16)), __dmul_rn((double)(int16_t)(e & 0xffffu), inv)));
+        s = __dadd_rn(s, __dmul_rn(__ldg(w + (e >> 16)), __dmul_rn((double)((int)(e & 0xffffu) - 0x8000), inv)));
       }
     }
     __syncthreads();  // the stage is refilled next iteration
@@ -1534,7 +1534,7 @@ extern "C" {
 namespace pars_b200 {
 namespace capi_detail {
 
-// Compact (idx << 16 | count16) rows for the cluster SGD kernel, built once
+// Compact (idx << 16 | count + 2^15) rows for the cluster SGD kernel, built once
 // per feature set; -1 when the features are not representable that way.
 int ensure_compact(pars_ctx* ctx, pars_features* f, cudaStream_t st) {
   if (f->cpk_state != 0) return PARS_OK;

@@ -6,7 +6,7 @@
 // of 8 CTAs (8 SMs) with the step's data staged in shared memory ahead of
 // time:
 //   * hashed features are kept in a compact form, one u32 per entry
-//     (idx << 16 | count16), since every value is exactly count * inv_row
+//     (idx << 16 | count + 2^15), since every value is exactly count * inv_row
 //     (features.cpp:113-120); v is rebuilt with __dmul_rn(count, inv), the
 //     very product the featurizer stored;
 //   * every CTA holds the full weight vector in shared memory; a CTA owns 1/8
@@ -59,13 +59,13 @@ __global__ void cpk_build_kernel(const int64_t* __restrict__ rp, const uint32_t*
     const uint32_t i = idx[b + k];
     const int32_t c = cnt[b + k];
     if (i > 0xffffu || c > 32767 || c < -32768) atomicExch(bad, 1);
-    out[k] = (i << 16) | ((uint32_t)c & 0xffffu);
+    out[k] = (i << 16) | ((uint32_t)(c + 0x8000) & 0xffffu);  // count biased by 2^15
   }
 }
 
 // ---- per-batch CSC, compact ---------------------------------------------
 // One CTA per batch: stable counting sort of the batch's (slot, idx, count)
-// entries by idx, slots in order. Entry = slot << 16 | count16. Runs are
+// entries by idx, slots in order. Entry = slot << 16 | count + 2^15. Runs are
 // (idx, first entry); rb[q][r] = first run of rank r's bucket range.
 __global__ void __launch_bounds__(kBuildThreads) csc_build_kernel(
     const int64_t* __restrict__ rp, const uint32_t* __restrict__ cpk,
@@ -252,7 +252,7 @@ __global__ void slot_table_kernel(const uint32_t* __restrict__ pa, const uint32_
 // (a slow conversion pipe on this part): the bits of 2^52 + (c + 2^15), less
 // 2^52 + 2^15, in one DADD.
 __device__ __forceinline__ double cnt_of(uint32_t E) {
-  const double biased = __hiloint2double(0x43300000, (int)((E + 0x8000u) & 0xffffu));
+  const double biased = __hiloint2double(0x43300000, (int)(E & 0xffffu));  // the stored count is biased
   return __dsub_rn(biased, 4503599627403264.0);  // 2^52 + 2^15
 }
 
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #pragma unroll 8
           for (; e < len; ++e) {
             const uint32_t E = row[e];
-            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)(int16_t)(E & 0xffffu), inv)));
+            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)((int)(E & 0xffffu) - 0x8000), inv)));
           }
         }
         score[k] = __dadd_rn(acc, a.bias);
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #pragma unroll 8
         for (; e < e1; ++e) {
           const uint32_t E = csc[e];
-          g = __dadd_rn(g, __dmul_rn((double)(int16_t)(E & 0xffffu), sinv[E >> 16]));
+          g = __dadd_rn(g, __dmul_rn((double)((int)(E & 0xffffu) - 0x8000), sinv[E >> 16]));
         }
       }
       if (g != 0.0) {
