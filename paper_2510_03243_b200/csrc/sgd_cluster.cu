@@ -38,7 +38,7 @@ namespace {
 constexpr int kCL = kSgdCluster;  // CTAs per cluster
 constexpr int kThreads = 256;
 #ifndef PARS_SGD_CHAIN_WARPS
-#define PARS_SGD_CHAIN_WARPS 2
+#define PARS_SGD_CHAIN_WARPS 3
 #endif
 constexpr int kChainWarps = PARS_SGD_CHAIN_WARPS;  // warps running the step's score chains
 constexpr int kChainThreads = kChainWarps * 32;
