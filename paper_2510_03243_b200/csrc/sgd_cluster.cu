@@ -36,7 +36,10 @@ namespace pars_b200 {
 namespace {
 
 constexpr int kCL = kSgdCluster;  // CTAs per cluster
-constexpr int kThreads = 256;
+#ifndef PARS_SGD_THREADS
+#define PARS_SGD_THREADS 256
+#endif
+constexpr int kThreads = PARS_SGD_THREADS;
 #ifndef PARS_SGD_CHAIN_WARPS
 #define PARS_SGD_CHAIN_WARPS 3
 #endif
