@@ -248,6 +248,10 @@ __global__ void csc_place(const int64_t* __restrict__ rp, const uint32_t* __rest
 
 __device__ __forceinline__ int64_t lower_row(const uint32_t* __restrict__ rows, int64_t lo,
                                              int64_t hi, int64_t r) {
+  // a task wholly above / below r (every task of a one-rank run, most of a
+  // shard's) needs no search
+  if (lo >= hi || (int64_t)rows[lo] >= r) return lo;
+  if ((int64_t)rows[hi - 1] < r) return hi;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
     if ((int64_t)rows[mid] < r)
