@@ -11,6 +11,7 @@ mkdir -p $OUT
 : > $OUT/summary.txt
 SEL_FEAT="exact_scores_bit_identical or sequential_lane_kernel_random_texts or fast_scores"
 SEL_SORT="priority_order_sizes or priority_order_large or merge_shard"
+SEL_CSR="features_score or score_records or dp_train or allpairs_matches"
 for tool in racecheck synccheck; do
   for grp in FEAT SORT; do
     sel=SEL_$grp
@@ -28,6 +29,11 @@ for tool in racecheck synccheck; do
     -m gpu -q -x -k "$SEL_FEAT" > $OUT/${tool}_FEAT_unfused.log 2>&1
   echo "$tool FEAT (unfused) rc=$?" >> $OUT/summary.txt
   tail -n 3 $OUT/${tool}_FEAT_unfused.log >> $OUT/summary.txt
+  # the staged CSR gather-dot (pars_dev_features_score) and the DP step around it
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests -m gpu -q -x \
+    -k "$SEL_CSR" > $OUT/${tool}_CSR.log 2>&1
+  echo "$tool CSR rc=$?" >> $OUT/summary.txt
+  tail -n 3 $OUT/${tool}_CSR.log >> $OUT/summary.txt
   # the cluster SGD epoch (csc_build_kernel + sgd_cluster_kernel) at a size
   # racecheck finishes: tools/san_sgd.py
   timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/san_sgd.py \
