@@ -1135,7 +1135,7 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
     const int64_t rem = a.n - a.first - ((int64_t)blockIdx.x * kFuseH + h);
     const bool valid = j < items && (int64_t)t * nw < rem;
     if (valid)
-      while (produced[h] <= t) __nanosleep(64);
+      while (atomicAdd(const_cast<int*>(&produced[h]), 0) <= t) __nanosleep(64);
     __syncwarp();
     __threadfence_block();
     int m = -1;
@@ -1144,9 +1144,13 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
     const int slot = t % kFuseD;
     if (valid) {
       const FuseMeta& f = meta[h * kFuseD + slot];
-      m = f.nnz;
-      inv = f.inv;
-      prompt = f.prompt;
+      // hand-off fields read as atomics (ordered by the fences around the
+      // sequence counters; atomic so the sanitizer sees no plain race)
+      FuseMeta& fm = const_cast<FuseMeta&>(f);
+      m = atomicAdd(&fm.nnz, 0);
+      inv = __longlong_as_double(
+          (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&fm.inv), 0ull));
+      prompt = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&fm.prompt), 0ull);
     }
     const uint4* L = reinterpret_cast<const uint4*>(ring + ((size_t)h * kFuseD + slot) * kRingCap);
     const int nq = m > 0 ? (m + 3) >> 2 : 0;
@@ -1180,7 +1184,7 @@ __device__ __forceinline__ void fused_chain_warp(const FeatConfig& c, const Feat
     if (m >= 0) a.scores[prompt] = __dadd_rn(s, a.bias);
     __threadfence_block();
     __syncwarp();
-    if (valid) free_gen[h * kFuseD + slot] = t + kFuseD;  // the slot's next writer
+    if (valid) atomicExch(const_cast<int*>(&free_gen[h * kFuseD + slot]), t + kFuseD);  // the slot's next writer
   }
 }
 
@@ -1230,7 +1234,8 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
   // fused: wait until the chain warp has released slot gen % kFuseD
   auto wait_slot = [&]() {
     if (lane == 0)
-      while (free_gen[warp * kFuseD + gen % kFuseD] != gen) __nanosleep(PARS_FUSE_SPIN_NS);
+      while (atomicAdd(const_cast<int*>(&free_gen[warp * kFuseD + gen % kFuseD]), 0) != gen)
+        __nanosleep(PARS_FUSE_SPIN_NS);
     __syncwarp();
   };
   // fused: publish generation gen (its slot's entries written by the lanes)
@@ -1239,11 +1244,11 @@ __global__ void __launch_bounds__(FUSED ? (kFuseH + kFuseC) * 32 : 576, 1)
     __syncwarp();
     if (lane == 0) {
       FuseMeta& f = meta[warp * kFuseD + gen % kFuseD];
-      f.inv = inv;
-      f.prompt = prompt;
-      f.nnz = nnz;
+      atomicExch(reinterpret_cast<unsigned long long*>(&f.inv), (unsigned long long)__double_as_longlong(inv));
+      atomicExch(reinterpret_cast<unsigned long long*>(&f.prompt), (unsigned long long)prompt);
+      atomicExch(&f.nnz, nnz);
       __threadfence_block();
-      produced[warp] = gen + 1;
+      atomicExch(const_cast<int*>(&produced[warp]), gen + 1);
     }
     __syncwarp();
     ++gen;
