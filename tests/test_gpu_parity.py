@@ -709,3 +709,33 @@ def test_c4_hard_variant_scores_bit_identical(ctx, oracle):
     assert (got.view(np.uint64) == want.view(np.uint64)).all()
     fast = ctx.score_text(Extractor.make(), wl.text, wl.offsets, w, 0.0, mode=MODE_FAST)
     assert np.abs(fast - want).max() < 1e-5 * np.abs(w).sum()
+
+
+def test_fused_ring_many_tiny_and_mixed_prompts(ctx, oracle):
+    """The fused kernel's ring hand-off under stress: 200,000 prompts that are
+    mostly empty or one token (hashing warps finish prompts far faster than
+    the chain warps consume rounds, so slots wrap many times), mixed with a
+    few ~1,700-bucket prompts (lists past the old 512-entry slot) and a few
+    too long for a slot (the hashing warp's own chain): every exact score
+    bit-identical to the oracle."""
+    from paper_2510_03243_b200 import Extractor, pack_texts
+    rng = np.random.default_rng(77)
+    words = [bytes(rng.integers(97, 123, size=rng.integers(1, 9)).astype(np.uint8)) for _ in range(5000)]
+    texts = []
+    for k in range(200_000):
+        r = rng.random()
+        if r < 0.3:
+            texts.append(b"")
+        elif r < 0.9:
+            texts.append(words[rng.integers(0, len(words))])
+        elif r < 0.999:
+            texts.append(b" ".join(words[j] for j in rng.integers(0, len(words), size=rng.integers(2, 60))))
+        elif r < 0.9995:
+            texts.append(b" ".join(bytes(rng.integers(97, 123, size=6).astype(np.uint8)) for _ in range(500)))
+        else:
+            texts.append(b" ".join(bytes(rng.integers(97, 123, size=6).astype(np.uint8)) for _ in range(1400)))
+    arena, offs = pack_texts(texts)
+    w = np.random.default_rng(5).normal(size=4096)
+    got = ctx.score_text(Extractor.make(), arena, offs, w, 0.5)
+    want = oracle.score_batch(OEx.make(), arena, offs, w, 0.5, threads=os.cpu_count())
+    assert (got.view(np.uint64) == want.view(np.uint64)).all()

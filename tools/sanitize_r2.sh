@@ -20,11 +20,9 @@ for tool in racecheck synccheck; do
     echo "$tool $grp rc=$?" >> $OUT/summary.txt
     tail -n 3 $OUT/${tool}_${grp}.log >> $OUT/summary.txt
   done
-  # the same featurize tests on the two-kernel (unfused) exact path: the
-  # fused kernel hands ring slots from hashing to chain warps with a
-  # release/acquire flag protocol (__threadfence_block + volatile sequence
-  # counters) that racecheck does not model, so its slot metadata shows up
-  # as hazards there; everything else (hashing, walk, chains) is the same code
+  # the same featurize tests on the two-kernel (unfused) exact path (the
+  # fused kernel's ring hand-off between hashing and chain warps uses
+  # shared-memory atomics ordered by fences; both paths are checked)
   PARS_FEAT_UNFUSED=1 timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_parity.py \
     -m gpu -q -x -k "$SEL_FEAT" > $OUT/${tool}_FEAT_unfused.log 2>&1
   echo "$tool FEAT (unfused) rc=$?" >> $OUT/summary.txt
