@@ -540,7 +540,7 @@ def run_ours(args):
                                            "rank 0 (pars_dev_merge_orders), inside the step"}
                           if world > 1 else {}), "extractor": "hashed word{1}+char{3}, D=4096, L2",
                        "l2_flush": "inputs larger than L2 (%.2f GB text per rank)" % (text_bytes / 1e9)},
-            "roofline": {"bound": "hbm", "kernel": "featurize_seq_kernel (fused tokenise+hash+histogram+L2+dot)",
+            "roofline": {"bound": "hbm", "kernel": "featurize_lane_kernel<exact, fused> (tokenise+hash+histogram+L2+dot)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_kind": peak_kind, "traffic": traffic, "issue_bound_evidence": issue,
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": feat_ms,
@@ -558,7 +558,7 @@ def run_ours(args):
                                                 "(LOP3+IMAD) mix, profiles/r2_int_issue.json"
                                                 if meas_issue else "spec issue rate",
                                    "spec_peak": spec_issue / 1e12}},
-            "sort": sort_roofline(n, sort_ms, hbm),
+            "sort": sort_roofline(n, sort_ms, hbm, got),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "prompts/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "pars_score_order (host buffers: score + SJF order in one call)"},
@@ -622,18 +622,30 @@ def timed_ms(torch, stream, world, fn, k):
     return barrier_max(world, a.elapsed_time(b)) / k
 
 
-def sort_roofline(n, sort_ms, hbm):
-    """The priority sort's HBM roofline: LSD radix traffic of the passes it
-    runs (8 B key + 4 B tie rank + 4 B index read and written per key per
-    pass; C4's burst tie ranks are already in input order, so only the score's
-    varying digit positions run) and, beside it, the one-pass I/O floor (read
-    score + tie rank, write the order)."""
+def sort_roofline(n, sort_ms, hbm, scores=None):
+    """The priority sort's HBM roofline: the one-pass I/O floor (read score +
+    tie rank, write the order) and, beside it, the LSD passes it actually runs
+    (one per score byte position where the keys differ; C4's burst tie ranks
+    are already in input order, so the 4 tie-rank positions are skipped), each
+    moving the 8 B key + 4 B index in and out (24 B per key)."""
     floor = n * (8 + 4 + 4)
-    return {"kernel": "radix sort (pars_dev_priority_order)", "ms": sort_ms, "bound": "hbm",
-            "floor_bytes": floor, "bytes_model": "one-pass I/O floor: 8 B score + 4 B tie rank "
-            "read, 4 B order written per key",
-            "achieved": floor / (sort_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": floor / (sort_ms / 1e3) / 1e9 / hbm}
+    out = {"kernel": "radix sort (pars_dev_priority_order)", "ms": sort_ms, "bound": "hbm",
+           "floor_bytes": floor, "bytes_model": "one-pass I/O floor: 8 B score + 4 B tie rank "
+           "read, 4 B order written per key",
+           "achieved": floor / (sort_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+           "frac": floor / (sort_ms / 1e3) / 1e9 / hbm}
+    if scores is not None and len(scores):
+        b = np.ascontiguousarray(scores, np.float64).view(np.uint64).copy()
+        b[(b << np.uint64(1)) == 0] = 0  # -0.0 == +0.0
+        neg = (b >> np.uint64(63)) == 1
+        key = np.where(neg, ~b, b | np.uint64(1 << 63))
+        passes = sum(int(np.unique((key >> np.uint64(8 * p)) & np.uint64(0xff)).size > 1) for p in range(8))
+        moved = passes * n * 24
+        out.update({"passes": passes, "pass_bytes": moved,
+                    "pass_model": "24 B per key per active pass (8 B key + 4 B index, read and written)",
+                    "pass_achieved": moved / (sort_ms / 1e3) / 1e9,
+                    "pass_frac": moved / (sort_ms / 1e3) / 1e9 / hbm})
+    return out
 
 
 def issue_peaks():
