@@ -1054,13 +1054,14 @@ __host__ inline size_t lane_slot_bytes(int64_t n) {
 
 // Exact mode, fused (default): the CTA is kFuseH hashing warps plus kFuseC
 // chain warps. A hashing warp walks each prompt's touched buckets in
-// ascending order into a ring slot (kFuseD slots per hashing warp, in global
-// memory that stays L2-resident: 148 x 16 x 8 x 2 KB = 38 MB, rewritten every
-// few microseconds) and publishes it through a shared-memory sequence
+// ascending order into a ring slot (kFuseD slots of kRingCap entries per
+// hashing warp, in global memory; for C4 the written part stays L2-resident:
+// 148 x 18 x 8 x ~1.2 KB) and publishes it through a shared-memory sequence
 // counter; the chain warp runs the sequential fp64 dots of 32 prompts at a
-// time, one per lane (two generations of every hashing warp), with the
-// weights in shared memory, and hands the slots back. The (idx, count) lists
-// never travel to DRAM and no second kernel runs.
+// time, one per lane, with the weights read through L1, and hands the slots
+// back. The counters and the slot metadata are shared-memory atomics
+// (ordered by __threadfence_block). The (idx, count) lists never travel to
+// DRAM and no second kernel runs.
 #ifndef PARS_FUSE_H
 #define PARS_FUSE_H 18
 #endif
