@@ -38,6 +38,9 @@ struct PairPlanDev {
   double* ss = nullptr;      // per call: sorted scores
   double* T = nullptr;       // per call: hinge thresholds
   int32_t* cs = nullptr;     // per call: coefficients in sorted order
+  double* srtS = nullptr;    // per call: each 256-tile's scores, sorted
+  double* srtT = nullptr;    // per call: each 256-tile's thresholds, sorted
+  int* nanflag = nullptr;    // per call: tile holds a NaN score / threshold
   unsigned long long kept = 0;
   bool monotone = true;  // g_j = L_j - dmin[L_j] non-decreasing (suffix masks valid)
 };
