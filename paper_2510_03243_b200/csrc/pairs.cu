@@ -49,9 +49,10 @@ __global__ void __launch_bounds__(kTile) allpairs_kernel(
   __shared__ unsigned long long redu[kTile / 32];
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long kept_acc = 0, act_acc = 0;
+  int64_t I = 0, J = 0;
+  if (t0 + blockIdx.x < t1) tile_of(t0 + blockIdx.x, nt, &I, &J);
   for (int64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    int64_t I, J;
-    tile_of(t, nt, &I, &J);
+    if (t != t0 + blockIdx.x) tile_advance(gridDim.x, nt, I, J);
     const int64_t gi = I * kTile + tid;
     const bool row_ok = gi < n;
     const double si = row_ok ? s[gi] : 0.0;
@@ -132,9 +133,10 @@ __global__ void __launch_bounds__(kTile) tau_kernel(const double* __restrict__ x
   __shared__ unsigned long long red[kTile / 32];
   const int tid = threadIdx.x;
   unsigned long long nc = 0, nd = 0, n1 = 0, n2 = 0;
+  int64_t I = 0, J = 0;
+  if (t0 + blockIdx.x < t1) tile_of(t0 + blockIdx.x, nt, &I, &J);
   for (int64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    int64_t I, J;
-    tile_of(t, nt, &I, &J);
+    if (t != t0 + blockIdx.x) tile_advance(gridDim.x, nt, I, J);
     const int64_t gi = I * kTile + tid;
     const bool row_ok = gi < n;
     const double xi = row_ok ? x[gi] : 0.0, yi = row_ok ? y[gi] : 0.0;

@@ -205,36 +205,45 @@ __global__ void __launch_bounds__(kT) allpairs_sorted_kernel(
   __shared__ int sC[kT];
   __shared__ double redd[kT / 32];
   __shared__ unsigned long long redu[kT / 32];
+  __shared__ int64_t sNext[2];  // the block's next tile, walked by thread 0
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long kept_acc = 0, act_acc = 0;
+  int64_t I = 0, J = 0;
+  if (t0 + blockIdx.x < t1) tile_of(t0 + blockIdx.x, nt, &I, &J);
   for (int64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    int64_t I, J;
-    tile_of(t, nt, &I, &J);
     const int64_t i = I * kT + tid, J0 = J * kT;
     const int64_t jn = min((int64_t)kT, n - J0);
     const bool row_ok = i < n;
     const double si = row_ok ? ss[i] : 0.0;
     const double Ti = row_ok ? T[i] : -CUDART_INF;
     const int64_t fi = row_ok ? (int64_t)f[i] : INT64_MAX;
-    sS[tid] = (tid < jn) ? ss[J0 + tid] : CUDART_NAN;
-    sC[tid] = 0;
     const int64_t fmin = f[I * kT];
     const int64_t fmax = f[min(n, (I + 1) * kT) - 1];
-    __syncthreads();
-    int cnt = 0;
     const bool diag = I == J;
-    if (diag) {
+    // fully kept and NaN-free: counts by rank in the tiles' sorted scores / thresholds
+    const bool ranked = !diag && fmax <= J0 && !nanflag[I] && !nanflag[J];
+    sS[tid] = (tid < jn) ? ss[J0 + tid] : CUDART_NAN;
+    if (ranked) {
+      sSs[tid] = srtS[J0 + tid];
+      sTs[tid] = srtT[I * kT + tid];
+    } else {
+      sC[tid] = 0;
+    }
+    __syncthreads();
+    if (tid == 0 && t + gridDim.x < t1) {
+      int64_t In = I, Jn = J;
+      tile_advance(gridDim.x, nt, In, Jn);
+      sNext[0] = In;
+      sNext[1] = Jn;
+    }
+    int cnt = 0;
+    if (ranked) {
+      cnt = row_ok ? rank_in<false>(sSs, Ti) : 0;
+      sC[tid] = kT - rank_in<true>(sTs, sS[tid]);  // (a padding column's count is never read)
+    } else if (diag) {
       tile_columns<2>(sS, Ti, fi, J0, tid, lane, cnt, sC);
     } else if (fmax <= J0) {
-      if (!nanflag[I] && !nanflag[J]) {  // fully kept: counts by rank
-        sSs[tid] = srtS[J0 + tid];
-        sTs[tid] = srtT[I * kT + tid];
-        __syncthreads();
-        cnt = row_ok ? rank_in<false>(sSs, Ti) : 0;
-        if (tid < jn) sC[tid] = kT - rank_in<true>(sTs, sS[tid]);
-      } else {
-        tile_columns<0>(sS, Ti, fi, J0, tid, lane, cnt, sC);
-      }
+      tile_columns<0>(sS, Ti, fi, J0, tid, lane, cnt, sC);
     } else if (fmin < J0 + jn) {
       tile_columns<1>(sS, Ti, fi, J0, tid, lane, cnt, sC);
     }
@@ -250,8 +259,12 @@ __global__ void __launch_bounds__(kT) allpairs_sorted_kernel(
       atomicSub(&cs[J0 + tid], sC[tid]);
       part = __dsub_rn(part, __dmul_rn((double)sC[tid], sS[tid]));
     }
-    const double tl = block_sum_fixed<double>(part, redd);
+    // no trailing barrier: red (and sNext) are next written after this
+    // loop's first barrier; block_sum's barrier publishes sNext
+    const double tl = block_sum_fixed<double, false>(part, redd);
     if (tid == 0) loss_part[t - t0] = tl;
+    I = sNext[0];
+    J = sNext[1];
   }
   const unsigned long long k = block_sum_fixed<unsigned long long>(kept_acc, redu);
   const unsigned long long a = block_sum_fixed<unsigned long long>(act_acc, redu);

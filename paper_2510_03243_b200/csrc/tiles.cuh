@@ -22,8 +22,18 @@ __device__ __forceinline__ void tile_of(int64_t t, int64_t nt, int64_t* I, int64
   *J = i + (t - start(i));
 }
 
+// Moves (I, J) forward by `step` tiles in the same enumeration (the target
+// must exist): a grid-stride walk pays tile_of's sqrt once per block.
+__device__ __forceinline__ void tile_advance(int64_t step, int64_t nt, int64_t& I, int64_t& J) {
+  J += step;
+  while (J >= nt) {  // spill into the next row, which starts at column I + 1
+    J -= nt - (I + 1);
+    ++I;
+  }
+}
+
 // Deterministic (fixed-order) block reduction; result valid in thread 0.
-template <typename T>
+template <typename T, bool TRAIL = true>
 __device__ __forceinline__ T block_sum_fixed(T v, T* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -33,7 +43,7 @@ __device__ __forceinline__ T block_sum_fixed(T v, T* red) {
   T r = 0;
   if (threadIdx.x == 0)
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[w];
-  __syncthreads();
+  if (TRAIL) __syncthreads();  // callers with another barrier before red's next use may skip it
   return r;
 }
 
