@@ -624,10 +624,14 @@ def timed_ms(torch, stream, world, fn, k):
 
 def sort_roofline(n, sort_ms, hbm, scores=None):
     """The priority sort's HBM roofline: the one-pass I/O floor (read score +
-    tie rank, write the order) and, beside it, the LSD passes it actually runs
-    (one per score byte position where the keys differ; C4's burst tie ranks
-    are already in input order, so the 4 tie-rank positions are skipped), each
-    moving the 8 B key + 4 B index in and out (24 B per key)."""
+    tie rank, write the order) and, beside it, the passes it actually runs.
+    LSD passes run per score byte position where the keys differ (C4's burst
+    tie ranks are already in input order, so the 4 tie-rank positions are
+    skipped), each moving the 8 B key + 4 B index in and out (24 B per key);
+    when two or more of the low four byte positions are active, the passes
+    over the top four run first and radix_fixup orders runs of equal top
+    words (16 B per key: key + index read, order written) — held if no run
+    is longer than 32 keys, else the full LSD passes run as well."""
     floor = n * (8 + 4 + 4)
     out = {"kernel": "radix sort (pars_dev_priority_order)", "ms": sort_ms, "bound": "hbm",
            "floor_bytes": floor, "bytes_model": "one-pass I/O floor: 8 B score + 4 B tie rank "
@@ -639,10 +643,17 @@ def sort_roofline(n, sort_ms, hbm, scores=None):
         b[(b << np.uint64(1)) == 0] = 0  # -0.0 == +0.0
         neg = (b >> np.uint64(63)) == 1
         key = np.where(neg, ~b, b | np.uint64(1 << 63))
-        passes = sum(int(np.unique((key >> np.uint64(8 * p)) & np.uint64(0xff)).size > 1) for p in range(8))
-        moved = passes * n * 24
-        out.update({"passes": passes, "pass_bytes": moved,
-                    "pass_model": "24 B per key per active pass (8 B key + 4 B index, read and written)",
+        act = [int(np.unique((key >> np.uint64(8 * p)) & np.uint64(0xff)).size > 1) for p in range(8)]
+        lo_act, hi_act = sum(act[:4]), sum(act[4:])
+        spec = hi_act > 0 and lo_act >= 2
+        longest = int(np.unique(key >> np.uint64(32), return_counts=True)[1].max()) if spec else 0
+        held = spec and longest <= 32
+        passes = hi_act if held else lo_act + hi_act + (hi_act if spec else 0)
+        moved = passes * n * 24 + (n * 16 if spec else 0)
+        out.update({"passes": passes, "high_word_speculation": spec, "fixup_held": held,
+                    "longest_top_word_run": longest, "pass_bytes": moved,
+                    "pass_model": "24 B per key per radix pass (8 B key + 4 B index, read and "
+                                  "written) + 16 B per key for the fixup when speculating",
                     "pass_achieved": moved / (sort_ms / 1e3) / 1e9,
                     "pass_frac": moved / (sort_ms / 1e3) / 1e9 / hbm})
     return out

@@ -23,6 +23,15 @@
 //   radix_scatter   stable rank within the CTA via warp ballots +
 //                   per-warp digit counters; the tile is laid out in digit
 //                   order in shared memory and written run by run (coalesced).
+//
+// Speculative high-word sort (when at least two of the low eight positions
+// are active): the passes over the key's top 32 bits run first (positions
+// 8..11, stable), then radix_fixup orders each run of equal top words by the
+// full key with one thread per element (rank = number of smaller keys in the
+// run). A run longer than kFixRun sets `redo`, and the full LSD sort — the
+// same passes as without speculation, launched behind a device-side gate —
+// runs instead. For scores spread over many binades the runs are a few keys
+// long and 4 passes replace 8 (12 with tie ranks).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,6 +48,16 @@ constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kTileKeys = kThreads * kItems;  // 2048
 constexpr unsigned kFull = 0xffffffffu;
+
+// Programmatic dependent launch: the sort's kernels after radix_init are
+// launched with programmatic stream serialisation, so each is dispatched
+// while its predecessor drains; it waits here (predecessor complete, its
+// writes visible) before touching any data, and releases its own successor
+// at once.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint64_t ordered_bits(double x) {
   uint64_t b = (uint64_t)__double_as_longlong(x);
@@ -98,12 +117,20 @@ __global__ void radix_init(const double* __restrict__ score, const uint8_t* __re
 struct PassPlan {
   int active, first, last, src, carry_lo, none;
 };
+// spec: the speculative high-word passes ran (fixup has work); src: the
+// ping-pong buffer holding their output; use_lo: the tie ranks order keys;
+// redo: run the full LSD passes (no speculation, or a run over kFixRun)
+struct FixPlan {
+  int spec, src, use_lo, redo;
+};
+constexpr int kFixRun = 32;
 
 __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ dh, int64_t n,
-                                                  PassPlan* __restrict__ plan,
-                                                  uint32_t* __restrict__ dbase) {
+                                                  PassPlan* __restrict__ plan, PassPlan* __restrict__ plan_hi,
+                                                  FixPlan* __restrict__ fix, uint32_t* __restrict__ dbase) {
   __shared__ int trivial[12];
   __shared__ int act[12];
+  pdl_enter();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const bool tie_sorted = dh[12 * 256] == 0u;
   if (t < 12) trivial[t] = 0;
@@ -146,7 +173,71 @@ __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ d
       plan[p] = q;
       cnt += act[p];
     }
+    int low = 0, high = 0, use_lo = 0;
+    for (int p = 0; p < 12; ++p) {
+      if (p < 8) low += act[p]; else high += act[p];
+      if (p < 4) use_lo |= act[p];
+    }
+    const int spec = high > 0 && low >= 2;
+    int k = 0;
+    for (int p = 0; p < 12; ++p) {
+      PassPlan q{};
+      q.active = spec && p >= 8 && act[p];
+      q.first = q.active && k == 0;
+      q.src = k & 1;
+      q.carry_lo = use_lo;
+      plan_hi[p] = q;  // never `last`: the keys go on to radix_fixup
+      k += q.active;
+    }
+    FixPlan f;
+    f.spec = spec;
+    f.src = k & 1;  // after k passes the keys sit in buffer k & 1
+    f.use_lo = use_lo;
+    f.redo = !spec;
+    *fix = f;
   }
+}
+
+// One thread per element of the high-word order: its run of equal top
+// words (bounded scans both ways), and its place in the run by counting the
+// run's smaller full keys (hi, tie if it orders, index) — every key is
+// distinct, so the places are a permutation of the run.
+__global__ void __launch_bounds__(256) radix_fixup(const uint64_t* __restrict__ khi0,
+                                                   const uint64_t* __restrict__ khi1,
+                                                   const uint32_t* __restrict__ klo0,
+                                                   const uint32_t* __restrict__ klo1,
+                                                   const uint32_t* __restrict__ val0,
+                                                   const uint32_t* __restrict__ val1, int64_t n,
+                                                   FixPlan* __restrict__ fix, uint32_t* __restrict__ order) {
+  pdl_enter();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!fix->spec || k >= n) return;
+  const int src = fix->src;
+  const uint64_t* kh = src ? khi1 : khi0;
+  const uint32_t* kl = src ? klo1 : klo0;
+  const uint32_t* kv = src ? val1 : val0;
+  const uint64_t h = kh[k];
+  const uint32_t top = (uint32_t)(h >> 32), v = kv[k];
+  int64_t a = k, b = k + 1;
+  while (a > 0 && k - a < kFixRun && (uint32_t)(kh[a - 1] >> 32) == top) --a;
+  while (b < n && b - k <= kFixRun && (uint32_t)(kh[b] >> 32) == top) ++b;
+  if (b - a > kFixRun) {
+    atomicExch(&fix->redo, 1);
+    return;
+  }
+  if (b - a == 1) {
+    order[k] = v;
+    return;
+  }
+  const bool use_lo = fix->use_lo;
+  const uint32_t l = use_lo ? kl[k] : 0u;
+  int64_t r = a;
+  for (int64_t j = a; j < b; ++j) {
+    const uint64_t hj = kh[j];
+    const uint32_t lj = use_lo ? kl[j] : 0u, vj = kv[j];
+    r += hj < h || (hj == h && (lj < l || (lj == l && vj < v)));
+  }
+  order[r] = v;
 }
 
 // One onesweep LSD pass: dynamic tile ids (launch order), per-tile digit
@@ -181,7 +272,10 @@ __global__ void __launch_bounds__(kSweepThreads) radix_onesweep(
     uint32_t* __restrict__ klo0, uint32_t* __restrict__ klo1, uint32_t* __restrict__ val0,
     uint32_t* __restrict__ val1, uint32_t* __restrict__ order, int64_t n, int pos,
     const PassPlan* __restrict__ plans, const uint32_t* __restrict__ dbase,
-    unsigned long long* __restrict__ status, unsigned* __restrict__ tile_ctr) {
+    unsigned long long* __restrict__ status, unsigned* __restrict__ tile_ctr,
+    const FixPlan* __restrict__ gate) {
+  pdl_enter();
+  if (gate && !gate->redo) return;  // the speculative high-word sort held
   const PassPlan pl = plans[pos];
   if (!pl.active) {
     if (pos == 11 && pl.none)  // every key equal: the stable order is the input order
@@ -486,10 +580,28 @@ size_t sort_scratch_bytes(int64_t n) {
   const int64_t nb = ceil_div(std::max<int64_t>(n, 1), kSweepTile);
   size_t b = 0;
   b += 2 * ((size_t)n * 8 + 256) + 2 * ((size_t)n * 4 + 256) * 2;  // khi, klo, val ping-pong
-  b += (size_t)nb * 256 * 8 * 12 + 256;                            // look-back status per pass
-  b += 12 * 256 * 4 * 2 + 1024 + 12 * sizeof(PassPlan) + 64 * 4;  // histograms, bases, plan, tile ids
+  b += (size_t)nb * 256 * 8 * 16 + 256;                            // look-back status per pass (4 + 12)
+  b += 12 * 256 * 4 * 2 + 1024 + 24 * sizeof(PassPlan) + 256 + 64 * 4;  // histograms, bases, plans, tile ids
   return b + 4096;
 }
+
+namespace {
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+}  // namespace
 
 int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boosted,
                          const uint32_t* tie, int64_t n, uint32_t* order, void* scratch,
@@ -522,7 +634,7 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   uint32_t* klo[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
   uint32_t* val[2] = {(uint32_t*)take(n * 4), (uint32_t*)take(n * 4)};
   // zeroed together: status words, tile counters, histograms + tie flag
-  const size_t status_bytes = (size_t)nb * 256 * 8 * 12;
+  const size_t status_bytes = (size_t)nb * 256 * 8 * 16;  // 4 high-word passes + 12
   char* zero0 = p;
   auto* status = (unsigned long long*)take(status_bytes);
   auto* tile_ctr = (unsigned*)take(64 * 4);
@@ -530,6 +642,8 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   const size_t zero_bytes = (size_t)(p - zero0);
   auto* dbase = (uint32_t*)take(12 * 256 * 4);
   auto* plan = (PassPlan*)take(12 * sizeof(PassPlan));
+  auto* plan_hi = (PassPlan*)take(12 * sizeof(PassPlan));
+  auto* fix = (FixPlan*)take(sizeof(FixPlan));
   PARS_CUDA_CHECK(cudaMemsetAsync(zero0, 0, zero_bytes, st));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -544,14 +658,24 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
     set_error("priority order: cannot configure the sort kernel's shared memory");
     return PARS_ERR_CUDA;
   }
-  radix_plan<<<1, 256, 0, st>>>(dh, n, plan, dbase);
+  PARS_CUDA_CHECK(launch_pdl(radix_plan, 1, 256, 0, st, dh, n, plan, plan_hi, fix, dbase));
   count_launch(ctx, 2);
-  // without tie ranks the tie digits are all zero: those passes are known
-  // trivial on the host and not launched at all
+  const FixPlan* no_gate = nullptr;
+  for (int pos = 8; pos < 12; ++pos) {  // speculative: the top 32 bits only
+    PARS_CUDA_CHECK(launch_pdl(radix_onesweep, (unsigned)nb, kSweepThreads, kSweepSmem, st, score, boosted, tie,
+                               khi[0], khi[1], klo[0], klo[1], val[0], val[1], order, n, pos, plan_hi, dbase,
+                               status + (size_t)nb * 256 * (pos - 8), tile_ctr + pos, no_gate));
+    count_launch(ctx);
+  }
+  PARS_CUDA_CHECK(launch_pdl(radix_fixup, (unsigned)ceil_div(n, 256), 256, 0, st, khi[0], khi[1], klo[0], klo[1],
+                             val[0], val[1], n, fix, order));
+  count_launch(ctx);
+  // the full LSD sort, gated on fix->redo; without tie ranks the tie digits
+  // are all zero: those passes are known trivial on the host and not launched
   for (int pos = tie ? 0 : 4; pos < 12; ++pos) {
-    radix_onesweep<<<nb, kSweepThreads, kSweepSmem, st>>>(score, boosted, tie, khi[0], khi[1], klo[0], klo[1], val[0],
-                                            val[1], order, n, pos, plan, dbase,
-                                            status + (size_t)nb * 256 * pos, tile_ctr + pos);
+    PARS_CUDA_CHECK(launch_pdl(radix_onesweep, (unsigned)nb, kSweepThreads, kSweepSmem, st, score, boosted, tie,
+                               khi[0], khi[1], klo[0], klo[1], val[0], val[1], order, n, pos, plan, dbase,
+                               status + (size_t)nb * 256 * (4 + pos), tile_ctr + 16 + pos, (const FixPlan*)fix));
     count_launch(ctx);
   }
   PARS_CUDA_CHECK(cudaGetLastError());

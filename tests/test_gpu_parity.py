@@ -695,6 +695,29 @@ def test_priority_order_radix_sizes(ctx, n):
     assert (got == want).all()
 
 
+@pytest.mark.parametrize("run", [1, 2, 31, 32, 33, 200])
+@pytest.mark.parametrize("ties", [True, False])
+def test_priority_order_high_word_runs(ctx, run, ties):
+    """The speculative high-word sort (sort.cu radix_fixup): keys whose top
+    32 bits repeat in shuffled runs of `run` keys with distinct or equal low
+    words, a few boosted keys (one run of top word 0), tie ranks that order
+    equal scores. Runs up to kFixRun = 32 are placed by the fixup, longer
+    ones make the full LSD passes run; both against numpy's lexsort."""
+    n = 150_000
+    rng = np.random.default_rng(100 + run)
+    nb = n // run + 1
+    top = (rng.normal(size=nb) * 10).view(np.uint64) & np.uint64(0xFFFFFFFF00000000)
+    low = rng.integers(0, 2**32, size=(nb, run), dtype=np.uint64)
+    low[:, 0] = low[:, -1]  # equal full scores inside a run
+    score = (top[:, None] | low).reshape(-1)[:n].view(np.float64)[rng.permutation(n)]
+    tie = rng.integers(0, 3, size=n) if ties else np.zeros(n)  # all-zero ranks: no tie passes
+    tie = tie.astype(np.uint32)
+    boosted = (rng.random(n) < 1e-4).astype(np.uint8)
+    got = ctx.priority_order(score, tie, boosted)
+    want = np.lexsort((np.arange(n), tie, np.where(boosted == 1, 0.0, score), 1 - boosted.astype(np.int64)))
+    assert (got == want).all()
+
+
 
 def test_c4_hard_variant_scores_bit_identical(ctx, oracle):
     """SURVEY 8(d)'s hard C4 variant (prompts padded to 512 tokens with random
