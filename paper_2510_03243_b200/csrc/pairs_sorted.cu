@@ -195,6 +195,15 @@ __device__ __forceinline__ void tile_columns(const double* sS, double Ti, int64_
   }
 }
 
+// Tiles are taken in chunks of kChunk consecutive tiles of the enumeration
+// (row tile I, columns J, J + 1, ...): the row side — scores, thresholds,
+// first kept columns, the row tile's sorted thresholds — is loaded once per
+// row of the chunk, and each row's count goes to cs once per row of the
+// chunk. Per tile: its columns, the counts, the column atomics and the
+// tile's loss part (one per tile, as before: the fixed-order sum is
+// independent of the chunking).
+constexpr int kChunk = 4;
+
 __global__ void __launch_bounds__(kT) allpairs_sorted_kernel(
     const double* __restrict__ ss, const double* __restrict__ T, const int32_t* __restrict__ f,
     int64_t n, int64_t nt, double m, int64_t t0, int64_t t1, int32_t* __restrict__ cs,
@@ -205,66 +214,75 @@ __global__ void __launch_bounds__(kT) allpairs_sorted_kernel(
   __shared__ int sC[kT];
   __shared__ double redd[kT / 32];
   __shared__ unsigned long long redu[kT / 32];
-  __shared__ int64_t sNext[2];  // the block's next tile, walked by thread 0
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long kept_acc = 0, act_acc = 0;
-  int64_t I = 0, J = 0;
-  if (t0 + blockIdx.x < t1) tile_of(t0 + blockIdx.x, nt, &I, &J);
-  for (int64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    const int64_t i = I * kT + tid, J0 = J * kT;
-    const int64_t jn = min((int64_t)kT, n - J0);
-    const bool row_ok = i < n;
-    const double si = row_ok ? ss[i] : 0.0;
-    const double Ti = row_ok ? T[i] : -CUDART_INF;
-    const int64_t fi = row_ok ? (int64_t)f[i] : INT64_MAX;
-    const int64_t fmin = f[I * kT];
-    const int64_t fmax = f[min(n, (I + 1) * kT) - 1];
-    const bool diag = I == J;
-    // fully kept and NaN-free: counts by rank in the tiles' sorted scores / thresholds
-    const bool ranked = !diag && fmax <= J0 && !nanflag[I] && !nanflag[J];
-    sS[tid] = (tid < jn) ? ss[J0 + tid] : CUDART_NAN;
-    if (ranked) {
-      sSs[tid] = srtS[J0 + tid];
-      sTs[tid] = srtT[I * kT + tid];
-    } else {
-      sC[tid] = 0;
+  const int64_t nchunks = (t1 - t0 + kChunk - 1) / kChunk;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t tA = t0 + c * kChunk, tB = min(t1, tA + kChunk);
+    int64_t I, J;
+    tile_of(tA, nt, &I, &J);
+    int64_t i = 0, fi = 0, fmin = 0, fmax = 0;
+    bool row_ok = false, nanI = false;
+    double si = 0.0, Ti = 0.0;
+    int rowcnt = 0;
+    for (int64_t t = tA; t < tB; ++t, ++J) {
+      if (J == nt || t == tA) {  // a new row tile: flush the last one's counts, load its row side
+        if (t != tA) {
+          if (row_ok && rowcnt) atomicAdd(&cs[i], rowcnt);
+          rowcnt = 0;
+          ++I;
+          J = I;
+        }
+        i = I * kT + tid;
+        row_ok = i < n;
+        si = row_ok ? ss[i] : 0.0;
+        Ti = row_ok ? T[i] : -CUDART_INF;
+        fi = row_ok ? (int64_t)f[i] : INT64_MAX;
+        fmin = f[I * kT];
+        fmax = f[min(n, (I + 1) * kT) - 1];
+        nanI = nanflag[I] != 0;
+        sTs[tid] = srtT[I * kT + tid];  // (read only after this tile's first barrier)
+      }
+      const int64_t J0 = J * kT;
+      const int64_t jn = min((int64_t)kT, n - J0);
+      const bool diag = I == J;
+      // fully kept and NaN-free: counts by rank in the tiles' sorted scores / thresholds
+      const bool ranked = !diag && fmax <= J0 && !nanI && !nanflag[J];
+      sS[tid] = (tid < jn) ? ss[J0 + tid] : CUDART_NAN;
+      if (ranked)
+        sSs[tid] = srtS[J0 + tid];
+      else
+        sC[tid] = 0;
+      __syncthreads();
+      int cnt = 0;
+      if (ranked) {
+        cnt = row_ok ? rank_in<false>(sSs, Ti) : 0;
+        sC[tid] = kT - rank_in<true>(sTs, sS[tid]);  // (a padding column's count is never read)
+      } else if (diag) {
+        tile_columns<2>(sS, Ti, fi, J0, tid, lane, cnt, sC);
+      } else if (fmax <= J0) {
+        tile_columns<0>(sS, Ti, fi, J0, tid, lane, cnt, sC);
+      } else if (fmin < J0 + jn) {
+        tile_columns<1>(sS, Ti, fi, J0, tid, lane, cnt, sC);
+      }
+      __syncthreads();
+      if (row_ok) {
+        const int64_t from = max(max(fi, J0), diag ? i + 1 : (int64_t)0);
+        kept_acc += (unsigned long long)max((int64_t)0, J0 + jn - from);
+        act_acc += (unsigned)cnt;
+        rowcnt += cnt;
+      }
+      double part = cnt ? __dmul_rn((double)cnt, __dadd_rn(si, m)) : 0.0;
+      if (tid < jn && sC[tid]) {
+        atomicSub(&cs[J0 + tid], sC[tid]);
+        part = __dsub_rn(part, __dmul_rn((double)sC[tid], sS[tid]));
+      }
+      // no trailing barrier: red, sS, sSs, sTs and sC are next written
+      // before a barrier that every thread reaches after this one
+      const double tl = block_sum_fixed<double, false>(part, redd);
+      if (tid == 0) loss_part[t - t0] = tl;
     }
-    __syncthreads();
-    if (tid == 0 && t + gridDim.x < t1) {
-      int64_t In = I, Jn = J;
-      tile_advance(gridDim.x, nt, In, Jn);
-      sNext[0] = In;
-      sNext[1] = Jn;
-    }
-    int cnt = 0;
-    if (ranked) {
-      cnt = row_ok ? rank_in<false>(sSs, Ti) : 0;
-      sC[tid] = kT - rank_in<true>(sTs, sS[tid]);  // (a padding column's count is never read)
-    } else if (diag) {
-      tile_columns<2>(sS, Ti, fi, J0, tid, lane, cnt, sC);
-    } else if (fmax <= J0) {
-      tile_columns<0>(sS, Ti, fi, J0, tid, lane, cnt, sC);
-    } else if (fmin < J0 + jn) {
-      tile_columns<1>(sS, Ti, fi, J0, tid, lane, cnt, sC);
-    }
-    __syncthreads();
-    if (row_ok) {
-      const int64_t from = max(max(fi, J0), diag ? i + 1 : (int64_t)0);
-      kept_acc += (unsigned long long)max((int64_t)0, J0 + jn - from);
-      act_acc += (unsigned)cnt;
-      if (cnt) atomicAdd(&cs[i], cnt);
-    }
-    double part = cnt ? __dmul_rn((double)cnt, __dadd_rn(si, m)) : 0.0;
-    if (tid < jn && sC[tid]) {
-      atomicSub(&cs[J0 + tid], sC[tid]);
-      part = __dsub_rn(part, __dmul_rn((double)sC[tid], sS[tid]));
-    }
-    // no trailing barrier: red (and sNext) are next written after this
-    // loop's first barrier; block_sum's barrier publishes sNext
-    const double tl = block_sum_fixed<double, false>(part, redd);
-    if (tid == 0) loss_part[t - t0] = tl;
-    I = sNext[0];
-    J = sNext[1];
+    if (row_ok && rowcnt) atomicAdd(&cs[i], rowcnt);
   }
   const unsigned long long k = block_sum_fixed<unsigned long long>(kept_acc, redu);
   const unsigned long long a = block_sum_fixed<unsigned long long>(act_acc, redu);
@@ -355,7 +373,12 @@ int launch_allpairs_sorted(pars_ctx* ctx, const PairPlanDev& p, const double* d_
   prep_kernel<<<blocks, 256, 0, st>>>(p.perm, d_scores, n, margin, p.ss, p.T, p.cs);
   const int64_t nt = ceil_div(n, kT);
   tile_sort_kernel<<<(unsigned)nt, kT, 0, st>>>(p.ss, p.T, n, p.srtS, p.srtT, p.nanflag);
-  const int64_t grid = std::min<int64_t>(t1 - t0, (int64_t)sm_count() * 8);
+  static const int per_sm = [] {  // resident CTAs per SM: one wave of chunk walkers
+    int k = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, allpairs_sorted_kernel, kT, 0);
+    return std::max(k, 1);
+  }();
+  const int64_t grid = std::min<int64_t>(ceil_div(t1 - t0, kChunk), (int64_t)sm_count() * per_sm);
   allpairs_sorted_kernel<<<(unsigned)grid, kT, 0, st>>>(p.ss, p.T, p.f, n, nt, margin, t0, t1,
                                                         p.cs, d_counters, d_loss_part, p.srtS, p.srtT,
                                                         p.nanflag);
