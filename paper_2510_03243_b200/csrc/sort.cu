@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ d
                                                   FixPlan* __restrict__ fix, uint32_t* __restrict__ dbase) {
   __shared__ int trivial[12];
   __shared__ int act[12];
+  __shared__ int plow;
+  __shared__ unsigned long long sqw[8];
   pdl_enter();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const bool tie_sorted = dh[12 * 256] == 0u;
@@ -139,6 +141,23 @@ __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ d
     if (dh[k] == (uint32_t)n) trivial[k >> 8] = 1;
   __syncthreads();
   if (t < 12) act[t] = !trivial[t] && !(t < 4 && tie_sorted);
+  __syncthreads();
+  if (t == 0) {
+    plow = -1;
+    for (int p = 7; p >= 4; --p)
+      if (act[p]) plow = p;
+  }
+  __syncthreads();
+  // duplication probe for the speculation below: the sum of squared digit
+  // counts at the lowest active score byte (n distinct, evenly spread low
+  // bytes give a variance-to-mean ratio near 1; keys repeated r times, ~r)
+  {
+    const unsigned long long c = plow >= 0 ? dh[plow * 256 + t] : 0u;
+    unsigned long long v = c * c;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+    if (lane == 0) sqw[warp] = v;
+  }
   // exclusive bases of every position, warp w scanning positions w, w+8
   for (int p = warp; p < 12; p += 8) {
     uint32_t base = 0;
@@ -178,7 +197,14 @@ __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ d
       if (p < 8) low += act[p]; else high += act[p];
       if (p < 4) use_lo |= act[p];
     }
-    const int spec = high > 0 && low >= 2;
+    // speculate when it saves passes and the keys do not look repetitive
+    // (a wrong guess costs the 4 high-word passes; the result is exact
+    // either way)
+    const double mean = (double)n / 256.0;
+    unsigned long long sq = 0;
+    for (int w = 0; w < 8; ++w) sq += sqw[w];
+    const double ratio = plow >= 0 ? ((double)sq / 256.0 - mean * mean) / mean : 0.0;
+    const int spec = high > 0 && low >= 2 && ratio < 8.0;
     int k = 0;
     for (int p = 0; p < 12; ++p) {
       PassPlan q{};
@@ -210,21 +236,29 @@ __global__ void __launch_bounds__(256) radix_fixup(const uint64_t* __restrict__ 
                                                    const uint32_t* __restrict__ val1, int64_t n,
                                                    FixPlan* __restrict__ fix, uint32_t* __restrict__ order) {
   pdl_enter();
+  if (!fix->spec) return;  // (uniform)
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!fix->spec || k >= n) return;
   const int src = fix->src;
   const uint64_t* kh = src ? khi1 : khi0;
   const uint32_t* kl = src ? klo1 : klo0;
   const uint32_t* kv = src ? val1 : val0;
-  const uint64_t h = kh[k];
-  const uint32_t top = (uint32_t)(h >> 32), v = kv[k];
-  int64_t a = k, b = k + 1;
-  while (a > 0 && k - a < kFixRun && (uint32_t)(kh[a - 1] >> 32) == top) --a;
-  while (b < n && b - k <= kFixRun && (uint32_t)(kh[b] >> 32) == top) ++b;
-  if (b - a > kFixRun) {
-    atomicExch(&fix->redo, 1);
+  const bool valid = k < n;
+  const uint64_t h = valid ? kh[k] : 0ull;
+  const uint32_t top = (uint32_t)(h >> 32);
+  // the keys are in top-word order, so k's run is longer than kFixRun iff
+  // the key kFixRun places before or after k has the same top word: two
+  // loads decide it, and no thread scans a long run
+  const bool long_run = valid && ((k >= kFixRun && (uint32_t)(kh[k - kFixRun] >> 32) == top) ||
+                                  (k + kFixRun < n && (uint32_t)(kh[k + kFixRun] >> 32) == top));
+  if (__syncthreads_or(long_run)) {
+    if (threadIdx.x == 0) atomicExch(&fix->redo, 1);
     return;
   }
+  if (!valid) return;
+  const uint32_t v = kv[k];
+  int64_t a = k, b = k + 1;  // the run, at most kFixRun keys
+  while (a > 0 && (uint32_t)(kh[a - 1] >> 32) == top) --a;
+  while (b < n && (uint32_t)(kh[b] >> 32) == top) ++b;
   if (b - a == 1) {
     order[k] = v;
     return;
