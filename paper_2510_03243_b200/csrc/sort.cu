@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -124,6 +125,14 @@ struct FixPlan {
   int spec, src, use_lo, redo;
 };
 constexpr int kFixRun = 32;
+// Speculation from this many keys (PARS_SORT_SPEC_MIN overrides at run
+// time). Measured (tools/sort_ab.py, burst tie ranks, stream timing): with /
+// without speculation 0.077 / 0.117 ms at 8,192 keys, 0.086 / 0.133 at 131 k,
+// 0.122 / 0.169 at 1 M — it pays at every size the radix path serves.
+#ifndef PARS_SORT_SPEC_MIN
+#define PARS_SORT_SPEC_MIN 0
+#endif
+constexpr int64_t kSpecMin = PARS_SORT_SPEC_MIN;
 
 __global__ void __launch_bounds__(256) radix_plan(const uint32_t* __restrict__ dh, int64_t n,
                                                   PassPlan* __restrict__ plan, PassPlan* __restrict__ plan_hi,
@@ -695,21 +704,30 @@ int launch_priority_sort(pars_ctx* ctx, const double* score, const uint8_t* boos
   PARS_CUDA_CHECK(launch_pdl(radix_plan, 1, 256, 0, st, dh, n, plan, plan_hi, fix, dbase));
   count_launch(ctx, 2);
   const FixPlan* no_gate = nullptr;
-  for (int pos = 8; pos < 12; ++pos) {  // speculative: the top 32 bits only
+  // without speculation the full LSD runs ungated
+  static const int64_t spec_min = [] {
+    const char* e = std::getenv("PARS_SORT_SPEC_MIN");
+    return e ? std::atoll(e) : (int64_t)kSpecMin;
+  }();
+  const bool speculate = n >= spec_min;
+  for (int pos = 8; speculate && pos < 12; ++pos) {  // speculative: the top 32 bits only
     PARS_CUDA_CHECK(launch_pdl(radix_onesweep, (unsigned)nb, kSweepThreads, kSweepSmem, st, score, boosted, tie,
                                khi[0], khi[1], klo[0], klo[1], val[0], val[1], order, n, pos, plan_hi, dbase,
                                status + (size_t)nb * 256 * (pos - 8), tile_ctr + pos, no_gate));
     count_launch(ctx);
   }
-  PARS_CUDA_CHECK(launch_pdl(radix_fixup, (unsigned)ceil_div(n, 256), 256, 0, st, khi[0], khi[1], klo[0], klo[1],
-                             val[0], val[1], n, fix, order));
-  count_launch(ctx);
+  if (speculate) {
+    PARS_CUDA_CHECK(launch_pdl(radix_fixup, (unsigned)ceil_div(n, 256), 256, 0, st, khi[0], khi[1], klo[0],
+                               klo[1], val[0], val[1], n, fix, order));
+    count_launch(ctx);
+  }
   // the full LSD sort, gated on fix->redo; without tie ranks the tie digits
   // are all zero: those passes are known trivial on the host and not launched
   for (int pos = tie ? 0 : 4; pos < 12; ++pos) {
     PARS_CUDA_CHECK(launch_pdl(radix_onesweep, (unsigned)nb, kSweepThreads, kSweepSmem, st, score, boosted, tie,
                                khi[0], khi[1], klo[0], klo[1], val[0], val[1], order, n, pos, plan, dbase,
-                               status + (size_t)nb * 256 * (4 + pos), tile_ctr + 16 + pos, (const FixPlan*)fix));
+                               status + (size_t)nb * 256 * (4 + pos), tile_ctr + 16 + pos,
+                               speculate ? (const FixPlan*)fix : no_gate));
     count_launch(ctx);
   }
   PARS_CUDA_CHECK(cudaGetLastError());

@@ -85,11 +85,16 @@ int main(int argc, char** argv) {
   pars::SimConfig sjf;
   sjf.policy.policy =
       pars::make_sjf_policy("pars", std::make_shared<pars::LinearScorer>(model.scorer));
+  // twice: the first run also pays one-time costs (lazy module loading of
+  // the kernels it launches, buffer growth); the reported wall is the second
+  t0 = std::chrono::steady_clock::now();
+  (void)pars::run_simulation(trace, ds, sjf);
+  const double wp_first = secs_since(t0);
   t0 = std::chrono::steady_clock::now();
   const pars::SimResult rp = pars::run_simulation(trace, ds, sjf);
   const double wp = secs_since(t0);
 
-  std::printf("{\"n\": %zu, \"train_s\": %.6f, ", n, train_s);
+  std::printf("{\"n\": %zu, \"train_s\": %.6f, \"pars_first_wall_s\": %.6f, ", n, train_s, wp_first);
   report("fcfs", rf, wf, false);
   report("pars", rp, wp, true);
   std::printf("}\n");
