@@ -613,6 +613,45 @@ def test_merge_shard_orders_equals_global_order(ctx, n, runs):
     assert (got.cpu().numpy() == want.cpu().numpy()).all()
 
 
+def test_priority_order_graph_replay_follows_the_data(ctx):
+    """pars_dev_priority_order captured once as a CUDA graph (its pass plan,
+    the high-word speculation and the fallback gate are all decided on the
+    device, its kernels chained by programmatic dependent launch) and replayed
+    over new key contents: spread scores (the fixup holds), scores repeated
+    40 times (no speculation), distinct scores on four top words (the fixup
+    falls back to the full LSD) — each replay's order equal to lexsort."""
+    import torch
+    from paper_2510_03243_b200 import lib
+    n = 300_000
+    rng = np.random.default_rng(77)
+    base = rng.normal(size=n) * 0.3
+    inputs = [base,
+              rng.choice(base[: n // 40], size=n),
+              (1.0 + rng.integers(0, 2**32, size=n) * 2.0**-52) * rng.choice([1.0, 2.0, 4.0, 8.0], size=n)]
+    tie = rng.integers(0, 1000, size=n).astype(np.uint32)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        d_s = torch.from_numpy(inputs[0]).to(dev)
+        d_t = torch.from_numpy(tie.astype(np.int32)).to(dev)
+        d_o = torch.empty(n, dtype=torch.int32, device=dev)
+
+        def run():
+            assert lib().pars_dev_priority_order(ctx.h, d_s.data_ptr(), None, d_t.data_ptr(), n,
+                                                 d_o.data_ptr(), stream.cuda_stream) == 0
+        run()  # scratch sized before capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            run()
+        for s in inputs + inputs[::-1]:
+            d_s.copy_(torch.from_numpy(s).to(dev))
+            g.replay()
+            torch.cuda.synchronize()
+            want = np.lexsort((np.arange(n), tie, s))
+            assert (d_o.cpu().numpy() == want).all()
+
+
 def test_dp_train_step_replays_as_a_cuda_graph(ctx):
     """The C5 step (score, all-pairs plan tiles, X^T c, update) captured once as
     a CUDA graph and replayed trains bit-identically to launching it."""
