@@ -800,6 +800,11 @@ int launch_sgd_cluster(pars_ctx* ctx, const int64_t* rp, const uint32_t* cpk,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (kCL > 8) {
+    static const bool np = cudaFuncSetAttribute(sgd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                                1) == cudaSuccess;
+    (void)np;
+  }
   PARS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, sgd_cluster_kernel, L, ea));
 #ifdef PARS_SGD_TIMING
   {

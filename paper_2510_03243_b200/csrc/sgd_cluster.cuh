@@ -6,7 +6,10 @@
 
 namespace pars_b200 {
 
-constexpr int kSgdCluster = 8;          // CTAs (SMs) per epoch cluster
+#ifndef PARS_SGD_CLUSTER_CTAS
+#define PARS_SGD_CLUSTER_CTAS 8
+#endif
+constexpr int kSgdCluster = PARS_SGD_CLUSTER_CTAS;  // CTAs (SMs) per epoch cluster (> 8: non-portable)
 constexpr uint32_t kSgdRowCap = 10240;  // staged row entries per CTA per step
 constexpr uint32_t kSgdCscCap = 10240;  // staged CSC entries per CTA per step
 constexpr uint32_t kSgdRunCap = 1024;   // staged runs per CTA per step
