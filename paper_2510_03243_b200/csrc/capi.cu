@@ -339,10 +339,10 @@ __global__ void cpk_score_kernel(const int64_t* __restrict__ rp, const uint32_t*
     const uint32_t e[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      s = __dadd_rn(s, __dmul_rn(w[e[j] >> 16], __dmul_rn((double)((int)(e[j] & 0xffffu) - 0x8000), inv)));
+      s = __dadd_rn(s, __dmul_rn(w[e[j] >> 16], __dmul_rn(biased16_to_f64(e[j]), inv)));
   }
   for (; k < len; ++k)
-    s = __dadd_rn(s, __dmul_rn(w[row[k] >> 16], __dmul_rn((double)((int)(row[k] & 0xffffu) - 0x8000), inv)));
+    s = __dadd_rn(s, __dmul_rn(w[row[k] >> 16], __dmul_rn(biased16_to_f64(row[k]), inv)));
   out[r] = __dadd_rn(s, bias);
 }
 
@@ -423,12 +423,12 @@ __global__ void __launch_bounds__(kCpkRows) cpk_score_coop_kernel(
         const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          s = __dadd_rn(s, __dmul_rn(__ldg(w + (e[j] >> 16)), __dmul_rn((double)((int)(e[j] & 0xffffu) - 0x8000), inv)));
+          s = __dadd_rn(s, __dmul_rn(__ldg(w + (e[j] >> 16)), __dmul_rn(biased16_to_f64(e[j]), inv)));
       }
     } else {
       for (int q = 0; q < n; ++q) {
         const uint32_t e = row[q];
-        s = __dadd_rn(s, __dmul_rn(__ldg(w + (e >> 16)), __dmul_rn((double)((int)(e & 0xffffu) - 0x8000), inv)));
+        s = __dadd_rn(s, __dmul_rn(__ldg(w + (e >> 16)), __dmul_rn(biased16_to_f64(e), inv)));
       }
     }
     __syncthreads();  // the stage is refilled next iteration

@@ -58,6 +58,18 @@ __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ?
 // ---- integer divide helpers -------------------------------------------------
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// ---- exact integer -> double without I2F.F64 ---------------------------------
+// The conversion pipe is slow on this part; the bits of 2^52 + u (u < 2^32
+// in the low word) are exactly that double, so one DADD removes the bias.
+// A 16-bit count stored biased by 2^15 (compact rows: count + 0x8000):
+__device__ __forceinline__ double biased16_to_f64(uint32_t e) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)(e & 0xffffu)), 4503599627403264.0);  // 2^52 + 2^15
+}
+// any int32:
+__device__ __forceinline__ double i32_to_f64(int32_t c) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)((uint32_t)c ^ 0x80000000u)), 4503601774854144.0);  // 2^52 + 2^31
+}
+
 // ---- launch telemetry -----------------------------------------------------
 void count_launch(pars_ctx* ctx, uint64_t k = 1);
 

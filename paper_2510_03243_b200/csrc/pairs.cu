@@ -288,11 +288,11 @@ __global__ void xtc_csc_kernel(const CscTask* __restrict__ tasks, int64_t ntasks
   for (; k + 96 < e; k += 128) {  // four independent gathers in flight
     const uint32_t q0 = crow[k], q1 = crow[k + 32], q2 = crow[k + 64], q3 = crow[k + 96];
     const double v0 = cval[k], v1 = cval[k + 32], v2 = cval[k + 64], v3 = cval[k + 96];
-    const double p0 = __dmul_rn((double)c[q0], v0), p1 = __dmul_rn((double)c[q1], v1);
-    const double p2 = __dmul_rn((double)c[q2], v2), p3 = __dmul_rn((double)c[q3], v3);
+    const double p0 = __dmul_rn(i32_to_f64(c[q0]), v0), p1 = __dmul_rn(i32_to_f64(c[q1]), v1);
+    const double p2 = __dmul_rn(i32_to_f64(c[q2]), v2), p3 = __dmul_rn(i32_to_f64(c[q3]), v3);
     s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
   }
-  for (; k < e; k += 32) s = __dadd_rn(s, __dmul_rn((double)c[crow[k]], cval[k]));
+  for (; k < e; k += 32) s = __dadd_rn(s, __dmul_rn(i32_to_f64(c[crow[k]]), cval[k]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
   if (lane == 0) part[t] = s;

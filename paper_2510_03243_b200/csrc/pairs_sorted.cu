@@ -272,10 +272,10 @@ __global__ void __launch_bounds__(kT) allpairs_sorted_kernel(
         act_acc += (unsigned)cnt;
         rowcnt += cnt;
       }
-      double part = cnt ? __dmul_rn((double)cnt, __dadd_rn(si, m)) : 0.0;
+      double part = cnt ? __dmul_rn(i32_to_f64(cnt), __dadd_rn(si, m)) : 0.0;
       if (tid < jn && sC[tid]) {
         atomicSub(&cs[J0 + tid], sC[tid]);
-        part = __dsub_rn(part, __dmul_rn((double)sC[tid], sS[tid]));
+        part = __dsub_rn(part, __dmul_rn(i32_to_f64(sC[tid]), sS[tid]));
       }
       // no trailing barrier: red, sS, sSs, sTs and sC are next written
       // before a barrier that every thread reaches after this one

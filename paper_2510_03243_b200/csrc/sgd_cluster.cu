@@ -254,10 +254,7 @@ __global__ void slot_table_kernel(const uint32_t* __restrict__ pa, const uint32_
 // The entry's signed 16-bit count as a double, exactly, without an I2F.F64
 // (a slow conversion pipe on this part): the bits of 2^52 + (c + 2^15), less
 // 2^52 + 2^15, in one DADD.
-__device__ __forceinline__ double cnt_of(uint32_t E) {
-  const double biased = __hiloint2double(0x43300000, (int)(E & 0xffffu));  // the stored count is biased
-  return __dsub_rn(biased, 4503599627403264.0);  // 2^52 + 2^15
-}
+__device__ __forceinline__ double cnt_of(uint32_t E) { return biased16_to_f64(E); }
 
 __device__ __forceinline__ double chain_row_s(const uint32_t* __restrict__ rs, uint32_t len, double inv,
                                               const double* __restrict__ W) {
@@ -601,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #pragma unroll 8
           for (; e < len; ++e) {
             const uint32_t E = row[e];
-            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn((double)((int)(E & 0xffffu) - 0x8000), inv)));
+            acc = __dadd_rn(acc, __dmul_rn(W[E >> 16], __dmul_rn(cnt_of(E), inv)));
           }
         }
         score[k] = __dadd_rn(acc, a.bias);
@@ -661,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) sgd_cluster_kernel(const Layout L
 #pragma unroll 8
         for (; e < e1; ++e) {
           const uint32_t E = csc[e];
-          g = __dadd_rn(g, __dmul_rn((double)((int)(E & 0xffffu) - 0x8000), sinv[E >> 16]));
+          g = __dadd_rn(g, __dmul_rn(cnt_of(E), sinv[E >> 16]));
         }
       }
       if (g != 0.0) {
