@@ -32,8 +32,11 @@ namespace pars_b200 {
 
 namespace {
 
-constexpr int kTileT = 1024;              // threads per tile CTA
-constexpr int kTile = 2 * kTileT;         // elements per tile
+#ifndef PARS_TAU_TILE_T
+#define PARS_TAU_TILE_T 1024
+#endif
+constexpr int kTileT = PARS_TAU_TILE_T;  // threads per tile CTA
+constexpr int kTile = 2 * kTileT;        // elements per tile
 
 __device__ __forceinline__ uint64_t key_of(double v) {
   uint64_t b = (uint64_t)__double_as_longlong(v);
@@ -124,6 +127,24 @@ __global__ void tau_xrun_kernel(const uint64_t* __restrict__ kx, const uint32_t*
   add_u64(n3, t3);
 }
 
+// 32-bit forms for the shared-memory tile (runs shorter than kTile)
+__device__ __forceinline__ int lower_idx32(const uint32_t* a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] < v) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_idx32(const uint32_t* a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] <= v) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
 // step 4a: sort tiles of kTile elements in shared memory, counting the
 // inversions inside each tile
 __global__ void __launch_bounds__(kTileT) tau_tile_merge_kernel(uint32_t* __restrict__ Y, int64_t n,
@@ -142,10 +163,10 @@ __global__ void __launch_bounds__(kTileT) tau_tile_merge_kernel(uint32_t* __rest
       const int base = k & ~(2 * w - 1);
       const uint32_t v = a[k];
       if (k < base + w) {  // left run element
-        const int r = (int)lower_idx(a + base + w, w, v);
+        const int r = lower_idx32(a + base + w, w, v);
         b[k + r] = v;
       } else {             // right run element: left elements greater than v
-        const int u = (int)upper_idx(a + base, w, v);
+        const int u = upper_idx32(a + base, w, v);
         // padding (0xffffffff) sits at the end of the last tile only and is
         // never greater than a real value's left partner: count real ones
         if (k < len) inv += (unsigned long long)(w - u);
@@ -221,11 +242,10 @@ int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n
   const unsigned g256 = (unsigned)ceil_div(n, 256);
   tau_finite_kernel<<<(unsigned)std::min<int64_t>(g256, (int64_t)sms * 4), 256, 0, st>>>(
       x, y, n, reinterpret_cast<unsigned*>(aux));
-  unsigned bad = 0;
-  PARS_CUDA_CHECK(cudaMemcpyAsync(&bad, aux, 4, cudaMemcpyDeviceToHost, st));
-  PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  // the flag is read with the counts at the end (one synchronisation per
+  // call): the sorts and searches below are safe on any bit patterns, their
+  // counts are only meaningless when a value is not finite
   count_launch(ctx);
-  if (bad) return PARS_ERR_UNSUPPORTED;
   // 1. y order and y-run ranks
   PARS_TRY(launch_priority_sort(ctx, y, nullptr, nullptr, n, oy, sort_scr, st));
   tau_yrank_kernel<<<g256, 256, 0, st>>>(y, oy, n, k64);
@@ -249,6 +269,7 @@ int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n
   unsigned long long a[6];
   PARS_CUDA_CHECK(cudaMemcpyAsync(a, aux, sizeof a, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
+  if ((unsigned)a[0]) return PARS_ERR_UNSUPPORTED;
   const uint64_t n0 = (uint64_t)n * (uint64_t)(n - 1) / 2;
   counts4[1] = a[3];
   counts4[2] = a[4];
