@@ -141,6 +141,12 @@ struct pars_ctx {
   // a serving loop that scores with unchanged weights skips the upload
   std::vector<double> w_shadow;
   bool w64_valid = false, w32_valid = false;
+  // the sorted Kendall tau's ~30 dependent launches as one CUDA graph,
+  // re-instantiated when its inputs, size or scratch change
+  cudaGraphExec_t tau_exec = nullptr;
+  const void* tau_key[3] = {nullptr, nullptr, nullptr};
+  int64_t tau_key_n = -1;
+  uint64_t tau_launches = 0;
 };
 
 struct pars_features {
@@ -634,6 +640,7 @@ void pars_ctx_destroy(pars_ctx* c) {
   for (HostBuf* b : {&c->h_offs[0], &c->h_offs[1], &c->h_scores, &c->h_text[0], &c->h_text[1]})
     if (b->p) cudaFreeHost(b->p);
   c->pool.reset();
+  if (c->tau_exec) cudaGraphExecDestroy(c->tau_exec);
   for (cudaEvent_t e : c->ev_chunk) cudaEventDestroy(e);
   if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
   for (int k = 0; k < 2; ++k) {
@@ -2053,6 +2060,49 @@ int pars_dev_merge_orders(pars_ctx* ctx, const double* d_scores, const uint8_t* 
 namespace pars_b200 {
 namespace capi_detail {
 
+// The sorted counts' device steps replayed from a CUDA graph captured on
+// the first call with these inputs and scratch (launch gaps of ~30 dependent
+// kernels are most of the call at n <= 10^5), then the one read-back.
+int tau_sorted_graph(pars_ctx* ctx, const double* d_x, const double* d_y, int64_t n, uint64_t* c4,
+                     cudaStream_t st) {
+  void* scr = ctx->tau.p;
+  if (!ctx->tau_exec || ctx->tau_key[0] != d_x || ctx->tau_key[1] != d_y ||
+      ctx->tau_key[2] != scr || ctx->tau_key_n != n) {
+    if (ctx->tau_exec) cudaGraphExecDestroy(ctx->tau_exec);
+    ctx->tau_exec = nullptr;
+    ctx->tau_key_n = -1;
+    const uint64_t before = ctx->launches.load();
+    PARS_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_tau_sorted(ctx, d_x, d_y, n, scr, st);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (rc != PARS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) {
+      set_error("kendall_tau_b: graph capture failed: %s", cudaGetErrorString(ce));
+      return PARS_ERR_CUDA;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&ctx->tau_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      ctx->tau_exec = nullptr;
+      set_error("kendall_tau_b: graph instantiation failed: %s", cudaGetErrorString(ie));
+      return PARS_ERR_CUDA;
+    }
+    ctx->tau_launches = ctx->launches.load() - before;  // counted at replay
+    ctx->launches.fetch_sub(ctx->tau_launches);
+    ctx->tau_key[0] = d_x;
+    ctx->tau_key[1] = d_y;
+    ctx->tau_key[2] = scr;
+    ctx->tau_key_n = n;
+  }
+  PARS_CUDA_CHECK(cudaGraphLaunch(ctx->tau_exec, st));
+  count_launch(ctx, ctx->tau_launches);
+  return finish_tau_sorted(n, c4, scr, st);
+}
+
 // tau-b of device arrays on `st`: the O(n log n) sorted counts (tau_sorted.cu)
 // unless an input is non-finite (or algo asks for it), else the all-pairs
 // tiles (pairs.cu). Both give the reference's exact integers.
@@ -2070,7 +2120,8 @@ int kendall_dev_impl(pars_ctx* ctx, const double* d_x, const double* d_y, int64_
   int rc = PARS_ERR_UNSUPPORTED;
   if (algo != PARS_TAU_PAIRS) {
     PARS_TRY(ensure(ctx->tau, tau_sorted_scratch_bytes(n) + 4096));
-    rc = launch_tau_sorted(ctx, d_x, d_y, n, c4, ctx->tau.p, st);
+    rc = capturing(st) ? launch_tau_sorted(ctx, d_x, d_y, n, c4, ctx->tau.p, st)
+                       : tau_sorted_graph(ctx, d_x, d_y, n, c4, st);
     if (rc != PARS_OK && rc != PARS_ERR_UNSUPPORTED) return rc;
     if (rc == PARS_ERR_UNSUPPORTED && algo == PARS_TAU_SORTED) {
       set_error("kendall_tau_b: the sorted algorithm needs finite inputs");

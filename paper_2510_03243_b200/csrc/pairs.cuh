@@ -99,6 +99,11 @@ int launch_merge_runs(pars_ctx* ctx, const double* score, const uint8_t* boosted
 size_t tau_sorted_scratch_bytes(int64_t n);
 int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n,
                       uint64_t* counts4, void* scratch, cudaStream_t st);
+// the same as two halves: every device step on `st` (no host synchronisation,
+// capturable into a CUDA graph), then the read-back and finish
+int enqueue_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n, void* scratch,
+                       cudaStream_t st);
+int finish_tau_sorted(int64_t n, uint64_t* counts4, void* scratch, cudaStream_t st);
 
 // PointwiseL1 / ListMLE epochs (baselines.cu). kind 0 = pointwise, 1 = ListMLE.
 size_t baseline_smem_bytes(uint32_t dim, int64_t max_slots);

@@ -204,7 +204,7 @@ __global__ void tau_merge_level_kernel(const uint32_t* __restrict__ a, uint32_t*
 }  // namespace
 
 size_t tau_sorted_scratch_bytes(int64_t n) {
-  size_t b = sort_scratch_bytes(n) + 1024;
+  size_t b = 256 + sort_scratch_bytes(n) + 1024;  // counts block first
   b += 2 * ((size_t)n * 4 + 256);  // oy, o
   b += (size_t)n * 8 + 256;        // kys / kx
   b += 3 * ((size_t)n * 4 + 256);  // ry, Y ping-pong
@@ -214,13 +214,27 @@ size_t tau_sorted_scratch_bytes(int64_t n) {
 
 // counts4 (host) receives {n_c, n_d, n1, n2}; synchronises `st`. Returns
 // PARS_ERR_UNSUPPORTED (nothing written) when x or y holds a non-finite value.
+namespace {
+// the counts block sits at the front of the scratch (its place does not
+// depend on n, so the read-back needs only the scratch pointer)
+unsigned long long* tau_aux(void* scratch) { return static_cast<unsigned long long*>(scratch); }
+}  // namespace
+
 int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n,
                       uint64_t* counts4, void* scratch, cudaStream_t st) {
+  PARS_TRY(enqueue_tau_sorted(ctx, x, y, n, scratch, st));
+  return finish_tau_sorted(n, counts4, scratch, st);
+}
+
+int enqueue_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n, void* scratch,
+                       cudaStream_t st) {
   if (n > 0x7fffffffLL) {
     set_error("kendall_tau_b: n=%lld exceeds 2^31-1", (long long)n);
     return PARS_ERR_UNSUPPORTED;
   }
-  char* p = static_cast<char*>(scratch);
+  // aux: [0] non-finite flag, [1] n3, [2..5] {n_c, n_d, n1, n2}
+  unsigned long long* aux = tau_aux(scratch);
+  char* p = static_cast<char*>(scratch) + 256;
   auto take = [&](size_t bytes) {
     char* r = p;
     p += (bytes + 255) & ~(size_t)255;
@@ -232,8 +246,6 @@ int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n
   uint64_t* k64 = (uint64_t*)take((size_t)n * 8);
   uint32_t* ry = (uint32_t*)take((size_t)n * 4);
   uint32_t* Y[2] = {(uint32_t*)take((size_t)n * 4), (uint32_t*)take((size_t)n * 4)};
-  // aux: [0] non-finite flag, [1] n3, [2..5] {n_c, n_d, n1, n2}
-  unsigned long long* aux = (unsigned long long*)take(64);
   unsigned long long* dc = aux + 2;
   PARS_CUDA_CHECK(cudaMemsetAsync(aux, 0, 64, st));
   int dev = 0, sms = 148;
@@ -265,9 +277,13 @@ int launch_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t n
   }
   count_launch(ctx, 5);
   PARS_CUDA_CHECK(cudaGetLastError());
+  return PARS_OK;
+}
+
+int finish_tau_sorted(int64_t n, uint64_t* counts4, void* scratch, cudaStream_t st) {
   // n_c = n0 - n1 - n2 + n3 - n_d, on the host after one read
   unsigned long long a[6];
-  PARS_CUDA_CHECK(cudaMemcpyAsync(a, aux, sizeof a, cudaMemcpyDeviceToHost, st));
+  PARS_CUDA_CHECK(cudaMemcpyAsync(a, tau_aux(scratch), sizeof a, cudaMemcpyDeviceToHost, st));
   PARS_CUDA_CHECK(cudaStreamSynchronize(st));
   if ((unsigned)a[0]) return PARS_ERR_UNSUPPORTED;
   const uint64_t n0 = (uint64_t)n * (uint64_t)(n - 1) / 2;

@@ -229,6 +229,36 @@ def test_kendall_sorted_counts_exact(ctx, oracle, n):
         assert c.tolist() == oc.tolist() and tau == otau
 
 
+def test_kendall_sorted_graph_replay_and_recapture(ctx, oracle):
+    """The sorted counts run as a CUDA graph cached on (inputs, n, scratch):
+    new contents of the same device buffers replay it, a shorter n on the
+    same pointers and a non-finite value (the tile path) re-check it; every
+    call against the reference's all-pairs integers."""
+    import torch
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(77)
+    n = 5000
+    dx = torch.empty(n, dtype=torch.float64, device=dev)
+    dy = torch.empty(n, dtype=torch.float64, device=dev)
+    cases = [(rng.normal(size=n), rng.integers(0, 40, n).astype(float), n),
+             (rng.integers(0, 9, n).astype(float), rng.normal(size=n), n),
+             (rng.normal(size=n), rng.normal(size=n).round(1), 2049),
+             (rng.normal(size=n), rng.integers(0, 40, n).astype(float), n)]
+    for x, y, m in cases:
+        dx.copy_(torch.from_numpy(x))
+        dy.copy_(torch.from_numpy(y))
+        torch.cuda.synchronize()
+        tau, c = ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), m)
+        otau, oc = oracle.kendall(x[:m], y[:m], threads=os.cpu_count() or 1)
+        assert [int(v) for v in c] == oc.tolist() and tau == otau
+    x[3] = np.inf
+    dx.copy_(torch.from_numpy(x))
+    torch.cuda.synchronize()
+    tau, c = ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), n)
+    otau, oc = oracle.kendall(x, y, threads=os.cpu_count() or 1)
+    assert [int(v) for v in c] == oc.tolist() and tau == otau
+
+
 def test_kendall_non_finite_falls_back_to_pairs(ctx, oracle):
     """inf - inf = NaN is neither a tie nor negative in the reference, so the
     sorted method does not apply: auto runs the all-pairs tiles."""

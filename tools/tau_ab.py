@@ -41,6 +41,16 @@ tau, c = r
 tp, cp = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
 out["tau_b"] = tau
 out["counts_equal_pairs_path"] = [int(v) for v in c] == [int(v) for v in cp]
+# graph replay over new contents of the same buffers, then a shorter n on
+# the same pointers (re-capture): counts against the tile path each time
+dx.copy_(torch.from_numpy(rng.normal(size=n)).to(dev))
+t1, c1 = ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), n, stream=sh)
+t2, c2 = D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh)
+out["replay_new_contents_equal"] = [int(v) for v in c1] == [int(v) for v in c2]
+h = n // 2 + 1
+t1, c1 = ctx.dev_kendall_tau(dx.data_ptr(), dy.data_ptr(), h, stream=sh)
+t2, c2 = D.kendall_tau_gpu(ctx, dx[:h].contiguous(), dy[:h].contiguous(), h, stream=sh)
+out["recapture_shorter_equal"] = [int(v) for v in c1] == [int(v) for v in c2]
 # non-finite inputs: the sorted path must step aside (same counts as tiles)
 xn = x.copy()
 xn[n // 3] = np.inf
