@@ -871,7 +871,7 @@ def bench_tau(P, ctx, torch, dev, stream, world, rank, args, dp=None):
         ms_pairs, (tau_p, c_p) = timed(lambda: D.kendall_tau_gpu(ctx, dx, dy, n, stream=sh))
     pairs = n * (n - 1) // 2
     out = {"metric": "pairs/s", "value": pairs / (ms / 1e3), "ms_per_call": ms, "tau_b": tau,
-           "algorithm": "sorted counts (two radix sorts + merge inversion count), exact",
+           "algorithm": "sorted counts (two radix sorts + merge inversion count, replayed as one CUDA graph), exact",
            "roofline": {"bound": "latency", "floor_bytes": 16 * n + 32,
                         "bytes_model": "one-pass I/O floor: x and y (8 B each) read once, 4 counts written",
                         "achieved": (16 * n + 32) / (ms / 1e3) / 1e9, "peak": peaks()[0], "unit": "GB/s",
