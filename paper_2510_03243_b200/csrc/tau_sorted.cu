@@ -36,7 +36,10 @@ namespace {
 #define PARS_TAU_TILE_T 1024
 #endif
 constexpr int kTileT = PARS_TAU_TILE_T;  // threads per tile CTA
-constexpr int kTile = 2 * kTileT;        // elements per tile
+#ifndef PARS_TAU_TILE_PER_T
+#define PARS_TAU_TILE_PER_T 2
+#endif
+constexpr int kTile = PARS_TAU_TILE_PER_T * kTileT;  // elements per tile
 
 __device__ __forceinline__ uint64_t key_of(double v) {
   uint64_t b = (uint64_t)__double_as_longlong(v);
