@@ -74,20 +74,22 @@ __device__ __forceinline__ int64_t upper_idx(const T* a, int64_t n, T v) {
   return lo;
 }
 
-__global__ void tau_finite_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                  int64_t n, unsigned* __restrict__ bad) {
-  bool b = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    b |= !isfinite(x[i]) || !isfinite(y[i]);
+// step 1: ky sorted by the y order; ry[i] = start of y_i's run; n2
+// (oy and o are permutations, so these two gathers see every y and every x
+// once: they also raise the non-finite flag)
+__device__ __forceinline__ void flag_nonfinite(bool b, unsigned* bad) {
   if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
-
-// step 1: ky sorted by the y order; ry[i] = start of y_i's run; n2
 __global__ void tau_yrank_kernel(const double* __restrict__ y, const uint32_t* __restrict__ oy,
-                                 int64_t n, uint64_t* __restrict__ kys) {
+                                 int64_t n, uint64_t* __restrict__ kys, unsigned* __restrict__ bad) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) kys[k] = key_of(y[oy[k]]);
+  bool b = false;
+  if (k < n) {
+    const double v = y[oy[k]];
+    kys[k] = key_of(v);
+    b = !isfinite(v);
+  }
+  flag_nonfinite(b, bad);
 }
 __global__ void tau_yrun_kernel(const uint64_t* __restrict__ kys, const uint32_t* __restrict__ oy,
                                 int64_t n, uint32_t* __restrict__ ry,
@@ -105,13 +107,18 @@ __global__ void tau_yrun_kernel(const uint64_t* __restrict__ kys, const uint32_t
 // steps 2-3: X / Y in (x, ry) order; n1 and n3 (pairs tied in both)
 __global__ void tau_gather_kernel(const double* __restrict__ x, const uint32_t* __restrict__ ry,
                                   const uint32_t* __restrict__ o, int64_t n,
-                                  uint64_t* __restrict__ kx, uint32_t* __restrict__ Y) {
+                                  uint64_t* __restrict__ kx, uint32_t* __restrict__ Y,
+                                  unsigned* __restrict__ bad) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool b = false;
   if (k < n) {
     const uint32_t i = o[k];
-    kx[k] = key_of(x[i]);
+    const double v = x[i];
+    kx[k] = key_of(v);
     Y[k] = ry[i];
+    b = !isfinite(v);
   }
+  flag_nonfinite(b, bad);
 }
 __global__ void tau_xrun_kernel(const uint64_t* __restrict__ kx, const uint32_t* __restrict__ Y,
                                 int64_t n, unsigned long long* __restrict__ counts,
@@ -251,24 +258,18 @@ int enqueue_tau_sorted(pars_ctx* ctx, const double* x, const double* y, int64_t 
   uint32_t* Y[2] = {(uint32_t*)take((size_t)n * 4), (uint32_t*)take((size_t)n * 4)};
   unsigned long long* dc = aux + 2;
   PARS_CUDA_CHECK(cudaMemsetAsync(aux, 0, 64, st));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned g256 = (unsigned)ceil_div(n, 256);
-  tau_finite_kernel<<<(unsigned)std::min<int64_t>(g256, (int64_t)sms * 4), 256, 0, st>>>(
-      x, y, n, reinterpret_cast<unsigned*>(aux));
-  // the flag is read with the counts at the end (one synchronisation per
-  // call): the sorts and searches below are safe on any bit patterns, their
-  // counts are only meaningless when a value is not finite
-  count_launch(ctx);
+  // the non-finite flag is raised by the two gathers below and read with the
+  // counts at the end (one synchronisation per call): the sorts and searches
+  // are safe on any bit patterns, their counts only meaningless then
   // 1. y order and y-run ranks
   PARS_TRY(launch_priority_sort(ctx, y, nullptr, nullptr, n, oy, sort_scr, st));
-  tau_yrank_kernel<<<g256, 256, 0, st>>>(y, oy, n, k64);
+  tau_yrank_kernel<<<g256, 256, 0, st>>>(y, oy, n, k64, reinterpret_cast<unsigned*>(aux));
   tau_yrun_kernel<<<g256, 256, 0, st>>>(k64, oy, n, ry, dc);
   // 2. (x, ry) order
   PARS_TRY(launch_priority_sort(ctx, x, nullptr, ry, n, o, sort_scr, st));
   // 3. n1, n3
-  tau_gather_kernel<<<g256, 256, 0, st>>>(x, ry, o, n, k64, Y[0]);
+  tau_gather_kernel<<<g256, 256, 0, st>>>(x, ry, o, n, k64, Y[0], reinterpret_cast<unsigned*>(aux));
   tau_xrun_kernel<<<g256, 256, 0, st>>>(k64, Y[0], n, dc, aux + 1);
   // 4. inversions of Y = n_d
   tau_tile_merge_kernel<<<(unsigned)ceil_div(n, kTile), kTileT, 0, st>>>(Y[0], n, dc + 1);
